@@ -1,0 +1,153 @@
+/*
+ * sgb200.h — C ABI of the B200-native Dolphin probabilistic hot path.
+ *
+ * Every entry point:
+ *   - returns 0 on success or a cudaError_t value (never throws across the ABI);
+ *   - takes CALLER-ALLOCATED DEVICE buffers (the PyTorch caching allocator owns them);
+ *   - enqueues work on the given cudaStream_t and never synchronises the host;
+ *   - has no global mutable state (re-entrant; use distinct streams per thread);
+ *   - has no CPU fallback: if the device code is missing the call fails.
+ *
+ * Tag layouts in HBM (symbol-major, batch innermost, so lane == sample is coalesced):
+ *   DAMP tags      float    [rows][B]
+ *   DTKP members   uint64   [rows][K][W][B]   bit j of word w = input column 64*w + j
+ *   DTKP present   uint8    [rows][K][B]
+ *   registry probs float    [I][B]
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src/symgrad/):
+ *   sg_damp_apply_fwd   provenance.py:233 gather + :236 conj fold + :242-253 group_disj
+ *                       (distribution.py:262-270 tag work of apply_if)
+ *   sg_damp_apply_bwd   tensor.py:287 clamp bw, :415 affine bw, :240 mul bw, :386-391 select_rows bw
+ *   sg_segsum_run       provenance.py:242-253 Damp.group_disj (and select_rows bw scatter-add)
+ *   sg_damp_rows_add    provenance.py:239-240 Damp.disj; distribution.py:279-297 union
+ *   sg_rows_gather      provenance.py:233-234 / :320-326 gather (filter, distribution.py:158-169)
+ *   sg_to_symbol_major  provenance.py:223-225 Damp.input_tags (layout + fp32 cast of the block)
+ *   sg_dtkp_apply       provenance.py:328-341 conj, :343-350 disj, :352-364 group_disj,
+ *                       :366-379 _normalize (fused streaming top-k, bit-exact ranking)
+ *   sg_dtkp_probs_fwd   provenance.py:398-413 DtkpAm.probs / :415-423 forward_probs
+ *   sg_dtkp_probs_bwd   tensor.py:302-318 reduce_prod leave-one-out bw (+ clamp/sum/mul bw)
+ *   sg_dedup_topk       _dtkpcore.pyx:17-96 dedup_topk (kernels.py:29-42 dispatch) — same
+ *                       argument meaning, byte layout and ordering semantics
+ */
+#ifndef SGB200_H
+#define SGB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* sg_stream_t; /* == cudaStream_t */
+
+#define SG_MAX_ARITY 8
+
+/* One segmented sum-of-products problem:
+ *   out[seg][b] = (clamp?)  sum_{rec in seg}  prod_{i < n_ops}  op_i[ recs[rec][i] ][b]
+ * Segments are cut into items of bounded length; a segment cut into several items
+ * writes partial rows into `scratch` and is finished by a deterministic fix-up pass. */
+typedef struct sg_segsum {
+  int32_t n_seg;      /* output rows                                            */
+  int32_t rec_words;  /* int32 words per record: 1, 2, 4 or 8 (>= n_ops)         */
+  int32_t n_items;    /* work items                                             */
+  int32_t n_blocks;   /* CTA chunks along grid.y                                */
+  int32_t n_split;    /* segments spread over more than one item                */
+  int32_t n_partial;  /* partial rows needed in scratch ([n_partial][B] floats)  */
+  int32_t staged;     /* 1: stage operand tiles in shared memory                */
+  int32_t pad_;
+  const int32_t* recs;  /* [n_recs][rec_words]                                  */
+  const int32_t* items; /* [n_items][4] = seg, rec_begin, rec_end, dest (-1 = direct) */
+  const int32_t* blk;   /* [n_blocks + 1] item range of each CTA chunk            */
+  const int32_t* split; /* [n_split][3] = seg, partial_begin, partial_end          */
+} sg_segsum;
+
+/* A memoised apply plan (host-built from the black-box symbol function). */
+typedef struct sg_damp_plan {
+  int32_t arity;
+  int32_t n_out;
+  int32_t sizes[SG_MAX_ARITY];
+  int32_t conv;        /* 1 when arity == 2 and T[s0][s1] == s0 + s1 (Toeplitz table)  */
+  int32_t conv_short;  /* which input (0/1) is the short "filter" side                  */
+  sg_segsum fwd;              /* segments = output symbols, records = input positions   */
+  sg_segsum bwd[SG_MAX_ARITY];/* segments = positions of input k, records = (T[c], s_j!=k) */
+} sg_damp_plan;
+
+int sg_version(void);
+int sg_device_sm_count(int device);
+
+/* ---- layout: user (B, n) block  <->  symbol-major [n][B] fp32 ----------------------
+ * dtype codes: 0 = float32, 1 = float64, 2 = float16, 3 = bfloat16 (strides in elements) */
+int sg_to_symbol_major(const void* src, int32_t src_dtype, int64_t B, int64_t n,
+                       int64_t stride_b, int64_t stride_n, float* dst, sg_stream_t stream);
+int sg_from_symbol_major(const float* src, int64_t B, int64_t n, void* dst, int32_t dst_dtype,
+                         int64_t stride_b, int64_t stride_n, sg_stream_t stream);
+
+/* ---- DAMP (add-mult) --------------------------------------------------------------- */
+int sg_segsum_run(const sg_segsum* prob, const float* const* ops, const int32_t* op_rows,
+                  int32_t n_ops, int64_t B, int32_t clamp01, float* out, float* scratch,
+                  sg_stream_t stream);
+int sg_damp_apply_fwd(const sg_damp_plan* plan, const float* const* inputs, int64_t B,
+                      float* out, float* scratch, sg_stream_t stream);
+int sg_damp_apply_bwd(const sg_damp_plan* plan, const float* const* inputs,
+                      const float* grad_out, int64_t B, float* const* grad_in,
+                      float* scratch, sg_stream_t stream);
+/* out[r][b] = clamp01(A[ia[r]][b] + Bm[ib[r]][b]); index -1 contributes 0. */
+int sg_damp_rows_add(const float* A, const int32_t* ia, const float* Bm, const int32_t* ib,
+                     int64_t n_rows, int64_t B, int32_t clamp01, float* out, sg_stream_t stream);
+
+/* ---- row gather (filter / placement / inverse scatter), any tag kind -----------------
+ * dst row r = src row idx[r] (idx -1 -> zero row); rows are row_bytes contiguous bytes. */
+int sg_rows_gather(const void* src, const int32_t* idx, int64_t n_rows, int64_t row_bytes,
+                   void* dst, sg_stream_t stream);
+
+/* ---- DTKP-AM (top-k proofs) --------------------------------------------------------- */
+typedef struct sg_dtkp_operand {
+  const uint64_t* member; /* [rows][K][W][B] */
+  const uint8_t* present; /* [rows][K][B]    */
+  int32_t rows;
+  int32_t W;              /* words stored for this operand (<= W_out; missing words are 0) */
+} sg_dtkp_operand;
+
+typedef struct sg_dtkp_apply_desc {
+  int32_t arity;          /* number of conjoined inputs (1 = group_disj / union / merge)    */
+  int32_t K;              /* proofs kept per tag                                            */
+  int32_t W;              /* output words = ceil(I / 64)                                    */
+  int32_t I;              /* registry width (columns of p)                                  */
+  int64_t B;
+  sg_dtkp_operand ops[SG_MAX_ARITY];
+  sg_dtkp_operand op_tail;  /* arity == 1 only: record r >= ops[0].rows reads op_tail row r - ops[0].rows */
+  const float* p;          /* registry probabilities [I][B] (fp32; ranking keys are fp64 of these) */
+  sg_segsum seg;           /* segments = output symbols; records = input positions           */
+  uint64_t* out_member;    /* [seg.n_seg][K][W][B] */
+  uint8_t* out_present;    /* [seg.n_seg][K][B]    */
+  uint64_t* scratch_member;/* [seg.n_partial][K][W][B] partial top-k of split segments      */
+  uint8_t* scratch_present;/* [seg.n_partial][K][B] */
+  sg_segsum merge;         /* arity-1 merge of partial rows (seg.n_split segments)           */
+} sg_dtkp_apply_desc;
+
+int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream);
+
+/* P[n][b] = clamp01( sum_r present * prod_{j in row r} p[j][b] )  (fp64 inside, fp32 out) */
+int sg_dtkp_probs_fwd(const uint64_t* member, const uint8_t* present, int32_t N, int32_t K,
+                      int32_t W, const float* p, int32_t I, int64_t B, float* out,
+                      sg_stream_t stream);
+/* dp[j][b] = sum_{n,r: j in row} g[n][b] * present * prod_{j' != j} p[j'][b] (exact zeros rule).
+ * scratch: >= sg_dtkp_probs_bwd_scratch(N, I, B) bytes. */
+int64_t sg_dtkp_probs_bwd_scratch(int32_t N, int32_t I, int64_t B);
+int sg_dtkp_probs_bwd(const uint64_t* member, const uint8_t* present, int32_t N, int32_t K,
+                      int32_t W, const float* p, int32_t I, int64_t B, const float* grad_out,
+                      float* grad_p, void* scratch, sg_stream_t stream);
+
+/* Drop-in for _dtkpcore.dedup_topk (device buffers, caller-allocated outputs):
+ *   member u8 [M][R][I], present u8 [M][R], p f64 [M][I]  ->
+ *   out_member u8 [M][k][I], out_present u8 [M][k]
+ * Dedup identical present rows (first wins), rank by fp64 product of p over member
+ * columns in ascending column order, ties by row index, copy source bytes. */
+int sg_dedup_topk(const uint8_t* member, const uint8_t* present, const double* p, int64_t M,
+                  int32_t R, int32_t I, int32_t k, uint8_t* out_member, uint8_t* out_present,
+                  sg_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGB200_H */

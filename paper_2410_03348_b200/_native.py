@@ -1,0 +1,171 @@
+"""ctypes binding of the sm_100a C-ABI library ``libsgb200.so`` (see include/sgb200.h).
+
+The library is loaded from the package directory (built in-tree by ``_build.py``).  There
+is no fallback: if the library is missing or a call returns a CUDA error, a
+``NativeError`` is raised.  All buffers passed in are device tensors owned by PyTorch's
+caching allocator; work is enqueued on the current torch stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, Structure, c_double, c_int32, c_int64, c_void_p
+from pathlib import Path
+
+import torch
+
+MAX_ARITY = 8
+LIB_PATH = Path(__file__).resolve().parent / "libsgb200.so"
+
+
+class NativeError(RuntimeError):
+    """The CUDA library is missing or a kernel launch failed."""
+
+
+class SgSegsum(Structure):
+    _fields_ = [
+        ("n_seg", c_int32),
+        ("rec_words", c_int32),
+        ("n_items", c_int32),
+        ("n_blocks", c_int32),
+        ("n_split", c_int32),
+        ("n_partial", c_int32),
+        ("staged", c_int32),
+        ("pad_", c_int32),
+        ("recs", c_void_p),
+        ("items", c_void_p),
+        ("blk", c_void_p),
+        ("split", c_void_p),
+    ]
+
+
+class SgDampPlan(Structure):
+    _fields_ = [
+        ("arity", c_int32),
+        ("n_out", c_int32),
+        ("sizes", c_int32 * MAX_ARITY),
+        ("conv", c_int32),
+        ("conv_short", c_int32),
+        ("fwd", SgSegsum),
+        ("bwd", SgSegsum * MAX_ARITY),
+    ]
+
+
+class SgDtkpOperand(Structure):
+    _fields_ = [
+        ("member", c_void_p),
+        ("present", c_void_p),
+        ("rows", c_int32),
+        ("W", c_int32),
+    ]
+
+
+class SgDtkpApplyDesc(Structure):
+    _fields_ = [
+        ("arity", c_int32),
+        ("K", c_int32),
+        ("W", c_int32),
+        ("I", c_int32),
+        ("B", c_int64),
+        ("ops", SgDtkpOperand * MAX_ARITY),
+        ("op_tail", SgDtkpOperand),
+        ("p", c_void_p),
+        ("seg", SgSegsum),
+        ("out_member", c_void_p),
+        ("out_present", c_void_p),
+        ("scratch_member", c_void_p),
+        ("scratch_present", c_void_p),
+        ("merge", SgSegsum),
+    ]
+
+
+# (name, restype, argtypes) of every exported entry point in include/sgb200.h
+EXPORTS = {
+    "sg_version": (c_int32, []),
+    "sg_device_sm_count": (c_int32, [c_int32]),
+    "sg_to_symbol_major": (c_int32, [c_void_p, c_int32, c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p]),
+    "sg_from_symbol_major": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_int32, c_int64, c_int64, c_void_p]),
+    "sg_segsum_run": (
+        c_int32,
+        [POINTER(SgSegsum), POINTER(c_void_p), POINTER(c_int32), c_int32, c_int64, c_int32, c_void_p, c_void_p, c_void_p],
+    ),
+    "sg_damp_apply_fwd": (c_int32, [POINTER(SgDampPlan), POINTER(c_void_p), c_int64, c_void_p, c_void_p, c_void_p]),
+    "sg_damp_apply_bwd": (
+        c_int32,
+        [POINTER(SgDampPlan), POINTER(c_void_p), c_void_p, c_int64, POINTER(c_void_p), c_void_p, c_void_p],
+    ),
+    "sg_damp_rows_add": (
+        c_int32,
+        [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p],
+    ),
+    "sg_rows_gather": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
+    "sg_dtkp_apply": (c_int32, [POINTER(SgDtkpApplyDesc), c_void_p]),
+    "sg_dtkp_probs_fwd": (
+        c_int32,
+        [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32, c_int64, c_void_p, c_void_p],
+    ),
+    "sg_dtkp_probs_bwd_scratch": (c_int64, [c_int32, c_int32, c_int64]),
+    "sg_dtkp_probs_bwd": (
+        c_int32,
+        [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_void_p,
+         c_void_p],
+    ),
+    "sg_dedup_topk": (
+        c_int32,
+        [c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p],
+    ),
+}
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load (once) and return the library; raises NativeError when it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise NativeError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2410_03348_b200._build` "
+            "(there is no CPU fallback for the probabilistic hot path)"
+        )
+    lib = ctypes.CDLL(str(LIB_PATH), mode=os.RTLD_LOCAL | getattr(os, "RTLD_NOW", 2))
+    for name, (res, args) in EXPORTS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+_CUDA_ERR = {1: "cudaErrorInvalidValue", 2: "cudaErrorMemoryAllocation", 98: "cudaErrorInvalidDeviceFunction",
+             209: "cudaErrorNoKernelImageForDevice", 801: "cudaErrorNotSupported"}
+
+
+def check(rc: int, what: str):
+    if rc != 0:
+        raise NativeError(f"{what} failed with CUDA error {rc} ({_CUDA_ERR.get(rc, 'see cudaError_t')})")
+
+
+def stream_ptr(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def ptr_array(tensors) -> ctypes.Array:
+    arr = (c_void_p * MAX_ARITY)()
+    for i, t in enumerate(tensors):
+        arr[i] = None if t is None else t.data_ptr()
+    return arr
+
+
+DTYPE_CODE = {torch.float32: 0, torch.float64: 1, torch.float16: 2, torch.bfloat16: 3}
+
+
+def require_cuda(t: torch.Tensor, what: str = "tensor"):
+    if not t.is_cuda:
+        raise NativeError(f"{what} must live on a CUDA device (the hot path has no CPU implementation)")

@@ -1,0 +1,54 @@
+// Shared helpers for the sm_100a kernels of the Dolphin hot path.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include "../../include/sgb200.h"
+
+#define SG_RETURN_IF(cond, err) \
+  do {                          \
+    if (cond) return (int)(err); \
+  } while (0)
+
+#define SG_LAUNCH_CHECK()                      \
+  do {                                         \
+    cudaError_t e__ = cudaGetLastError();      \
+    if (e__ != cudaSuccess) return (int)e__;   \
+  } while (0)
+
+namespace sg {
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ float clamp01(float x) { return fminf(fmaxf(x, 0.0f), 1.0f); }
+
+// Load one record of RW int32 words (RW in {1,2,4,8}); the address is warp-uniform.
+template <int RW>
+struct Rec {
+  int v[RW];
+};
+
+template <int RW>
+__device__ __forceinline__ Rec<RW> load_rec(const int32_t* __restrict__ p) {
+  Rec<RW> r;
+  if constexpr (RW == 1) {
+    r.v[0] = __ldg(p);
+  } else if constexpr (RW == 2) {
+    int2 t = __ldg(reinterpret_cast<const int2*>(p));
+    r.v[0] = t.x; r.v[1] = t.y;
+  } else if constexpr (RW == 4) {
+    int4 t = __ldg(reinterpret_cast<const int4*>(p));
+    r.v[0] = t.x; r.v[1] = t.y; r.v[2] = t.z; r.v[3] = t.w;
+  } else {
+    int4 t = __ldg(reinterpret_cast<const int4*>(p));
+    int4 u = __ldg(reinterpret_cast<const int4*>(p) + 1);
+    r.v[0] = t.x; r.v[1] = t.y; r.v[2] = t.z; r.v[3] = t.w;
+    r.v[4] = u.x; r.v[5] = u.y; r.v[6] = u.z; r.v[7] = u.w;
+  }
+  return r;
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace sg

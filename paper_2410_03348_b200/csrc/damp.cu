@@ -1,0 +1,556 @@
+// DAMP (add-mult) apply kernels for sm_100a.
+//
+// K1 forward  out[o][b]  = clamp01( sum_{c in seg(o)} prod_i p_i[s_i(c)][b] )
+//      reference: distribution.py:262-270 -> provenance.py:233 gather, :236 conj (T.mul),
+//                 :242-253 group_disj (dense 0/1 matmul + clamp)
+// K2 backward dp_k[s][b] = sum_{c: s_k(c)=s} g[T[c]][b] * prod_{j!=k} p_j[s_j(c)][b]
+//      reference: tensor.py:287 (clamp bw = identity), :415 (affine bw g @ G.T),
+//                 :240 (mul bw), :386-391 (select_rows bw np.add.at)
+//
+// Both are one "segmented sum of products" over memoised int32 records.  Layout is
+// symbol-major [rows][B]: lane == sample, so every operand row read by a warp is one
+// coalesced 128-byte line, index records are warp-uniform, and each output segment is
+// accumulated in a register (no atomics, no shared-memory read-modify-write).
+//
+// Toeplitz fast path (T[s0][s1] == s0 + s1, e.g. every Sum-N fold step): the short
+// input lives in registers and the long input streams through a register window, so a
+// combination costs one FFMA and the kernel runs at the HBM roofline.
+#include "common.cuh"
+
+namespace sg {
+
+struct SegsumK {
+  const float* ops[SG_MAX_ARITY];
+  int32_t op_off[SG_MAX_ARITY];  // row offset of operand i inside the shared tile
+  int32_t op_rows[SG_MAX_ARITY];
+  int32_t n_ops;
+  int32_t clamp;
+  int32_t total_rows;
+  int64_t B;
+  const int32_t* recs;
+  const int32_t* items;
+  const int32_t* blk;
+  float* out;
+  float* scratch;
+};
+
+template <int NOPS, int RW, bool STAGED>
+__global__ void __launch_bounds__(256) k_segsum(const SegsumK a) {
+  extern __shared__ float tile[];  // [total_rows][32]
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int64_t b = (int64_t)blockIdx.x * kWarp + lane;
+  const bool bval = b < a.B;
+  const int64_t bs = bval ? b : (a.B - 1);
+
+  if constexpr (STAGED) {
+#pragma unroll
+    for (int i = 0; i < NOPS; ++i) {
+      const float* __restrict__ src = a.ops[i] + bs;
+      float* dst = tile + (size_t)a.op_off[i] * kWarp + lane;
+      const int rows = a.op_rows[i];
+      int r = warp;
+      for (; r + 3 * nwarps < rows; r += 4 * nwarps) {
+        float v0 = __ldg(src + (size_t)r * a.B);
+        float v1 = __ldg(src + (size_t)(r + nwarps) * a.B);
+        float v2 = __ldg(src + (size_t)(r + 2 * nwarps) * a.B);
+        float v3 = __ldg(src + (size_t)(r + 3 * nwarps) * a.B);
+        dst[(size_t)r * kWarp] = v0;
+        dst[(size_t)(r + nwarps) * kWarp] = v1;
+        dst[(size_t)(r + 2 * nwarps) * kWarp] = v2;
+        dst[(size_t)(r + 3 * nwarps) * kWarp] = v3;
+      }
+      for (; r < rows; r += nwarps) dst[(size_t)r * kWarp] = __ldg(src + (size_t)r * a.B);
+    }
+    __syncthreads();
+  }
+
+  const float* opbase[NOPS];
+#pragma unroll
+  for (int i = 0; i < NOPS; ++i) {
+    if constexpr (STAGED)
+      opbase[i] = tile + (size_t)a.op_off[i] * kWarp + lane;
+    else
+      opbase[i] = a.ops[i] + bs;
+  }
+  const int64_t rstride = STAGED ? kWarp : a.B;
+
+  const int it0 = __ldg(a.blk + blockIdx.y);
+  const int it1 = __ldg(a.blk + blockIdx.y + 1);
+  for (int it = it0 + warp; it < it1; it += nwarps) {
+    const int4 item = __ldg(reinterpret_cast<const int4*>(a.items) + it);
+    float acc0 = 0.f, acc1 = 0.f;
+    int c = item.y;
+    const int32_t* rp = a.recs + (size_t)c * RW;
+    for (; c + 1 < item.z; c += 2, rp += 2 * RW) {
+      Rec<RW> r0 = load_rec<RW>(rp);
+      Rec<RW> r1 = load_rec<RW>(rp + RW);
+      float q0 = STAGED ? opbase[0][r0.v[0] * rstride] : __ldg(opbase[0] + (size_t)r0.v[0] * rstride);
+      float q1 = STAGED ? opbase[0][r1.v[0] * rstride] : __ldg(opbase[0] + (size_t)r1.v[0] * rstride);
+#pragma unroll
+      for (int i = 1; i < NOPS; ++i) {
+        q0 *= STAGED ? opbase[i][r0.v[i] * rstride] : __ldg(opbase[i] + (size_t)r0.v[i] * rstride);
+        q1 *= STAGED ? opbase[i][r1.v[i] * rstride] : __ldg(opbase[i] + (size_t)r1.v[i] * rstride);
+      }
+      acc0 += q0;
+      acc1 += q1;
+    }
+    if (c < item.z) {
+      Rec<RW> r0 = load_rec<RW>(rp);
+      float q0 = STAGED ? opbase[0][r0.v[0] * rstride] : __ldg(opbase[0] + (size_t)r0.v[0] * rstride);
+#pragma unroll
+      for (int i = 1; i < NOPS; ++i)
+        q0 *= STAGED ? opbase[i][r0.v[i] * rstride] : __ldg(opbase[i] + (size_t)r0.v[i] * rstride);
+      acc0 += q0;
+    }
+    float acc = acc0 + acc1;
+    if (bval) {
+      if (item.w < 0)
+        a.out[(size_t)item.x * a.B + b] = a.clamp ? clamp01(acc) : acc;
+      else
+        a.scratch[(size_t)item.w * a.B + b] = acc;
+    }
+  }
+}
+
+// Deterministic finish of segments spread over several items (pieces summed in order).
+__global__ void k_segsum_fixup(const int32_t* __restrict__ split, int n_split, const float* __restrict__ scratch,
+                               int64_t B, int clamp, float* __restrict__ out) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  for (int s = blockIdx.y; s < n_split; s += gridDim.y) {
+    const int seg = __ldg(split + 3 * s), p0 = __ldg(split + 3 * s + 1), p1 = __ldg(split + 3 * s + 2);
+    float acc = 0.f;
+    for (int q = p0; q < p1; ++q) acc += scratch[(size_t)q * B + b];
+    out[(size_t)seg * B + b] = clamp ? clamp01(acc) : acc;
+  }
+}
+
+template <int NOPS, int RW, bool STAGED>
+static int launch_segsum_t(const SegsumK& k, int n_blocks, size_t smem, cudaStream_t st) {
+  dim3 grid(ceil_div(k.B, kWarp), n_blocks);
+  if (STAGED && smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_segsum<NOPS, RW, STAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  k_segsum<NOPS, RW, STAGED><<<grid, 256, STAGED ? smem : 0, st>>>(k);
+  SG_LAUNCH_CHECK();
+  return 0;
+}
+
+template <int NOPS, int RW>
+static int launch_segsum_s(const SegsumK& k, bool staged, int n_blocks, size_t smem, cudaStream_t st) {
+  return staged ? launch_segsum_t<NOPS, RW, true>(k, n_blocks, smem, st)
+                : launch_segsum_t<NOPS, RW, false>(k, n_blocks, smem, st);
+}
+
+static constexpr size_t kMaxStageBytes = 200 * 1024;
+
+static int run_segsum(const sg_segsum* p, const float* const* ops, const int32_t* op_rows, int n_ops, int64_t B,
+                      int clamp, float* out, float* scratch, cudaStream_t st) {
+  SG_RETURN_IF(n_ops < 1 || n_ops > SG_MAX_ARITY, cudaErrorInvalidValue);
+  SG_RETURN_IF(p->rec_words < n_ops, cudaErrorInvalidValue);
+  if (B <= 0 || p->n_seg <= 0) return 0;
+  SegsumK k{};
+  int total = 0;
+  for (int i = 0; i < n_ops; ++i) {
+    k.ops[i] = ops[i];
+    k.op_rows[i] = op_rows[i];
+    k.op_off[i] = total;
+    total += op_rows[i];
+  }
+  k.n_ops = n_ops;
+  k.clamp = clamp;
+  k.total_rows = total;
+  k.B = B;
+  k.recs = p->recs;
+  k.items = p->items;
+  k.blk = p->blk;
+  k.out = out;
+  k.scratch = scratch;
+  const size_t smem = (size_t)total * kWarp * sizeof(float);
+  const bool staged = p->staged && smem <= kMaxStageBytes;
+  int rc = 0;
+  if (p->n_items > 0) {
+    const int rw = p->rec_words;
+    switch (n_ops) {
+      case 1: rc = rw == 1 ? launch_segsum_s<1, 1>(k, staged, p->n_blocks, smem, st)
+                           : launch_segsum_s<1, 2>(k, staged, p->n_blocks, smem, st); break;
+      case 2: rc = launch_segsum_s<2, 2>(k, staged, p->n_blocks, smem, st); break;
+      case 3: rc = launch_segsum_s<3, 4>(k, staged, p->n_blocks, smem, st); break;
+      case 4: rc = launch_segsum_s<4, 4>(k, staged, p->n_blocks, smem, st); break;
+      case 5: rc = launch_segsum_s<5, 8>(k, staged, p->n_blocks, smem, st); break;
+      case 6: rc = launch_segsum_s<6, 8>(k, staged, p->n_blocks, smem, st); break;
+      case 7: rc = launch_segsum_s<7, 8>(k, staged, p->n_blocks, smem, st); break;
+      default: rc = launch_segsum_s<8, 8>(k, staged, p->n_blocks, smem, st); break;
+    }
+    if (rc) return rc;
+  }
+  if (p->n_split > 0) {
+    dim3 grid(ceil_div(B, 128), p->n_split < 65535 ? p->n_split : 65535);
+    k_segsum_fixup<<<grid, 128, 0, st>>>(p->split, p->n_split, scratch, B, clamp, out);
+    SG_LAUNCH_CHECK();
+  }
+  return 0;
+}
+
+// ------------------------------- Toeplitz fast path -----------------------------------
+// out[o][b] = clamp01( sum_{j<KF} L[o-j][b] * S[j][b] ),  o in [0, nL + KF - 1)
+// Thread = (sample b, tile of R outputs). S lives in KF registers, L in a window of
+// R + KF - 1 registers: R*KF FFMA per (R + 2KF - 1) coalesced loads.
+constexpr int kConvR = 16;
+
+template <int KF>
+__global__ void __launch_bounds__(128) k_conv_fwd(const float* __restrict__ L, int nL, const float* __restrict__ S,
+                                                  float* __restrict__ out, int n_out, int64_t B, int n_tiles) {
+  const int lane = threadIdx.x;
+  const int t = blockIdx.y * blockDim.y + threadIdx.y;
+  const int64_t b = (int64_t)blockIdx.x * kWarp + lane;
+  if (b >= B || t >= n_tiles) return;
+  constexpr int R = kConvR;
+  constexpr int WN = R + KF - 1;
+  const int o0 = t * R;
+  float f[KF];
+#pragma unroll
+  for (int j = 0; j < KF; ++j) f[j] = __ldg(S + (size_t)j * B + b);
+  float w[WN];
+#pragma unroll
+  for (int i = 0; i < WN; ++i) {
+    const int s = o0 - (KF - 1) + i;
+    w[i] = (s >= 0 && s < nL) ? __ldg(L + (size_t)s * B + b) : 0.f;
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < KF; ++j) acc = fmaf(w[r + KF - 1 - j], f[j], acc);
+    const int o = o0 + r;
+    if (o < n_out) out[(size_t)o * B + b] = clamp01(acc);
+  }
+}
+
+// dL[s][b] = sum_j g[s+j][b] * S[j][b];   dS[j][b] = sum_s g[s+j][b] * L[s][b]
+// CTA = 32 samples x NW warps; warps stride over tiles of R positions of L, dS partials
+// are reduced across warps in shared memory in a fixed order (deterministic, no atomics).
+template <int KF>
+__global__ void __launch_bounds__(256) k_conv_bwd(const float* __restrict__ g, int n_out, const float* __restrict__ L,
+                                                  int nL, const float* __restrict__ S, float* __restrict__ dL,
+                                                  float* __restrict__ dS, int64_t B, int n_tiles) {
+  __shared__ float red[8][KF][kWarp];
+  const int lane = threadIdx.x;
+  const int warp = threadIdx.y;
+  const int nw = blockDim.y;
+  const int64_t b0 = (int64_t)blockIdx.x * kWarp + lane;
+  const bool bval = b0 < B;
+  const int64_t b = bval ? b0 : B - 1;
+  constexpr int R = kConvR;
+  constexpr int WN = R + KF - 1;
+  float f[KF], d2[KF];
+#pragma unroll
+  for (int j = 0; j < KF; ++j) {
+    f[j] = __ldg(S + (size_t)j * B + b);
+    d2[j] = 0.f;
+  }
+  for (int t = warp; t < n_tiles; t += nw) {
+    const int s0 = t * R;
+    float gw[WN];
+#pragma unroll
+    for (int i = 0; i < WN; ++i) {
+      const int o = s0 + i;
+      gw[i] = (o < n_out) ? __ldg(g + (size_t)o * B + b) : 0.f;
+    }
+    float pv[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int s = s0 + r;
+      pv[r] = (s < nL) ? __ldg(L + (size_t)s * B + b) : 0.f;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < KF; ++j) acc = fmaf(gw[r + j], f[j], acc);
+      const int s = s0 + r;
+      if (dL != nullptr && bval && s < nL) dL[(size_t)s * B + b] = acc;
+    }
+#pragma unroll
+    for (int j = 0; j < KF; ++j) {
+      float acc = d2[j];
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc = fmaf(gw[r + j], pv[r], acc);
+      d2[j] = acc;
+    }
+  }
+  if (dS == nullptr) return;
+#pragma unroll
+  for (int j = 0; j < KF; ++j) red[warp][j][lane] = d2[j];
+  __syncthreads();
+  if (warp == 0 && bval) {
+#pragma unroll
+    for (int j = 0; j < KF; ++j) {
+      float acc = red[0][j][lane];
+      for (int w = 1; w < nw; ++w) acc += red[w][j][lane];
+      dS[(size_t)j * B + b] = acc;
+    }
+  }
+}
+
+template <int KF>
+static int conv_fwd_t(const float* L, int nL, const float* S, float* out, int n_out, int64_t B, cudaStream_t st) {
+  const int n_tiles = ceil_div(n_out, kConvR);
+  dim3 block(kWarp, 4);
+  dim3 grid(ceil_div(B, kWarp), ceil_div(n_tiles, 4));
+  k_conv_fwd<KF><<<grid, block, 0, st>>>(L, nL, S, out, n_out, B, n_tiles);
+  SG_LAUNCH_CHECK();
+  return 0;
+}
+
+template <int KF>
+static int conv_bwd_t(const float* g, int n_out, const float* L, int nL, const float* S, float* dL, float* dS,
+                      int64_t B, cudaStream_t st) {
+  const int n_tiles = ceil_div(nL, kConvR);
+  const int nw = n_tiles < 8 ? n_tiles : 8;
+  dim3 block(kWarp, nw);
+  dim3 grid(ceil_div(B, kWarp));
+  k_conv_bwd<KF><<<grid, block, 0, st>>>(g, n_out, L, nL, S, dL, dS, B, n_tiles);
+  SG_LAUNCH_CHECK();
+  return 0;
+}
+
+#define SG_CONV_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
+
+static int conv_fwd(int kf, const float* L, int nL, const float* S, float* out, int n_out, int64_t B, cudaStream_t st) {
+  switch (kf) {
+#define X(K) \
+  case K: return conv_fwd_t<K>(L, nL, S, out, n_out, B, st);
+    SG_CONV_CASES(X)
+#undef X
+    default: return (int)cudaErrorInvalidValue;
+  }
+}
+
+static int conv_bwd(int kf, const float* g, int n_out, const float* L, int nL, const float* S, float* dL, float* dS,
+                    int64_t B, cudaStream_t st) {
+  switch (kf) {
+#define X(K) \
+  case K: return conv_bwd_t<K>(g, n_out, L, nL, S, dL, dS, B, st);
+    SG_CONV_CASES(X)
+#undef X
+    default: return (int)cudaErrorInvalidValue;
+  }
+}
+
+// ------------------------------- row kernels ----------------------------------------
+__global__ void k_rows_add(const float* __restrict__ A, const int32_t* __restrict__ ia, const float* __restrict__ Bm,
+                           const int32_t* __restrict__ ib, int64_t n_rows, int64_t B, int clamp,
+                           float* __restrict__ out) {
+  for (int64_t r = blockIdx.y; r < n_rows; r += gridDim.y) {
+    const int xa = ia ? __ldg(ia + r) : -1;
+    const int xb = ib ? __ldg(ib + r) : -1;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
+      float v = 0.f;
+      if (xa >= 0) v += __ldg(A + (size_t)xa * B + b);
+      if (xb >= 0) v += __ldg(Bm + (size_t)xb * B + b);
+      out[(size_t)r * B + b] = clamp ? clamp01(v) : v;
+    }
+  }
+}
+
+template <typename V>
+__global__ void k_rows_gather(const V* __restrict__ src, const int32_t* __restrict__ idx, int64_t n_rows,
+                              int64_t row_vecs, V* __restrict__ dst) {
+  for (int64_t r = blockIdx.y; r < n_rows; r += gridDim.y) {
+    const int x = __ldg(idx + r);
+    V* d = dst + (size_t)r * row_vecs;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < row_vecs;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      if (x >= 0)
+        d[i] = src[(size_t)x * row_vecs + i];
+      else
+        d[i] = V{};
+    }
+  }
+}
+
+// ------------------------------- layout kernels -------------------------------------
+template <typename T>
+__device__ __forceinline__ float to_f(T v) { return (float)v; }
+template <>
+__device__ __forceinline__ float to_f<__half>(__half v) { return __half2float(v); }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T>
+__device__ __forceinline__ T from_f(float v) { return (T)v; }
+template <>
+__device__ __forceinline__ __half from_f<__half>(float v) { return __float2half_rn(v); }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// dst[n][B] fp32 <- src(B, n) strided (32x32 tile transpose, both sides coalesced when possible)
+template <typename T>
+__global__ void k_to_symbol_major(const T* __restrict__ src, int64_t B, int64_t n, int64_t sb, int64_t sn,
+                                  float* __restrict__ dst) {
+  __shared__ float t[32][33];
+  const int64_t b0 = (int64_t)blockIdx.x * 32, n0 = (int64_t)blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t bb = b0 + i, nn = n0 + threadIdx.x;
+    if (bb < B && nn < n) t[i][threadIdx.x] = to_f<T>(src[bb * sb + nn * sn]);
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t nn = n0 + i, bb = b0 + threadIdx.x;
+    if (bb < B && nn < n) dst[nn * B + bb] = t[threadIdx.x][i];
+  }
+}
+
+template <typename T>
+__global__ void k_from_symbol_major(const float* __restrict__ src, int64_t B, int64_t n, T* __restrict__ dst,
+                                    int64_t sb, int64_t sn) {
+  __shared__ float t[32][33];
+  const int64_t b0 = (int64_t)blockIdx.x * 32, n0 = (int64_t)blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t nn = n0 + i, bb = b0 + threadIdx.x;
+    if (bb < B && nn < n) t[i][threadIdx.x] = src[nn * B + bb];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t bb = b0 + i, nn = n0 + threadIdx.x;
+    if (bb < B && nn < n) dst[bb * sb + nn * sn] = from_f<T>(t[threadIdx.x][i]);
+  }
+}
+
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" {
+
+int sg_version(void) { return 1; }
+
+int sg_device_sm_count(int device) {
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  return v;
+}
+
+int sg_segsum_run(const sg_segsum* prob, const float* const* ops, const int32_t* op_rows, int32_t n_ops, int64_t B,
+                  int32_t clamp01_, float* out, float* scratch, sg_stream_t stream) {
+  return run_segsum(prob, ops, op_rows, n_ops, B, clamp01_, out, scratch, (cudaStream_t)stream);
+}
+
+int sg_damp_apply_fwd(const sg_damp_plan* plan, const float* const* inputs, int64_t B, float* out, float* scratch,
+                      sg_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  SG_RETURN_IF(plan->arity < 1 || plan->arity > SG_MAX_ARITY, cudaErrorInvalidValue);
+  if (plan->conv) {
+    const int sh = plan->conv_short, lo = 1 - sh;
+    return conv_fwd(plan->sizes[sh], inputs[lo], plan->sizes[lo], inputs[sh], out, plan->n_out, B, st);
+  }
+  return run_segsum(&plan->fwd, inputs, plan->sizes, plan->arity, B, 1, out, scratch, st);
+}
+
+int sg_damp_apply_bwd(const sg_damp_plan* plan, const float* const* inputs, const float* grad_out, int64_t B,
+                      float* const* grad_in, float* scratch, sg_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = plan->arity;
+  SG_RETURN_IF(n < 1 || n > SG_MAX_ARITY, cudaErrorInvalidValue);
+  if (plan->conv) {
+    const int sh = plan->conv_short, lo = 1 - sh;
+    if (grad_in[0] == nullptr && grad_in[1] == nullptr) return 0;
+    return conv_bwd(plan->sizes[sh], grad_out, plan->n_out, inputs[lo], plan->sizes[lo], inputs[sh], grad_in[lo],
+                    grad_in[sh], B, st);
+  }
+  for (int k = 0; k < n; ++k) {
+    if (grad_in[k] == nullptr) continue;
+    const float* ops[SG_MAX_ARITY];
+    int32_t rows[SG_MAX_ARITY];
+    ops[0] = grad_out;
+    rows[0] = plan->n_out;
+    int m = 1;
+    for (int j = 0; j < n; ++j) {
+      if (j == k) continue;
+      ops[m] = inputs[j];
+      rows[m] = plan->sizes[j];
+      ++m;
+    }
+    int rc = run_segsum(&plan->bwd[k], ops, rows, n, B, 0, grad_in[k], scratch, st);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+int sg_damp_rows_add(const float* A, const int32_t* ia, const float* Bm, const int32_t* ib, int64_t n_rows, int64_t B,
+                     int32_t clamp01_, float* out, sg_stream_t stream) {
+  if (n_rows <= 0 || B <= 0) return 0;
+  const int threads = 256;
+  int gx = ceil_div(B, threads);
+  if (gx > 64) gx = 64;
+  dim3 grid(gx, n_rows < 65535 ? (unsigned)n_rows : 65535u);
+  k_rows_add<<<grid, threads, 0, (cudaStream_t)stream>>>(A, ia, Bm, ib, n_rows, B, clamp01_, out);
+  SG_LAUNCH_CHECK();
+  return 0;
+}
+
+int sg_rows_gather(const void* src, const int32_t* idx, int64_t n_rows, int64_t row_bytes, void* dst,
+                   sg_stream_t stream) {
+  if (n_rows <= 0 || row_bytes <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const uintptr_t al = (uintptr_t)src | (uintptr_t)dst;
+  dim3 grid(1, n_rows < 65535 ? (unsigned)n_rows : 65535u);
+  const int threads = 256;
+  if (row_bytes % 16 == 0 && al % 16 == 0) {
+    const int64_t v = row_bytes / 16;
+    grid.x = ceil_div(v, threads) < 32 ? ceil_div(v, threads) : 32;
+    k_rows_gather<uint4><<<grid, threads, 0, st>>>((const uint4*)src, idx, n_rows, v, (uint4*)dst);
+  } else if (row_bytes % 4 == 0 && al % 4 == 0) {
+    const int64_t v = row_bytes / 4;
+    grid.x = ceil_div(v, threads) < 32 ? ceil_div(v, threads) : 32;
+    k_rows_gather<uint32_t><<<grid, threads, 0, st>>>((const uint32_t*)src, idx, n_rows, v, (uint32_t*)dst);
+  } else {
+    grid.x = ceil_div(row_bytes, threads) < 32 ? ceil_div(row_bytes, threads) : 32;
+    k_rows_gather<uint8_t><<<grid, threads, 0, st>>>((const uint8_t*)src, idx, n_rows, row_bytes, (uint8_t*)dst);
+  }
+  SG_LAUNCH_CHECK();
+  return 0;
+}
+
+int sg_to_symbol_major(const void* src, int32_t src_dtype, int64_t B, int64_t n, int64_t stride_b, int64_t stride_n,
+                       float* dst, sg_stream_t stream) {
+  if (B <= 0 || n <= 0) return 0;
+  dim3 block(32, 8), grid(ceil_div(B, 32), ceil_div(n, 32));
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (src_dtype) {
+    case 0: k_to_symbol_major<float><<<grid, block, 0, st>>>((const float*)src, B, n, stride_b, stride_n, dst); break;
+    case 1: k_to_symbol_major<double><<<grid, block, 0, st>>>((const double*)src, B, n, stride_b, stride_n, dst); break;
+    case 2: k_to_symbol_major<__half><<<grid, block, 0, st>>>((const __half*)src, B, n, stride_b, stride_n, dst); break;
+    case 3:
+      k_to_symbol_major<__nv_bfloat16><<<grid, block, 0, st>>>((const __nv_bfloat16*)src, B, n, stride_b, stride_n,
+                                                                 dst);
+      break;
+    default: return (int)cudaErrorInvalidValue;
+  }
+  SG_LAUNCH_CHECK();
+  return 0;
+}
+
+int sg_from_symbol_major(const float* src, int64_t B, int64_t n, void* dst, int32_t dst_dtype, int64_t stride_b,
+                         int64_t stride_n, sg_stream_t stream) {
+  if (B <= 0 || n <= 0) return 0;
+  dim3 block(32, 8), grid(ceil_div(B, 32), ceil_div(n, 32));
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (dst_dtype) {
+    case 0: k_from_symbol_major<float><<<grid, block, 0, st>>>(src, B, n, (float*)dst, stride_b, stride_n); break;
+    case 1: k_from_symbol_major<double><<<grid, block, 0, st>>>(src, B, n, (double*)dst, stride_b, stride_n); break;
+    case 2: k_from_symbol_major<__half><<<grid, block, 0, st>>>(src, B, n, (__half*)dst, stride_b, stride_n); break;
+    case 3:
+      k_from_symbol_major<__nv_bfloat16><<<grid, block, 0, st>>>(src, B, n, (__nv_bfloat16*)dst, stride_b, stride_n);
+      break;
+    default: return (int)cudaErrorInvalidValue;
+  }
+  SG_LAUNCH_CHECK();
+  return 0;
+}
+
+}  // extern "C"

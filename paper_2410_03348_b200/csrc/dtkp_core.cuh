@@ -1,0 +1,293 @@
+// DTKP-AM device core: the streaming top-k set, ranking keys and the fused apply kernel.
+// See dtkp.cu for the semantics; this header is instantiated once per K (dtkp_apply_k.cu)
+// so the eight K variants compile in parallel.
+#pragma once
+#include "common.cuh"
+
+namespace sg {
+
+// Running top-k of distinct proofs ordered by (key desc, stream position asc).
+template <int K, int WT>
+struct TopK {
+  uint64_t m[K][WT];
+  double key[K];
+  int idx[K];
+  int n;
+
+  __device__ __forceinline__ void clear() { n = 0; }
+
+  // Insert a candidate that comes after every previously streamed candidate
+  // (_dtkpcore.pyx:58-94 semantics: first occurrence wins, ties keep stream order).
+  __device__ __forceinline__ void insert(const uint64_t (&mm)[WT], double kk, int id) {
+    if (n == K && !(kk > key[K - 1])) return;
+    bool dup = false;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      bool eq = i < n;
+#pragma unroll
+      for (int w = 0; w < WT; ++w) eq = eq && (m[i][w] == mm[w]);
+      dup = dup || eq;
+    }
+    if (dup) return;
+    int pos = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) pos += (i < n && key[i] >= kk) ? 1 : 0;
+#pragma unroll
+    for (int i = K - 1; i >= 1; --i) {
+      if (i > pos) {
+#pragma unroll
+        for (int w = 0; w < WT; ++w) m[i][w] = m[i - 1][w];
+        key[i] = key[i - 1];
+        idx[i] = idx[i - 1];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (i == pos) {
+#pragma unroll
+        for (int w = 0; w < WT; ++w) m[i][w] = mm[w];
+        key[i] = kk;
+        idx[i] = id;
+      }
+    }
+    n = n < K ? n + 1 : K;
+  }
+
+  // Copy entry q (runtime index) out of the register arrays without local memory.
+  __device__ __forceinline__ void get(int q, uint64_t (&mm)[WT], double& kk) const {
+#pragma unroll
+    for (int w = 0; w < WT; ++w) mm[w] = 0ull;
+    kk = 0.0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (i == q) {
+#pragma unroll
+        for (int w = 0; w < WT; ++w) mm[w] = m[i][w];
+        kk = key[i];
+      }
+    }
+  }
+};
+
+// One sample's probability column staged in shared memory: fp64 [I][32] when it fits,
+// else fp32 [I][32] upcast on read (identical keys: the registry values are fp32).
+struct PCol {
+  const double* smd;
+  const float* smf;
+  bool dbl;
+  __device__ __forceinline__ double operator()(int j) const {
+    return dbl ? smd[(size_t)j * kWarp] : (double)smf[(size_t)j * kWarp];
+  }
+};
+
+static constexpr size_t kMaxPTile = 192 * 1024;
+
+// Staging mode for a registry of I columns: 2 = fp64, 1 = fp32, 0 = does not fit.
+__host__ __device__ inline int ptile_mode(int I) {
+  if ((size_t)I * kWarp * sizeof(double) <= kMaxPTile) return 2;
+  if ((size_t)I * kWarp * sizeof(float) <= kMaxPTile) return 1;
+  return 0;
+}
+
+__device__ __forceinline__ PCol stage_pcol(void* tile, const float* __restrict__ p, int I, int64_t B, int64_t b,
+                                           int lane, int warp, int nwarps) {
+  const bool dbl = ptile_mode(I) == 2;
+  if (dbl) {
+    double* t = reinterpret_cast<double*>(tile);
+    for (int j = warp; j < I; j += nwarps) t[(size_t)j * kWarp + lane] = (double)__ldg(p + (size_t)j * B + b);
+  } else {
+    float* t = reinterpret_cast<float*>(tile);
+    for (int j = warp; j < I; j += nwarps) t[(size_t)j * kWarp + lane] = __ldg(p + (size_t)j * B + b);
+  }
+  return PCol{reinterpret_cast<const double*>(tile) + lane, reinterpret_cast<const float*>(tile) + lane, dbl};
+}
+
+// fp64 product of member probabilities in ascending column order (_dtkpcore.pyx:53-57).
+template <int WT>
+__device__ __forceinline__ double proof_key(const uint64_t (&mm)[WT], const PCol& pc) {
+  double prod = 1.0;
+#pragma unroll
+  for (int w = 0; w < WT; ++w) {
+    uint64_t x = mm[w];
+    while (x) {
+      const int j = __ffsll((long long)x) - 1;
+      prod *= pc(w * 64 + j);
+      x &= x - 1;
+    }
+  }
+  return prod;
+}
+
+struct DtkpK {
+  sg_dtkp_operand ops[SG_MAX_ARITY];
+  sg_dtkp_operand tail;
+  int32_t arity, K, W, I;
+  int64_t B;
+  const float* p;
+  const int32_t* recs;
+  int32_t rec_words;
+  const int32_t* items;
+  const int32_t* blk;
+  uint64_t* out_m;
+  uint8_t* out_p;
+  uint64_t* scr_m;
+  uint8_t* scr_p;
+};
+
+template <int WT>
+__device__ __forceinline__ void load_row(const sg_dtkp_operand& op, int K, int64_t B, int64_t b, int r, int q,
+                                         uint64_t (&mm)[WT]) {
+  const unsigned long long* base =
+      reinterpret_cast<const unsigned long long*>(op.member) + ((size_t)r * K + q) * (size_t)op.W * B + b;
+#pragma unroll
+  for (int w = 0; w < WT; ++w) mm[w] = (w < op.W) ? __ldg(base + (size_t)w * B) : 0ull;
+}
+
+__device__ __forceinline__ bool row_present(const sg_dtkp_operand& op, int K, int64_t B, int64_t b, int r, int q) {
+  return __ldg(op.present + ((size_t)r * K + q) * B + b) != 0;
+}
+
+template <int K, int WT>
+__global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
+  extern __shared__ __align__(16) unsigned char ptile_raw[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int64_t b0 = (int64_t)blockIdx.x * kWarp + lane;
+  const bool bval = b0 < a.B;
+  const int64_t b = bval ? b0 : a.B - 1;
+  const PCol pc = stage_pcol(ptile_raw, a.p, a.I, a.B, b, lane, warp, nwarps);
+  __syncthreads();
+
+  const int it0 = __ldg(a.blk + blockIdx.y), it1 = __ldg(a.blk + blockIdx.y + 1);
+  for (int it = it0 + warp; it < it1; it += nwarps) {
+    const int4 item = __ldg(reinterpret_cast<const int4*>(a.items) + it);
+    TopK<K, WT> S;
+    S.clear();
+    for (int c = item.y; c < item.z; ++c) {
+      const int32_t* rec = a.recs + (size_t)c * a.rec_words;
+      if (a.arity == 1) {
+        // group_disj / union / merge: stream the stored rows as they are
+        int r = __ldg(rec);
+        const sg_dtkp_operand* op = &a.ops[0];
+        if (r >= a.ops[0].rows) {
+          r -= a.ops[0].rows;
+          op = &a.tail;
+        }
+#pragma unroll 1
+        for (int q = 0; q < K; ++q) {
+          if (row_present(*op, K, a.B, b, r, q)) {
+            uint64_t mm[WT];
+            load_row<WT>(*op, K, a.B, b, r, q, mm);
+            S.insert(mm, proof_key<WT>(mm, pc), 0);
+          }
+        }
+      } else {
+        // conj fold, normalised after every step (candidate order ra*kb + rb)
+        TopK<K, WT> T;
+        T.clear();
+        const int r0 = __ldg(rec), r1 = __ldg(rec + 1);
+#pragma unroll 1
+        for (int qa = 0; qa < K; ++qa) {
+          if (!row_present(a.ops[0], K, a.B, b, r0, qa)) continue;
+          uint64_t ma[WT];
+          load_row<WT>(a.ops[0], K, a.B, b, r0, qa, ma);
+#pragma unroll 1
+          for (int qb = 0; qb < K; ++qb) {
+            if (!row_present(a.ops[1], K, a.B, b, r1, qb)) continue;
+            uint64_t mm[WT];
+            load_row<WT>(a.ops[1], K, a.B, b, r1, qb, mm);
+#pragma unroll
+            for (int w = 0; w < WT; ++w) mm[w] |= ma[w];
+            T.insert(mm, proof_key<WT>(mm, pc), 0);
+          }
+        }
+#pragma unroll 1
+        for (int i = 2; i < a.arity; ++i) {
+          const int ri = __ldg(rec + i);
+          TopK<K, WT> U;
+          U.clear();
+#pragma unroll 1
+          for (int qa = 0; qa < T.n; ++qa) {
+            uint64_t ma[WT];
+            double ka;
+            T.get(qa, ma, ka);
+#pragma unroll 1
+            for (int qb = 0; qb < K; ++qb) {
+              if (!row_present(a.ops[i], K, a.B, b, ri, qb)) continue;
+              uint64_t mm[WT];
+              load_row<WT>(a.ops[i], K, a.B, b, ri, qb, mm);
+#pragma unroll
+              for (int w = 0; w < WT; ++w) mm[w] |= ma[w];
+              U.insert(mm, proof_key<WT>(mm, pc), 0);
+            }
+          }
+          T = U;
+        }
+#pragma unroll 1
+        for (int q = 0; q < T.n; ++q) {
+          uint64_t mm[WT];
+          double kk;
+          T.get(q, mm, kk);
+          S.insert(mm, kk, 0);  // same mask, same p -> same key as a recomputation
+        }
+      }
+    }
+    if (bval) {
+      uint64_t* om;
+      uint8_t* opr;
+      if (item.w < 0) {
+        om = a.out_m + (size_t)item.x * K * a.W * a.B;
+        opr = a.out_p + (size_t)item.x * K * a.B;
+      } else {
+        om = a.scr_m + (size_t)item.w * K * a.W * a.B;
+        opr = a.scr_p + (size_t)item.w * K * a.B;
+      }
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        const bool live = q < S.n;
+        opr[(size_t)q * a.B + b0] = live ? 1 : 0;
+#pragma unroll
+        for (int w = 0; w < WT; ++w)
+          if (w < a.W) om[((size_t)q * a.W + w) * a.B + b0] = live ? S.m[q][w] : 0ull;
+      }
+    }
+  }
+}
+
+template <int K, int WT>
+static int launch_apply_kw(const DtkpK& k, int n_blocks, cudaStream_t st) {
+  const int mode = ptile_mode(k.I);
+  if (mode == 0) return (int)cudaErrorNotSupported;
+  const size_t smem = (size_t)k.I * kWarp * (mode == 2 ? sizeof(double) : sizeof(float));
+  dim3 grid(ceil_div(k.B, kWarp), n_blocks);
+  if (smem > 48 * 1024) {
+    cudaError_t e =
+        cudaFuncSetAttribute(k_dtkp_apply<K, WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  k_dtkp_apply<K, WT><<<grid, 128, smem, st>>>(k);
+  SG_LAUNCH_CHECK();
+  return 0;
+}
+
+template <int K>
+static int launch_apply_k(const DtkpK& k, int n_blocks, cudaStream_t st) {
+  if (k.W <= 1) return launch_apply_kw<K, 1>(k, n_blocks, st);
+  if (k.W <= 2) return launch_apply_kw<K, 2>(k, n_blocks, st);
+  if (k.W <= 4) return launch_apply_kw<K, 4>(k, n_blocks, st);
+  if (k.W <= 8) return launch_apply_kw<K, 8>(k, n_blocks, st);
+  return (int)cudaErrorNotSupported;
+}
+
+// One launcher per K, defined in dtkp_apply_k.cu (compiled once per K value).
+int launch_apply_K1(const DtkpK&, int, cudaStream_t);
+int launch_apply_K2(const DtkpK&, int, cudaStream_t);
+int launch_apply_K3(const DtkpK&, int, cudaStream_t);
+int launch_apply_K4(const DtkpK&, int, cudaStream_t);
+int launch_apply_K5(const DtkpK&, int, cudaStream_t);
+int launch_apply_K6(const DtkpK&, int, cudaStream_t);
+int launch_apply_K7(const DtkpK&, int, cudaStream_t);
+int launch_apply_K8(const DtkpK&, int, cudaStream_t);
+
+}  // namespace sg

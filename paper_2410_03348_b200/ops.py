@@ -1,0 +1,327 @@
+"""torch.autograd bindings of the C-ABI kernels (the thin layer between tags and CUDA).
+
+Every function here runs on the current CUDA stream of the tensors' device and calls
+into ``libsgb200.so``; there is no eager or CPU fallback.  DAMP tensors are symbol-major
+``[rows][B]`` fp32; DTKP tags are ``member int64 [rows][K][W][B]`` (bit patterns of u64)
+plus ``present uint8 [rows][K][B]``.
+
+Gradient conventions follow the reference tape (tensor.py):
+  * clamp backward is the identity everywhere (tensor.py:275-287) — the DAMP apply and
+    disjunction backward pass ``g`` through unchanged;
+  * reduce_prod backward is leave-one-out with the exact-zeros rule (tensor.py:302-318);
+  * batch-1 operands broadcast and their gradient is summed over the batch
+    (tensor.py:130-138) — done by expanding the operand before the kernel, so torch's
+    expand-backward sums it.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .plan import KernelPlan
+
+F32 = torch.float32
+
+
+def _lib():
+    return N.load()
+
+
+def _check_operand(t: torch.Tensor, what: str):
+    N.require_cuda(t, what)
+    if t.dtype != F32 or not t.is_contiguous():
+        raise N.NativeError(f"{what}: expected contiguous float32 [rows][B], got {t.dtype} {tuple(t.shape)}")
+
+
+# ------------------------------------------------------------------------ layout
+class ToSymbolMajor(torch.autograd.Function):
+    """(B, n) user probabilities (any float dtype/strides) -> [n][B] fp32 (Damp.input_tags)."""
+
+    @staticmethod
+    def forward(ctx, x: torch.Tensor):
+        N.require_cuda(x, "probabilities")
+        if x.dtype not in N.DTYPE_CODE:
+            x = x.float()
+        B, n = x.shape
+        out = torch.empty((n, B), device=x.device, dtype=F32)
+        rc = _lib().sg_to_symbol_major(x.data_ptr(), N.DTYPE_CODE[x.dtype], B, n, x.stride(0), x.stride(1),
+                                       out.data_ptr(), N.stream_ptr(x.device))
+        N.check(rc, "sg_to_symbol_major")
+        ctx.in_dtype = x.dtype
+        return out
+
+    @staticmethod
+    def backward(ctx, g: torch.Tensor):
+        g = g.contiguous().float()
+        n, B = g.shape
+        out = torch.empty((B, n), device=g.device, dtype=ctx.in_dtype)
+        rc = _lib().sg_from_symbol_major(g.data_ptr(), B, n, out.data_ptr(), N.DTYPE_CODE[ctx.in_dtype], out.stride(0),
+                                         out.stride(1), N.stream_ptr(g.device))
+        N.check(rc, "sg_from_symbol_major")
+        return out
+
+
+def to_symbol_major(x: torch.Tensor) -> torch.Tensor:
+    return ToSymbolMajor.apply(x)
+
+
+def expand_batch(x: torch.Tensor, B: int) -> torch.Tensor:
+    """[rows][1] -> [rows][B] (torch sums the gradient back over the batch)."""
+    if x.shape[1] == B:
+        return x
+    if x.shape[1] != 1:
+        raise ValueError(f"cannot broadcast batch {x.shape[1]} to {B}")
+    return x.expand(x.shape[0], B).contiguous()
+
+
+# ------------------------------------------------------------------------ DAMP apply
+class DampApply(torch.autograd.Function):
+    """K1/K2: fused gather -> conj fold -> group_disj (+clamp) and its backward."""
+
+    @staticmethod
+    def forward(ctx, kplan: KernelPlan, B: int, *inputs):
+        dev = inputs[0].device
+        for i, x in enumerate(inputs):
+            _check_operand(x, f"apply input {i}")
+        dplan = kplan.device(dev)
+        out = torch.empty((kplan.n_out, B), device=dev, dtype=F32)
+        st = N.stream_ptr(dev)
+        if kplan.clamp:
+            s = dplan.damp_struct(B)
+            scratch = None
+            if not kplan.conv and s.fwd.n_partial:
+                scratch = torch.empty((s.fwd.n_partial, B), device=dev, dtype=F32)
+            rc = _lib().sg_damp_apply_fwd(ctypes.byref(s), N.ptr_array(inputs), B, out.data_ptr(), N.ptr(scratch), st)
+            N.check(rc, "sg_damp_apply_fwd")
+        else:
+            seg = dplan.fwd().struct(B)
+            scratch = torch.empty((seg.n_partial, B), device=dev, dtype=F32) if seg.n_partial else None
+            rows = (ctypes.c_int32 * N.MAX_ARITY)(*kplan.sizes)
+            rc = _lib().sg_segsum_run(ctypes.byref(seg), N.ptr_array(inputs), rows, kplan.arity, B, 0, out.data_ptr(),
+                                      N.ptr(scratch), st)
+            N.check(rc, "sg_segsum_run")
+        ctx.kplan = kplan
+        ctx.B = B
+        ctx.save_for_backward(*inputs)
+        return out
+
+    @staticmethod
+    def backward(ctx, g: torch.Tensor):
+        inputs = ctx.saved_tensors
+        kplan: KernelPlan = ctx.kplan
+        B = ctx.B
+        g = g.contiguous()
+        dev = g.device
+        need = [i for i in range(len(inputs)) if ctx.needs_input_grad[2 + i]]
+        grads = [None] * len(inputs)
+        if need:
+            dplan = kplan.device(dev)
+            for i in need:
+                grads[i] = torch.empty_like(inputs[i])
+            if kplan.conv:
+                # the fused Toeplitz backward writes both gradients in one pass
+                for i in range(2):
+                    if grads[i] is None:
+                        grads[i] = torch.empty_like(inputs[i])
+            s = dplan.damp_struct(B, need_bwd=() if kplan.conv else need)
+            n_partial = 0 if kplan.conv else max((s.bwd[i].n_partial for i in need), default=0)
+            scratch = torch.empty((n_partial, B), device=dev, dtype=F32) if n_partial else None
+            rc = _lib().sg_damp_apply_bwd(ctypes.byref(s), N.ptr_array(inputs), g.data_ptr(), B, N.ptr_array(grads),
+                                          N.ptr(scratch), N.stream_ptr(dev))
+            N.check(rc, "sg_damp_apply_bwd")
+            if kplan.conv:
+                grads = [gr if ctx.needs_input_grad[2 + i] else None for i, gr in enumerate(grads)]
+        return (None, None, *grads)
+
+
+def damp_apply(kplan: KernelPlan, inputs, B: int) -> torch.Tensor:
+    inputs = [expand_batch(x, B) for x in inputs]
+    return DampApply.apply(kplan, B, *inputs)
+
+
+class _IndexMap:
+    """Host index list -> device index tensor + the scatter-sum plan of its backward."""
+
+    __slots__ = ("idx", "bwd", "n_src")
+
+    def __init__(self, indices: np.ndarray, n_src: int, device):
+        indices = np.asarray(indices, dtype=np.int32).reshape(-1)
+        self.n_src = int(n_src)
+        self.idx = torch.as_tensor(indices, device=device)
+        keep = indices >= 0
+        rec = np.nonzero(keep)[0].astype(np.int32).reshape(-1, 1)
+        # backward: grad_src[s] = sum_{r: idx[r] == s} g[r]  (select_rows bw, tensor.py:386-391)
+        self.bwd = KernelPlan(rec, indices[keep], self.n_src, (len(indices),), clamp=False)
+
+
+_MAP_CACHE: "dict[tuple, _IndexMap]" = {}
+
+
+def index_map(indices, n_src: int, device) -> _IndexMap:
+    arr = np.asarray(indices, dtype=np.int32).reshape(-1)
+    key = (torch.device(device), int(n_src), arr.tobytes())
+    m = _MAP_CACHE.get(key)
+    if m is None:
+        if len(_MAP_CACHE) > 4096:
+            _MAP_CACHE.clear()
+        m = _IndexMap(arr, n_src, device)
+        _MAP_CACHE[key] = m
+    return m
+
+
+def scatter_rows_sum(g: torch.Tensor, imap: _IndexMap) -> torch.Tensor:
+    return DampApply.apply(imap.bwd, g.shape[1], g.contiguous())
+
+
+class DampRowsAdd(torch.autograd.Function):
+    """out[r] = clamp01(A[ia[r]] + Bm[ib[r]]) — Damp.disj / union; clamp bw = identity."""
+
+    @staticmethod
+    def forward(ctx, A, Bm, ma: _IndexMap, mb: _IndexMap, clamp: bool):
+        _check_operand(A, "disj lhs")
+        _check_operand(Bm, "disj rhs")
+        B = A.shape[1]
+        n = int(ma.idx.numel())
+        out = torch.empty((n, B), device=A.device, dtype=F32)
+        rc = _lib().sg_damp_rows_add(A.data_ptr() if A.numel() else None, ma.idx.data_ptr(),
+                                     Bm.data_ptr() if Bm.numel() else None, mb.idx.data_ptr(), n, B,
+                                     1 if clamp else 0, out.data_ptr(), N.stream_ptr(A.device))
+        N.check(rc, "sg_damp_rows_add")
+        ctx.maps = (ma, mb)
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        ma, mb = ctx.maps
+        ga = scatter_rows_sum(g, ma) if ctx.needs_input_grad[0] else None
+        gb = scatter_rows_sum(g, mb) if ctx.needs_input_grad[1] else None
+        return ga, gb, None, None, None
+
+
+class RowsGather(torch.autograd.Function):
+    """Symbol-axis gather of DAMP rows (filter / gather / placement)."""
+
+    @staticmethod
+    def forward(ctx, x, imap: _IndexMap):
+        _check_operand(x, "gather source")
+        n = int(imap.idx.numel())
+        out = torch.empty((n, x.shape[1]), device=x.device, dtype=F32)
+        rows_gather(x, imap.idx, out)
+        ctx.imap = imap
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        return scatter_rows_sum(g, ctx.imap), None
+
+
+def rows_gather(src: torch.Tensor, idx: torch.Tensor, out: torch.Tensor):
+    """Copy whole symbol rows (any tag kind): out[r] = src[idx[r]] or zeros for -1."""
+    n = int(idx.numel())
+    if n == 0 or out.numel() == 0:
+        return out
+    row_bytes = out[0].numel() * out.element_size()
+    rc = _lib().sg_rows_gather(src.data_ptr() if src.numel() else None, idx.data_ptr(), n, row_bytes, out.data_ptr(),
+                               N.stream_ptr(out.device))
+    N.check(rc, "sg_rows_gather")
+    return out
+
+
+def index_tensor(indices, device) -> torch.Tensor:
+    return torch.as_tensor(np.asarray(indices, dtype=np.int32).reshape(-1), device=device)
+
+
+# ------------------------------------------------------------------------ DTKP
+def dtkp_apply(kplan_host, dseg, dmerge, operands, tail, K: int, W: int, I: int, B: int, p: torch.Tensor,
+               arity: int):
+    """Run sg_dtkp_apply; operands are (member, present) pairs with full batch B."""
+    dev = p.device
+    n_out = dseg.host.n_seg
+    out_m = torch.empty((n_out, K, W, B), device=dev, dtype=torch.int64)
+    out_p = torch.empty((n_out, K, B), device=dev, dtype=torch.uint8)
+    d = N.SgDtkpApplyDesc()
+    d.arity = arity
+    d.K = K
+    d.W = W
+    d.I = I
+    d.B = B
+    for i, (m, pr) in enumerate(operands):
+        d.ops[i].member = m.data_ptr() if m.numel() else None
+        d.ops[i].present = pr.data_ptr() if pr.numel() else None
+        d.ops[i].rows = m.shape[0]
+        d.ops[i].W = m.shape[2]
+    if tail is not None:
+        m, pr = tail
+        d.op_tail.member = m.data_ptr() if m.numel() else None
+        d.op_tail.present = pr.data_ptr() if pr.numel() else None
+        d.op_tail.rows = m.shape[0]
+        d.op_tail.W = m.shape[2]
+    d.p = p.data_ptr() if p.numel() else None
+    d.seg = dseg.struct(B)
+    d.out_member = out_m.data_ptr() if out_m.numel() else None
+    d.out_present = out_p.data_ptr() if out_p.numel() else None
+    scr_m = scr_p = None
+    if dseg.host.n_partial:
+        scr_m = torch.empty((dseg.host.n_partial, K, W, B), device=dev, dtype=torch.int64)
+        scr_p = torch.empty((dseg.host.n_partial, K, B), device=dev, dtype=torch.uint8)
+        d.scratch_member = scr_m.data_ptr()
+        d.scratch_present = scr_p.data_ptr()
+        d.merge = dmerge.struct(B)
+    rc = _lib().sg_dtkp_apply(ctypes.byref(d), N.stream_ptr(dev))
+    N.check(rc, "sg_dtkp_apply")
+    return out_m, out_p
+
+
+class DtkpProbs(torch.autograd.Function):
+    """K5: clamp(sum_r present * prod_{j in r} p_j) and its leave-one-out backward."""
+
+    @staticmethod
+    def forward(ctx, member, present, p):
+        Nn, K, W, B = member.shape
+        I = p.shape[0]
+        out = torch.empty((Nn, B), device=p.device, dtype=F32)
+        rc = _lib().sg_dtkp_probs_fwd(member.data_ptr() if member.numel() else None,
+                                      present.data_ptr() if present.numel() else None, Nn, K, W,
+                                      p.data_ptr() if p.numel() else None, I, B, out.data_ptr() if out.numel() else None,
+                                      N.stream_ptr(p.device))
+        N.check(rc, "sg_dtkp_probs_fwd")
+        ctx.save_for_backward(member, present, p)
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        member, present, p = ctx.saved_tensors
+        Nn, K, W, B = member.shape
+        I = p.shape[0]
+        g = g.contiguous()
+        gp = torch.empty_like(p)
+        nbytes = int(_lib().sg_dtkp_probs_bwd_scratch(Nn, I, B))
+        scratch = torch.empty(max(nbytes, 8), device=p.device, dtype=torch.uint8)
+        rc = _lib().sg_dtkp_probs_bwd(member.data_ptr() if member.numel() else None,
+                                      present.data_ptr() if present.numel() else None, Nn, K, W, p.data_ptr(), I, B,
+                                      g.data_ptr() if g.numel() else None, gp.data_ptr(), scratch.data_ptr(),
+                                      N.stream_ptr(p.device))
+        N.check(rc, "sg_dtkp_probs_bwd")
+        return None, None, gp
+
+
+def dedup_topk(member: torch.Tensor, present: torch.Tensor, p: torch.Tensor, k: int):
+    """Device drop-in for _dtkpcore.dedup_topk: u8 [M,R,I], u8 [M,R], f64 [M,I] -> u8 [M,k,I], u8 [M,k]."""
+    M, R, I = member.shape
+    member = member.contiguous().to(torch.uint8)
+    present = present.contiguous().to(torch.uint8)
+    p = p.contiguous().to(torch.float64)
+    om = torch.empty((M, k, I), device=member.device, dtype=torch.uint8)
+    op = torch.empty((M, k), device=member.device, dtype=torch.uint8)
+    if M == 0 or k == 0:
+        return om.zero_(), op.zero_()
+    rc = _lib().sg_dedup_topk(member.data_ptr() if member.numel() else None,
+                              present.data_ptr() if present.numel() else None, p.data_ptr() if p.numel() else None,
+                              M, R, I, k, om.data_ptr() if om.numel() else None, op.data_ptr(),
+                              N.stream_ptr(member.device))
+    N.check(rc, "sg_dedup_topk")
+    return om, op

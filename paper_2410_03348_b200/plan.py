@@ -1,0 +1,514 @@
+"""Host map/shuffle stage of ``apply_if`` and the memoised device plans it feeds.
+
+``build_plan`` restates ``apply_if``'s host part (distribution.py:244-260): the
+symbol function runs once per combination of input symbols, in ``itertools.product``
+order (last input fastest), ``cond`` before ``f``, ``UNDEFINED`` dropped, and output
+symbols numbered in first-derivation order.  The result is an int32 combination ->
+output-symbol table plus CSR views of it; it is memoised on the function's code and
+closure and on the identity of the input symbol lists, so a training loop calls the
+black-box function only once per distinct plan (sum_n builds a new lambda per fold step,
+programs.py:48, which this keying recognises as the same function).
+
+``KernelPlan`` turns (records, output index) pairs into the device work lists consumed by
+the CUDA library: a forward segmented problem (segments = outputs), one backward
+problem per input (segments = that input's positions), and the Toeplitz flag for tables
+with T[s0][s1] == s0 + s1.
+"""
+
+from __future__ import annotations
+
+import itertools
+from collections import OrderedDict
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+__all__ = [
+    "UNDEFINED",
+    "SymbolFunctionError",
+    "SymbolPlan",
+    "KernelPlan",
+    "build_plan",
+    "plan_cache_clear",
+    "plan_cache_info",
+    "canonical_symbols",
+]
+
+
+class _Undefined:
+    """Marker a mapping function returns for combinations with no result."""
+
+    __slots__ = ()
+
+    def __repr__(self):
+        return "UNDEFINED"
+
+    def __reduce__(self):
+        return (_undefined_singleton, ())
+
+
+def _undefined_singleton():
+    return UNDEFINED
+
+
+UNDEFINED = _Undefined()
+
+
+class SymbolFunctionError(RuntimeError):
+    """A user-supplied symbol function raised; carries the offending tuple."""
+
+    def __init__(self, message, symbols):
+        super().__init__(message)
+        self.symbols = symbols
+
+
+def call_user(fn, syms):
+    """distribution.py:179-185: wrap user errors with the offending symbol tuple."""
+    try:
+        return fn(*syms)
+    except Exception as exc:  # noqa: BLE001 - re-raised with context
+        raise SymbolFunctionError(f"symbol function failed on {syms!r}: {exc}", syms) from exc
+
+
+# ----------------------------------------------------------------------------- keys
+def _typed(s):
+    # 1, 1.0, True and Fraction(1) compare equal but may map differently under f
+    if isinstance(s, tuple):
+        return (type(s), tuple(_typed(x) for x in s))
+    return (type(s), s)
+
+
+class _SymbolIntern:
+    """Canonical symbol-tuple objects so plan keys are cheap identity lookups.
+
+    Plan outputs are canonical by construction; user-made lists are interned by a
+    type-aware value key (bounded LRU)."""
+
+    def __init__(self, limit=8192):
+        self.by_id = {}  # id(tuple) -> tuple (holds a reference so ids stay unique)
+        self.by_value = OrderedDict()
+        self.limit = limit
+
+    def canon(self, symbols: tuple) -> tuple:
+        hit = self.by_id.get(id(symbols))
+        if hit is symbols:
+            return symbols
+        key = _typed(symbols) if len(symbols) <= 4096 else None
+        if key is not None:
+            c = self.by_value.get(key)
+            if c is not None:
+                self.by_value.move_to_end(key)
+                return c
+        self.adopt(symbols, key)
+        return symbols
+
+    def adopt(self, symbols: tuple, key=None):
+        self.by_id[id(symbols)] = symbols
+        if key is None and len(symbols) <= 4096:
+            key = _typed(symbols)
+        if key is not None:
+            self.by_value[key] = symbols
+            while len(self.by_value) > self.limit:
+                _, old = self.by_value.popitem(last=False)
+                self.by_id.pop(id(old), None)
+
+
+_INTERN = _SymbolIntern()
+
+
+def canonical_symbols(symbols: tuple) -> tuple:
+    return _INTERN.canon(symbols)
+
+
+def _fn_key(fn):
+    """Hashable identity of a pure symbol function, or None when uncachable."""
+    if fn is None:
+        return ("none",)
+    code = getattr(fn, "__code__", None)
+    try:
+        if code is None:
+            hash(fn)
+            return ("obj", fn)
+        cells = getattr(fn, "__closure__", None)
+        contents = tuple(c.cell_contents for c in cells) if cells else ()
+        kw = getattr(fn, "__kwdefaults__", None)
+        key = (
+            "fn",
+            code,
+            getattr(fn, "__defaults__", None),
+            tuple(sorted(kw.items())) if kw else None,
+            contents,
+            getattr(fn, "__self__", None),
+        )
+        hash(key)
+        return key
+    except (TypeError, ValueError):
+        return None
+
+
+# ----------------------------------------------------------------------------- plans
+class SymbolPlan:
+    """Result of the host map + shuffle stage for one apply_if call.
+
+    combos   int32 [C+, arity]  input positions of every kept combination, ordinal order
+    out_idx  int32 [C+]         output symbol of each kept combination (first derivation)
+    table    int32 [prod S_i]   dense combination -> output index table, -1 = dropped
+    """
+
+    __slots__ = ("out_symbols", "sizes", "combos", "out_idx", "n_enumerated", "_kplan", "_table")
+
+    def __init__(self, out_symbols, sizes, combos, out_idx, n_enumerated):
+        self.out_symbols = out_symbols
+        self.sizes = tuple(sizes)
+        self.combos = combos
+        self.out_idx = out_idx
+        self.n_enumerated = n_enumerated
+        self._kplan = None
+        self._table = None
+
+    @property
+    def arity(self):
+        return len(self.sizes)
+
+    @property
+    def n_out(self):
+        return len(self.out_symbols)
+
+    @property
+    def n_kept(self):
+        return int(self.combos.shape[0])
+
+    @property
+    def table(self) -> np.ndarray:
+        if self._table is None:
+            t = np.full(self.n_enumerated, -1, dtype=np.int32)
+            if self.n_kept:
+                flat = np.ravel_multi_index(tuple(self.combos.T.astype(np.int64)), self.sizes)
+                t[flat] = self.out_idx
+            self._table = t
+        return self._table
+
+    def groups(self):
+        """Bucket member lists (ordinals) in output order, as the reference builds them."""
+        order = np.argsort(self.out_idx, kind="stable")
+        bounds = np.searchsorted(self.out_idx[order], np.arange(self.n_out + 1))
+        return [order[bounds[i] : bounds[i + 1]].tolist() for i in range(self.n_out)]
+
+    def kernel_plan(self) -> "KernelPlan":
+        if self._kplan is None:
+            self._kplan = KernelPlan(self.combos, self.out_idx, self.n_out, self.sizes, clamp=True)
+        return self._kplan
+
+
+_PLAN_CACHE: "OrderedDict[tuple, SymbolPlan]" = OrderedDict()
+_PLAN_CACHE_LIMIT = 1024
+_stats = {"hits": 0, "misses": 0, "uncachable": 0, "f_calls": 0}
+
+
+def plan_cache_clear():
+    _PLAN_CACHE.clear()
+    for k in _stats:
+        _stats[k] = 0
+
+
+def plan_cache_info() -> dict:
+    return dict(_stats, size=len(_PLAN_CACHE))
+
+
+def build_plan(f, cond, symbol_lists) -> SymbolPlan:
+    """Memoised host map/shuffle (distribution.py:244-260); bit-exact plan semantics."""
+    canon = [canonical_symbols(tuple(s)) for s in symbol_lists]
+    fk, ck = _fn_key(f), _fn_key(cond)
+    key = None
+    if fk is not None and ck is not None:
+        key = (fk, ck, tuple(id(s) for s in canon))
+        hit = _PLAN_CACHE.get(key)
+        if hit is not None:
+            _PLAN_CACHE.move_to_end(key)
+            _stats["hits"] += 1
+            return hit[0]
+        _stats["misses"] += 1
+    else:
+        _stats["uncachable"] += 1
+    plan = _map_shuffle(f, cond, canon)
+    if key is not None:
+        # the value keeps the canonical input tuples alive so their ids stay valid
+        _PLAN_CACHE[key] = (plan, canon)
+        while len(_PLAN_CACHE) > _PLAN_CACHE_LIMIT:
+            _PLAN_CACHE.popitem(last=False)
+    return plan
+
+
+def _map_shuffle(f, cond, symbol_lists) -> SymbolPlan:
+    sizes = [len(s) for s in symbol_lists]
+    n_enum = int(np.prod(sizes, dtype=np.int64)) if sizes else 0
+    kept = []
+    out_idx = []
+    buckets = {}
+    calls = 0
+    for ordinal, syms in enumerate(itertools.product(*symbol_lists)):
+        if cond is not None:
+            calls += 1
+            if not call_user(cond, syms):
+                continue
+        calls += 1
+        value = call_user(f, syms)
+        if value is UNDEFINED:
+            continue
+        idx = buckets.get(value)
+        if idx is None:
+            idx = len(buckets)
+            buckets[value] = idx
+        kept.append(ordinal)
+        out_idx.append(idx)
+    _stats["f_calls"] += calls
+    out_symbols = tuple(buckets.keys())
+    _INTERN.adopt(out_symbols)
+    if kept:
+        combos = np.stack(np.unravel_index(np.asarray(kept, dtype=np.int64), sizes), axis=1).astype(np.int32)
+    else:
+        combos = np.zeros((0, len(sizes)), dtype=np.int32)
+    return SymbolPlan(out_symbols, sizes, combos, np.asarray(out_idx, dtype=np.int32), n_enum)
+
+
+# ----------------------------------------------------------------------------- device plans
+def _rec_words(n_ops: int) -> int:
+    for w in (1, 2, 4, 8):
+        if n_ops <= w:
+            return w
+    raise ValueError(f"arity {n_ops} exceeds the supported maximum of {N.MAX_ARITY}")
+
+
+class HostSegsum:
+    """One segmented problem: records grouped into segments, cut into bounded items."""
+
+    __slots__ = ("n_seg", "rec_words", "recs", "items", "split", "n_partial", "work", "seg_off")
+
+    def __init__(self, seg_off: np.ndarray, recs: np.ndarray, max_item: int):
+        n_seg = len(seg_off) - 1
+        nrec, nops = recs.shape if recs.ndim == 2 else (recs.shape[0], 1)
+        rw = _rec_words(max(nops, 1))
+        packed = np.zeros((nrec, rw), dtype=np.int32)
+        packed[:, :nops] = recs.reshape(nrec, nops)
+        lens = np.diff(seg_off).astype(np.int64)
+        pieces = np.maximum(1, -(-lens // max_item))
+        n_items = int(pieces.sum())
+        seg_of = np.repeat(np.arange(n_seg, dtype=np.int64), pieces)
+        first = np.repeat(np.cumsum(pieces) - pieces, pieces)
+        piece = np.arange(n_items, dtype=np.int64) - first
+        rb = seg_off[seg_of].astype(np.int64) + piece * max_item
+        re = np.minimum(rb + max_item, seg_off[seg_of + 1])
+        re = np.maximum(re, rb)
+        is_split = pieces[seg_of] > 1
+        dest = np.full(n_items, -1, dtype=np.int64)
+        n_partial = int(is_split.sum())
+        dest[is_split] = np.arange(n_partial)
+        items = np.stack([seg_of, rb, re, dest], axis=1).astype(np.int32)
+        split_segs = np.nonzero(pieces > 1)[0]
+        if len(split_segs):
+            cnt = pieces[split_segs]
+            pb = np.cumsum(cnt) - cnt
+            split = np.stack([split_segs, pb, pb + cnt], axis=1).astype(np.int32)
+        else:
+            split = np.zeros((0, 3), dtype=np.int32)
+        self.n_seg = n_seg
+        self.rec_words = rw
+        self.recs = packed
+        self.items = items
+        self.split = split
+        self.n_partial = n_partial
+        self.work = (re - rb) + 2  # records + per-item overhead
+        self.seg_off = seg_off
+
+    def blocks(self, n_blocks: int) -> np.ndarray:
+        """Item ranges of n_blocks contiguous CTA chunks balanced by work."""
+        n_items = len(self.items)
+        n_blocks = max(1, min(n_blocks, n_items))
+        cum = np.concatenate([[0], np.cumsum(self.work)])
+        targets = cum[-1] * np.arange(1, n_blocks) / n_blocks
+        cuts = np.searchsorted(cum, targets, side="left")
+        blk = np.concatenate([[0], cuts, [n_items]]).astype(np.int32)
+        return np.maximum.accumulate(blk)
+
+
+class DeviceSegsum:
+    """HostSegsum uploaded to one device, with per-grid block partitions cached."""
+
+    def __init__(self, host: HostSegsum, device, staged: bool, min_chunk_work: int):
+        self.host = host
+        self.device = device
+        self.staged = staged
+        self.min_chunk_work = min_chunk_work
+        self.recs = torch.from_numpy(np.ascontiguousarray(host.recs.reshape(-1))).to(device)
+        self.items = torch.from_numpy(np.ascontiguousarray(host.items.reshape(-1))).to(device)
+        self.split = torch.from_numpy(np.ascontiguousarray(host.split.reshape(-1))).to(device)
+        self.total_work = int(host.work.sum()) if len(host.work) else 0
+        self._blk = {}
+
+    def struct(self, B: int) -> N.SgSegsum:
+        tiles = max(1, -(-B // 32))
+        want = max(1, -(-2 * 148 // tiles))
+        cap = max(1, self.total_work // max(1, self.min_chunk_work))
+        nb = 1
+        while nb < min(want, cap):
+            nb *= 2
+        nb = min(nb, max(1, len(self.host.items)), 65535)
+        blk = self._blk.get(nb)
+        if blk is None:
+            blk = torch.from_numpy(self.host.blocks(nb)).to(self.device)
+            self._blk[nb] = blk
+        s = N.SgSegsum()
+        h = self.host
+        s.n_seg = h.n_seg
+        s.rec_words = h.rec_words
+        s.n_items = len(h.items)
+        s.n_blocks = int(blk.numel()) - 1
+        s.n_split = len(h.split)
+        s.n_partial = h.n_partial
+        s.staged = 1 if self.staged else 0
+        s.recs = self.recs.data_ptr() if self.recs.numel() else None
+        s.items = self.items.data_ptr() if self.items.numel() else None
+        s.blk = blk.data_ptr()
+        s.split = self.split.data_ptr() if self.split.numel() else None
+        return s
+
+
+def csr(keys: np.ndarray, n_seg: int):
+    """Stable CSR grouping: (order, seg_off) with records sorted by (key, position)."""
+    order = np.argsort(keys, kind="stable")
+    counts = np.bincount(keys, minlength=n_seg) if len(keys) else np.zeros(n_seg, dtype=np.int64)
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    return order, off
+
+
+DAMP_MAX_ITEM = 128
+DTKP_MAX_ITEM = 48
+STAGE_BYTES = 200 * 1024
+
+
+class KernelPlan:
+    """Device-ready form of a (records -> outputs) sum-of-products structure.
+
+    records  int32 [n_rec, arity]: row of operand i used by record r
+    out_idx  int32 [n_rec]:        output row the record contributes to
+    """
+
+    def __init__(self, records: np.ndarray, out_idx: np.ndarray, n_out: int, sizes, clamp: bool):
+        self.records = np.ascontiguousarray(records, dtype=np.int32).reshape(len(out_idx), len(sizes))
+        self.out_idx = np.ascontiguousarray(out_idx, dtype=np.int32)
+        self.n_out = int(n_out)
+        self.sizes = tuple(int(s) for s in sizes)
+        self.arity = len(self.sizes)
+        self.clamp = bool(clamp)
+        if self.arity > N.MAX_ARITY:
+            raise ValueError(f"apply arity {self.arity} exceeds {N.MAX_ARITY}")
+        self.conv, self.conv_short = self._detect_toeplitz()
+        self._fwd_host = None
+        self._bwd_host = {}
+        self._dtkp_host = None
+        self._dev = {}
+
+    # T[s0][s1] == s0 + s1 for every combination, no drops: a 1-D convolution per sample
+    def _detect_toeplitz(self):
+        if self.arity != 2 or not self.clamp:
+            return False, 0
+        s0, s1 = self.sizes
+        if len(self.out_idx) != s0 * s1 or self.n_out != s0 + s1 - 1:
+            return False, 0
+        if min(s0, s1) > 16:
+            return False, 0
+        if not np.array_equal(self.out_idx, self.records[:, 0] + self.records[:, 1]):
+            return False, 0
+        return True, (1 if s1 <= s0 else 0)
+
+    @property
+    def n_rec(self):
+        return len(self.out_idx)
+
+    def fwd_host(self) -> HostSegsum:
+        if self._fwd_host is None:
+            order, off = csr(self.out_idx, self.n_out)
+            self._fwd_host = HostSegsum(off, self.records[order], DAMP_MAX_ITEM)
+        return self._fwd_host
+
+    def bwd_host(self, k: int) -> HostSegsum:
+        h = self._bwd_host.get(k)
+        if h is None:
+            order, off = csr(self.records[:, k], self.sizes[k])
+            cols = [self.out_idx[order]] + [self.records[order, j] for j in range(self.arity) if j != k]
+            h = HostSegsum(off, np.stack(cols, axis=1), DAMP_MAX_ITEM)
+            self._bwd_host[k] = h
+        return h
+
+    def dtkp_host(self) -> HostSegsum:
+        if self._dtkp_host is None:
+            order, off = csr(self.out_idx, self.n_out)
+            self._dtkp_host = HostSegsum(off, self.records[order], DTKP_MAX_ITEM)
+        return self._dtkp_host
+
+    def device(self, device) -> "DevicePlan":
+        key = torch.device(device)
+        dp = self._dev.get(key)
+        if dp is None:
+            dp = DevicePlan(self, key)
+            self._dev[key] = dp
+        return dp
+
+
+class DevicePlan:
+    """Per-device uploaded work lists of a KernelPlan (lazily, per direction)."""
+
+    def __init__(self, kp: KernelPlan, device):
+        self.kp = kp
+        self.device = device
+        self._fwd = None
+        self._bwd = {}
+        self._dtkp = None
+        self._dtkp_merge = None
+
+    def _staged(self, rows: int) -> bool:
+        return rows * 32 * 4 <= STAGE_BYTES
+
+    def fwd(self) -> DeviceSegsum:
+        if self._fwd is None:
+            rows = sum(self.kp.sizes)
+            self._fwd = DeviceSegsum(self.kp.fwd_host(), self.device, self._staged(rows), max(512, 2 * rows))
+        return self._fwd
+
+    def bwd(self, k: int) -> DeviceSegsum:
+        d = self._bwd.get(k)
+        if d is None:
+            rows = self.kp.n_out + sum(s for j, s in enumerate(self.kp.sizes) if j != k)
+            d = DeviceSegsum(self.kp.bwd_host(k), self.device, self._staged(rows), max(512, 2 * rows))
+            self._bwd[k] = d
+        return d
+
+    def dtkp(self):
+        if self._dtkp is None:
+            host = self.kp.dtkp_host()
+            self._dtkp = DeviceSegsum(host, self.device, True, 64)
+            if len(host.split):
+                off = np.concatenate([[0], host.split[:, 2]]).astype(np.int64)
+                merge_recs = np.arange(host.n_partial, dtype=np.int32).reshape(-1, 1)
+                mh = HostSegsum(off, merge_recs, 1 << 30)
+                # merge items write the original output segment
+                mh.items[:, 0] = host.split[:, 0]
+                self._dtkp_merge = DeviceSegsum(mh, self.device, True, 64)
+        return self._dtkp, self._dtkp_merge
+
+    def damp_struct(self, B: int, need_bwd=()) -> N.SgDampPlan:
+        kp = self.kp
+        s = N.SgDampPlan()
+        s.arity = kp.arity
+        s.n_out = kp.n_out
+        for i, n in enumerate(kp.sizes):
+            s.sizes[i] = n
+        s.conv = 1 if kp.conv else 0
+        s.conv_short = kp.conv_short
+        if not kp.conv:
+            s.fwd = self.fwd().struct(B)
+            for k in need_bwd:
+                s.bwd[k] = self.bwd(k).struct(B)
+        return s

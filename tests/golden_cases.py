@@ -1,0 +1,128 @@
+"""Golden workloads, written once against an abstract API so the SAME program runs on
+the reference (tools/make_golden.py), on the CPU oracle (tests/test_oracle.py) and on
+the CUDA path (tests/test_gpu_golden.py).
+
+``api`` provides apply / apply_if / union / UNDEFINED; ``P`` provides sum_n / hwf /
+path_closure with the reference signatures (programs.py:42-196).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+DIGITS = list(range(10))
+TOKENS = [str(d) for d in range(10)] + ["+", "-", "*", "/"]
+
+
+def rows(rng, n, cols):
+    r = rng.uniform(0.05, 1.0, size=(n, cols))
+    r = r / r.sum(axis=1, keepdims=True)
+    return r.astype(np.float32).astype(np.float64)
+
+
+def _sum(api, P, ctx, d):
+    return P.sum_n(ctx, d)
+
+
+def _apply_sum(api, P, ctx, d):
+    return api.apply(lambda *xs: sum(xs), *d)
+
+
+def _apply_prod(api, P, ctx, d):
+    return api.apply(lambda x, y: x * y, *d)
+
+
+def _mod_cond(api, P, ctx, d):
+    return api.apply_if(lambda x, y: api.UNDEFINED if (x + y) % 4 == 3 else (x * y) % 7, lambda x, y: x != y, *d)
+
+
+def _mod3(api, P, ctx, d):
+    return api.apply(lambda x, y, z: (x * y + z) % 5, *d)
+
+
+def _relabel(api, P, ctx, d):
+    return api.apply(lambda x: x % 3, *d)
+
+
+def _bcast_reuse(api, P, ctx, d):
+    x = api.apply(lambda u, v: u + v, d[0], d[1])
+    return api.apply(lambda u, v: u * v, x, d[0])
+
+
+def _union_filter(api, P, ctx, d):
+    e = d[0].filter(lambda s: s % 2 == 0)
+    return api.union(api.apply(lambda x: x * 2, e), d[1])
+
+
+def _hwf(length):
+    def prog(api, P, ctx, d):
+        return P.hwf(ctx, d, length)
+
+    return prog
+
+
+def _path(api, P, ctx, d):
+    return P.path_closure(ctx, d[0])
+
+
+def _edges(seed, nodes, prob):
+    rng = np.random.default_rng(seed)
+    return [(i, j) for i in range(nodes) for j in range(nodes) if i != j and rng.uniform() < prob]
+
+
+# name: (provenance, k, program, symbol-list builder, input builder)
+def _digit_inputs(n, B):
+    def make(rng):
+        return [rows(rng, B, 10) for _ in range(n)]
+
+    return make
+
+
+def _sized_inputs(arity, size, B):
+    def make(rng):
+        return [rows(rng, B, size) for _ in range(arity)]
+
+    return make
+
+
+CASES = {
+    "damp_sum2": ("damp", None, _sum, lambda P: [DIGITS] * 2, _digit_inputs(2, 16), 0),
+    "damp_sum4": ("damp", None, _sum, lambda P: [DIGITS] * 4, _digit_inputs(4, 8), 1),
+    "damp_sum15": ("damp", None, _sum, lambda P: [DIGITS] * 15, _digit_inputs(15, 4), 2),
+    "damp_sweep_a2_s10": ("damp", None, _apply_sum, lambda P: [list(range(10))] * 2, _sized_inputs(2, 10, 16), 3),
+    "damp_sweep_a2_s37": ("damp", None, _apply_sum, lambda P: [list(range(37))] * 2, _sized_inputs(2, 37, 8), 4),
+    "damp_sweep_a3_s7": ("damp", None, _apply_sum, lambda P: [list(range(7))] * 3, _sized_inputs(3, 7, 8), 5),
+    "damp_prod_a2_s10": ("damp", None, _apply_prod, lambda P: [list(range(10))] * 2, _sized_inputs(2, 10, 8), 6),
+    "damp_mod_cond_a2": ("damp", None, _mod_cond, lambda P: [list(range(9))] * 2, _sized_inputs(2, 9, 8), 7),
+    "damp_mod_a3": ("damp", None, _mod3, lambda P: [list(range(6))] * 3, _sized_inputs(3, 6, 8), 8),
+    "damp_a1_relabel": ("damp", None, _relabel, lambda P: [list(range(12))], _sized_inputs(1, 12, 8), 9),
+    "damp_bcast_reuse": ("damp", None, _bcast_reuse, lambda P: [list(range(5)), list(range(4))],
+                         lambda rng: [rows(rng, 6, 5), rows(rng, 1, 4)], 10),
+    "damp_union_filter": ("damp", None, _union_filter, lambda P: [list(range(6)), list(range(3, 8))],
+                          lambda rng: [rows(rng, 8, 6), rows(rng, 8, 5)], 11),
+    "dtkp_hwf3": ("dtkp", 3, _hwf(3), lambda P: [TOKENS] * 3, _sized_inputs(3, 14, 6), 12),
+    "dtkp_hwf5": ("dtkp", 3, _hwf(5), lambda P: [TOKENS] * 5, _sized_inputs(5, 14, 3), 13),
+    "dtkp_hwf3_k1": ("dtkp", 1, _hwf(3), lambda P: [TOKENS] * 3, _sized_inputs(3, 14, 4), 14),
+    "dtkp_hwf3_k7": ("dtkp", 7, _hwf(3), lambda P: [TOKENS] * 3, _sized_inputs(3, 14, 4), 15),
+    "dtkp_sum3_k2": ("dtkp", 2, _sum, lambda P: [DIGITS] * 3, _digit_inputs(3, 5), 16),
+    "dtkp_sum4_k5": ("dtkp", 5, _sum, lambda P: [DIGITS] * 4, _digit_inputs(4, 3), 17),
+    "dtkp_path_k3": ("dtkp", 3, _path, lambda P: [[P.Coord(*e) for e in _edges(20, 5, 0.45)]],
+                     lambda rng: [rng.uniform(0.05, 0.95, size=(4, len(_edges(20, 5, 0.45)))).astype(np.float32)
+                                  .astype(np.float64)], 18),
+    "dtkp_path_k5": ("dtkp", 5, _path, lambda P: [[P.Coord(*e) for e in _edges(21, 5, 0.45)]],
+                     lambda rng: [rng.uniform(0.05, 0.95, size=(4, len(_edges(21, 5, 0.45)))).astype(np.float32)
+                                  .astype(np.float64)], 19),
+    "damp_path": ("damp", None, _path, lambda P: [[P.Coord(*e) for e in _edges(22, 4, 0.5)]],
+                  lambda rng: [rng.uniform(0.05, 0.5, size=(4, len(_edges(22, 4, 0.5)))).astype(np.float32)
+                               .astype(np.float64)], 20),
+}
+
+
+def case_inputs(name):
+    prov, k, prog, syms, make, seed = CASES[name]
+    return make(np.random.default_rng(1000 + seed))
+
+
+def loss_weights(name, shape):
+    prov, k, prog, syms, make, seed = CASES[name]
+    return np.random.default_rng(5000 + seed).uniform(-1.0, 1.0, size=shape)
