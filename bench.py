@@ -1,0 +1,414 @@
+"""Benchmark of the Dolphin hot path on B200 (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): MNIST Sum-15 chained apply — 15 digit
+distributions folded by 14 ``apply(+)`` calls (output symbols 0..135), DAMP
+provenance, batch 16384 per GPU, synthetic digit probabilities resident in HBM.
+A step = forward (make_distribution x15, 14 applies, get_probs, loss_nll) + backward
+to the 15 input probability tensors.  The metric is symbol-combinations/s through
+``Distribution.apply``: units per step = B * sum_i |S1_i| * |S2_i| = B * 9590.
+
+value      device-timed (CUDA events) replay of the captured step (CUDA graph),
+           L2 flushed (512 MB write) before every timed step, max over ranks.
+e2e        the same step through the public Python API with host buffers: pinned
+           H2D of the inputs + targets, eager API calls, D2H of the loss, every step.
+roofline   dominant kernel of the step, algorithmic bytes / CUDA-event
+           duration per launch (cold L2), vs MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the reference symgrad (baseline/_ref, compiled backend) on a bounded
+           sample of the same workload on this host's cores (tools/ref_bench.py).
+
+``--impl reference`` runs only the reference CPU arm (rank 0) and prints its line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_DIGITS = 15
+DIGITS = list(range(10))
+METRIC = "apply symbol-combos/sec & train samples/sec (Sum-N, HWF) at 1/2/4/8 B200 vs host CPU"
+
+
+def combos_per_sample(n=N_DIGITS):
+    return sum(10 * (9 * i + 1) for i in range(1, n))
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU arm
+def cpu_reference(batch, repeats=3, port=False):
+    env = dict(os.environ)
+    cores = len(os.sched_getaffinity(0))
+    env["OPENBLAS_NUM_THREADS"] = str(cores)
+    cmd = [sys.executable, str(ROOT / "tools" / "ref_bench.py"), "--batch", str(batch), "--repeats", str(repeats)]
+    if port:
+        cmd.append("--port")
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900)
+    if out.returncode != 0:
+        raise RuntimeError(f"reference CPU arm failed:\n{out.stderr[-2000:]}")
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    ref = cpu_reference(args.cpu_batch, repeats=max(1, args.steps), port=False)
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": ref["value"],
+        "unit": ref["unit"],
+        "n_gpus": args.gpus,
+        "steps": max(1, args.steps),
+        "warmup": 1,
+        "ms_per_step": ref["seconds_per_step"] * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "MNIST Sum-15 chained apply, DAMP, fwd+bwd (BASELINE configs[1])",
+                   "global_batch": args.cpu_batch, "per_gpu_batch": None, "seq_len": None,
+                   "parallelism": "cpu", "l2": "n/a"},
+        "cpu_baseline": {"value": ref["value"], "unit": ref["unit"], "cores": ref["cores"], "kind": ref["kind"],
+                         "sample": ref["sample"]},
+        "e2e": {"value": ref["value"], "unit": ref["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "samples_per_s": ref["samples_per_s"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def make_inputs(torch, B, device, seed):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    x = torch.rand((N_DIGITS, B, 10), generator=g) * 0.95 + 0.05
+    x = x / x.sum(dim=2, keepdim=True)
+    t = torch.randint(0, 9 * N_DIGITS + 1, (B,), generator=g)
+    return x.float(), t
+
+
+def build_step(torch, sg, device):
+    from paper_2410_03348_b200 import programs as P
+    from paper_2410_03348_b200.learn import loss_nll
+
+    def step(xs, targets):
+        """xs: 15 leaf (B, 10) digit-probability tensors (the perception outputs)."""
+        ctx = sg.ProgramContext(sg.Damp(), device=device)
+        dists = [sg.make_distribution(ctx, x, DIGITS) for x in xs]
+        out = P.sum_n(ctx, dists)
+        probs = sg.get_probs(out)
+        loss = loss_nll(probs, targets)
+        gx = torch.autograd.grad(loss, xs)
+        return loss, gx
+
+    return step
+
+
+def kernel_roofline(torch, sg, device, B, flush, hbm_gbs, reps=3):
+    """Time every apply kernel of one Sum-15 step with CUDA events (cold L2 per launch)."""
+    import ctypes
+
+    from paper_2410_03348_b200 import _native as N
+    from paper_2410_03348_b200.plan import build_plan
+    from paper_2410_03348_b200.programs import _add
+
+    lib = N.load()
+    st = torch.cuda.current_stream(device)
+    syms = tuple(DIGITS)
+    kinds = {"damp_apply_fwd": [0.0, 0.0, 0], "damp_apply_bwd": [0.0, 0.0, 0]}
+    for i in range(1, N_DIGITS):
+        plan = build_plan(_add, None, [syms if i == 1 else tuple(range(9 * (i - 1) + 10)), syms])
+        kp = plan.kernel_plan()
+        s1, s2 = kp.sizes
+        a = torch.rand((s1, B), device=device)
+        b = torch.rand((s2, B), device=device)
+        out = torch.empty((kp.n_out, B), device=device)
+        g = torch.rand((kp.n_out, B), device=device)
+        ga = torch.empty_like(a)
+        gb = torch.empty_like(b)
+        s = kp.device(device).damp_struct(B)
+        fwd_bytes = 4 * B * (s1 + s2 + kp.n_out)
+        bwd_bytes = 4 * B * (kp.n_out + 2 * (s1 + s2))
+        for _ in range(reps):
+            for kind, call, nbytes in (
+                ("damp_apply_fwd", lambda: lib.sg_damp_apply_fwd(ctypes.byref(s), N.rows_array([a, b]), B,
+                                                                 out.data_ptr(), None, st.cuda_stream), fwd_bytes),
+                ("damp_apply_bwd", lambda: lib.sg_damp_apply_bwd(ctypes.byref(s), N.rows_array([a, b]), g.data_ptr(), B,
+                                                                 N.rows_array([ga, gb]), None, st.cuda_stream),
+                 bwd_bytes),
+            ):
+                flush()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                rc = call()
+                e1.record(st)
+                N.check(rc, kind)
+                e1.synchronize()
+                ms = e0.elapsed_time(e1)
+                kinds[kind][0] += ms
+                kinds[kind][1] += nbytes
+                kinds[kind][2] += 1
+    res = {}
+    for kind, (ms, nbytes, n) in kinds.items():
+        avg_ms = ms / n
+        avg_bytes = nbytes / n
+        gbs = avg_bytes / (avg_ms * 1e-3) / 1e9
+        res[kind] = {"launches": n, "avg_us": avg_ms * 1e3, "avg_bytes": avg_bytes, "achieved_gbs": gbs,
+                     "frac": gbs / hbm_gbs}
+    return res
+
+
+def run_gpu_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+
+    import paper_2410_03348_b200 as sg
+    from paper_2410_03348_b200 import _native as N
+
+    B = args.batch
+    pk, pk_src = peaks()
+    hbm = float(pk["hbm_gbs"])
+    x_h, t_h = make_inputs(torch, B, device, seed=1234 + rank)
+    x = [x_h[i].to(device).requires_grad_(True) for i in range(N_DIGITS)]
+    targets = t_h.to(device)
+    step = build_step(torch, sg, device)
+    flush_buf = torch.empty(512 * 1024 * 1024 // 4, device=device, dtype=torch.float32)
+
+    def flush():
+        flush_buf.zero_()
+
+    # warm-up (plans, device work lists, allocator) then capture the step in a CUDA graph
+    side = torch.cuda.Stream(device)
+    side.wait_stream(torch.cuda.current_stream(device))
+    with torch.cuda.stream(side):
+        for _ in range(max(3, args.warmup)):
+            step(x, targets)
+    torch.cuda.current_stream(device).wait_stream(side)
+    torch.cuda.synchronize(device)
+    graph = torch.cuda.CUDAGraph()
+    calls0 = N.CALLS["n"]
+    with torch.cuda.graph(graph):
+        s_loss, s_gx = step(x, targets)
+    launches = N.CALLS["n"] - calls0
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize(device)
+
+    # ---- device-timed steps (L2 flushed before each, flush excluded from the time)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.25)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush()
+        starts[i].record()
+        graph.replay()
+        ends[i].record()
+    torch.cuda.synchronize(device)
+    # keep the same load running ~1 s so the 100 ms nvidia-smi sampler sees it
+    t_end = time.perf_counter() + 1.0
+    while time.perf_counter() < t_end:
+        for _ in range(50):
+            graph.replay()
+        torch.cuda.synchronize(device)
+    clk = clocks.stop()
+    clk["window"] = "timed steps + 1 s of back-to-back step replays"
+    dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([dev_ms], device=device, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    units = world * B * combos_per_sample() * args.steps
+    value = units / (max_ms * 1e-3)
+
+    # ---- e2e through the public API with host buffers (eager, no graph)
+    x_pin = x_h.pin_memory()
+    t_pin = t_h.pin_memory()
+    e2e_steps = max(3, min(args.steps, 20))
+
+    def e2e_once():
+        xd = x_pin.to(device, non_blocking=True)
+        xs = [xd[i].detach().requires_grad_(True) for i in range(N_DIGITS)]
+        td = t_pin.to(device, non_blocking=True)
+        loss, _ = step(xs, td)
+        return loss.item()
+
+    for _ in range(2):
+        e2e_once()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(e2e_steps):
+        e2e_once()
+    e1.record()
+    torch.cuda.synchronize(device)
+    e2e_ms = e0.elapsed_time(e1)
+    t = torch.tensor([e2e_ms], device=device, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = world * B * combos_per_sample() * e2e_steps / (float(t.item()) * 1e-3)
+    h2d = x_h.numel() * 4 + t_h.numel() * 8
+    d2h = 8
+
+    # ---- per-kernel roofline (rank 0 only; cold L2 per launch)
+    roof = None
+    cpu = None
+    if rank == 0:
+        kr = kernel_roofline(torch, sg, device, B, flush, hbm)
+        dom_name = max(kr, key=lambda k: kr[k]["avg_us"] * kr[k]["launches"])
+        dom = kr[dom_name]
+        roof = {"bound": "hbm", "kernel": dom_name, "achieved": dom["achieved_gbs"], "peak": hbm, "unit": "GB/s",
+                "frac": dom["achieved_gbs"] / hbm, "traffic": None, "peak_source": pk_src,
+                "bytes_per_launch": dom["avg_bytes"], "avg_launch_us": dom["avg_us"], "kernels": kr}
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                ref = cpu_reference(args.cpu_batch, repeats=3)
+                cpu = {"value": ref["value"], "unit": ref["unit"], "cores": ref["cores"], "kind": ref["kind"],
+                       "sample": ref["sample"]}
+            except Exception as exc:  # noqa: BLE001 - reported, not fatal
+                cpu = {"value": None, "unit": "symbol-combos/s", "cores": None, "kind": "reference",
+                       "sample": f"failed: {exc}"[:300]}
+    if rank == 0:
+        ms_per_step = max_ms / args.steps
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "symbol-combos/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "MNIST Sum-15 chained apply (output symbols 0..135), DAMP, fwd+bwd "
+                                   "(BASELINE configs[1])",
+                       "global_batch": world * B, "per_gpu_batch": B, "seq_len": None,
+                       "parallelism": f"dp{world} (batch-sharded, no data-path collective)",
+                       "l2": "flushed (512 MB write) before every timed step", "cuda_graph": True},
+            "samples_per_s": world * B * args.steps / (max_ms * 1e-3),
+            "e2e": {"value": e2e_value, "unit": "symbol-combos/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": e2e_steps, "ms_per_step": float(t.item()) / e2e_steps},
+            "gpu_launches": launches * args.steps,
+            "gpu_launches_per_step": launches,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=16384, help="per-GPU batch")
+    ap.add_argument("--cpu-batch", type=int, default=2048, help="reference CPU sample batch")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -20,6 +20,7 @@
  *   sg_damp_apply_bwd   tensor.py:287 clamp bw, :415 affine bw, :240 mul bw, :386-391 select_rows bw
  *   sg_segsum_run       provenance.py:242-253 Damp.group_disj (and select_rows bw scatter-add)
  *   sg_damp_rows_add    provenance.py:239-240 Damp.disj; distribution.py:279-297 union
+ *   sg_nll_fwd/bwd      learn.py:92-119 loss_nll (the caller right after get_probs)
  *   sg_rows_gather      provenance.py:233-234 / :320-326 gather (filter, distribution.py:158-169)
  *   sg_to_symbol_major  provenance.py:223-225 Damp.input_tags (layout + fp32 cast of the block)
  *   sg_dtkp_apply       provenance.py:328-341 conj, :343-350 disj, :352-364 group_disj,
@@ -82,18 +83,42 @@ int sg_to_symbol_major(const void* src, int32_t src_dtype, int64_t B, int64_t n,
 int sg_from_symbol_major(const float* src, int64_t B, int64_t n, void* dst, int32_t dst_dtype,
                          int64_t stride_b, int64_t stride_n, sg_stream_t stream);
 
+/* A strided fp32 [rows][B] operand: element (r, b) lives at ptr[r * stride_row + b * stride_b].
+ * Symbol-major tags have (B, 1); a user (B, n) row-major block is read in place with (1, n);
+ * stride_b == 0 broadcasts a batch-1 operand (forward only). */
+typedef struct sg_rows {
+  float* ptr;
+  int64_t stride_row;
+  int64_t stride_b;
+} sg_rows;
+
 /* ---- DAMP (add-mult) --------------------------------------------------------------- */
-int sg_segsum_run(const sg_segsum* prob, const float* const* ops, const int32_t* op_rows,
-                  int32_t n_ops, int64_t B, int32_t clamp01, float* out, float* scratch,
+int sg_segsum_run(const sg_segsum* prob, const sg_rows* ops, const int32_t* op_rows,
+                  int32_t n_ops, int64_t B, int32_t clamp01, sg_rows out, float* scratch,
                   sg_stream_t stream);
-int sg_damp_apply_fwd(const sg_damp_plan* plan, const float* const* inputs, int64_t B,
+/* out: contiguous [n_out][B]; scratch: [fwd.n_partial][B] floats (may be NULL if 0). */
+int sg_damp_apply_fwd(const sg_damp_plan* plan, const sg_rows* inputs, int64_t B,
                       float* out, float* scratch, sg_stream_t stream);
-int sg_damp_apply_bwd(const sg_damp_plan* plan, const float* const* inputs,
-                      const float* grad_out, int64_t B, float* const* grad_in,
+/* grad_out: contiguous [n_out][B]; grad_in[k].ptr == NULL skips input k (the Toeplitz
+ * path needs both); scratch: [max_k bwd[k].n_partial][B] floats. */
+int sg_damp_apply_bwd(const sg_damp_plan* plan, const sg_rows* inputs,
+                      const float* grad_out, int64_t B, const sg_rows* grad_in,
                       float* scratch, sg_stream_t stream);
-/* out[r][b] = clamp01(A[ia[r]][b] + Bm[ib[r]][b]); index -1 contributes 0. */
-int sg_damp_rows_add(const float* A, const int32_t* ia, const float* Bm, const int32_t* ib,
+/* out[r][b] = clamp01(A[ia[r]][b] + Bm[ib[r]][b]) into contiguous [n_rows][B];
+ * index -1 contributes 0. */
+int sg_damp_rows_add(const sg_rows A, const int32_t* ia, const sg_rows Bm, const int32_t* ib,
                      int64_t n_rows, int64_t B, int32_t clamp01, float* out, sg_stream_t stream);
+
+/* ---- fused get_probs -> loss_nll (learn.py:92-119, pass-through clamps) ---------------
+ * loss = -(1/B) sum_b log(max(max(p[t_b][b] / (sum_n p[n][b] + 1e-8), 1e-12), 1e-12)),
+ * t_b = -1 marks "no mass" (the floor's penalty, no gradient).  fp64 inside.
+ * scratch: >= sg_nll_scratch_bytes(B) bytes, zero-initialised once (self-resetting). */
+int64_t sg_nll_scratch_bytes(int64_t B);
+int sg_nll_fwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, double* loss,
+               void* scratch, sg_stream_t stream);
+/* grad[n][b] = -(g/B) / c_b * (delta(n, t_b) / (s_b + 1e-8) - p[t_b][b] / (s_b + 1e-8)^2) */
+int sg_nll_bwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets,
+               const double* grad_loss, sg_rows grad, sg_stream_t stream);
 
 /* ---- row gather (filter / placement / inverse scatter), any tag kind -----------------
  * dst row r = src row idx[r] (idx -1 -> zero row); rows are row_bytes contiguous bytes. */

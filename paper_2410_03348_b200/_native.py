@@ -40,6 +40,10 @@ class SgSegsum(Structure):
     ]
 
 
+class SgRows(Structure):
+    _fields_ = [("ptr", c_void_p), ("stride_row", c_int64), ("stride_b", c_int64)]
+
+
 class SgDampPlan(Structure):
     _fields_ = [
         ("arity", c_int32),
@@ -88,17 +92,20 @@ EXPORTS = {
     "sg_from_symbol_major": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_int32, c_int64, c_int64, c_void_p]),
     "sg_segsum_run": (
         c_int32,
-        [POINTER(SgSegsum), POINTER(c_void_p), POINTER(c_int32), c_int32, c_int64, c_int32, c_void_p, c_void_p, c_void_p],
+        [POINTER(SgSegsum), POINTER(SgRows), POINTER(c_int32), c_int32, c_int64, c_int32, SgRows, c_void_p, c_void_p],
     ),
-    "sg_damp_apply_fwd": (c_int32, [POINTER(SgDampPlan), POINTER(c_void_p), c_int64, c_void_p, c_void_p, c_void_p]),
+    "sg_damp_apply_fwd": (c_int32, [POINTER(SgDampPlan), POINTER(SgRows), c_int64, c_void_p, c_void_p, c_void_p]),
     "sg_damp_apply_bwd": (
         c_int32,
-        [POINTER(SgDampPlan), POINTER(c_void_p), c_void_p, c_int64, POINTER(c_void_p), c_void_p, c_void_p],
+        [POINTER(SgDampPlan), POINTER(SgRows), c_void_p, c_int64, POINTER(SgRows), c_void_p, c_void_p],
     ),
     "sg_damp_rows_add": (
         c_int32,
-        [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p],
+        [SgRows, c_void_p, SgRows, c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p],
     ),
+    "sg_nll_scratch_bytes": (c_int64, [c_int64]),
+    "sg_nll_fwd": (c_int32, [SgRows, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sg_nll_bwd": (c_int32, [SgRows, c_int64, c_int64, c_void_p, c_void_p, SgRows, c_void_p]),
     "sg_rows_gather": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "sg_dtkp_apply": (c_int32, [POINTER(SgDtkpApplyDesc), c_void_p]),
     "sg_dtkp_probs_fwd": (
@@ -118,9 +125,30 @@ EXPORTS = {
 }
 
 _lib = None
+CALLS = {"n": 0}  # ABI calls issued (each launches one or two of our kernels)
 
 
-def load() -> ctypes.CDLL:
+class _Counted:
+    """Thin wrapper counting ABI calls (bench.py reports launches per step)."""
+
+    __slots__ = ("fn",)
+
+    def __init__(self, fn):
+        self.fn = fn
+
+    def __call__(self, *args):
+        CALLS["n"] += 1
+        return self.fn(*args)
+
+
+class _Lib:
+    def __init__(self, cdll):
+        self._cdll = cdll
+        for name in EXPORTS:
+            setattr(self, name, _Counted(getattr(cdll, name)))
+
+
+def load() -> "_Lib":
     """Load (once) and return the library; raises NativeError when it is absent."""
     global _lib
     if _lib is not None:
@@ -135,8 +163,8 @@ def load() -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    _lib = lib
-    return lib
+    _lib = _Lib(lib)
+    return _lib
 
 
 _CUDA_ERR = {1: "cudaErrorInvalidValue", 2: "cudaErrorMemoryAllocation", 98: "cudaErrorInvalidDeviceFunction",
@@ -154,6 +182,24 @@ def stream_ptr(device=None) -> int:
 
 def ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
+
+
+def rows(t) -> SgRows:
+    """A (rows, B) float32 tensor view as an sg_rows operand (any strides; NULL for None)."""
+    r = SgRows()
+    if t is not None:
+        r.ptr = t.data_ptr() if t.numel() else None
+        r.stride_row = t.stride(0)
+        r.stride_b = t.stride(1) if t.shape[1] > 1 else 0
+    return r
+
+
+def rows_array(tensors) -> ctypes.Array:
+    arr = (SgRows * MAX_ARITY)()
+    for i, t in enumerate(tensors):
+        if t is not None:
+            arr[i] = rows(t)
+    return arr
 
 
 def ptr_array(tensors) -> ctypes.Array:

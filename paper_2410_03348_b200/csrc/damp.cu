@@ -1,4 +1,4 @@
-// DAMP (add-mult) apply kernels for sm_100a.
+// DAMP (add-mult) kernels for sm_100a.
 //
 // K1 forward  out[o][b]  = clamp01( sum_{c in seg(o)} prod_i p_i[s_i(c)][b] )
 //      reference: distribution.py:262-270 -> provenance.py:233 gather, :236 conj (T.mul),
@@ -7,30 +7,83 @@
 //      reference: tensor.py:287 (clamp bw = identity), :415 (affine bw g @ G.T),
 //                 :240 (mul bw), :386-391 (select_rows bw np.add.at)
 //
-// Both are one "segmented sum of products" over memoised int32 records.  Layout is
-// symbol-major [rows][B]: lane == sample, so every operand row read by a warp is one
-// coalesced 128-byte line, index records are warp-uniform, and each output segment is
-// accumulated in a register (no atomics, no shared-memory read-modify-write).
+// Both are one "segmented sum of products" over memoised int32 records.  Operands are
+// strided [rows][B] views (sg_rows): tags our kernels produce are symbol-major (B, 1) so a
+// warp's 32 lanes (= 32 samples) read one coalesced 128-byte line per row; user (B, n)
+// classifier blocks are read in place with strides (1, n) — no layout copies.  Records
+// are warp-uniform, each segment accumulates in registers (no atomics, no shared-memory
+// read-modify-write), long segments spill partial rows to scratch and are finished by a
+// deterministic fix-up pass.
 //
-// Toeplitz fast path (T[s0][s1] == s0 + s1, e.g. every Sum-N fold step): the short
-// input lives in registers and the long input streams through a register window, so a
-// combination costs one FFMA and the kernel runs at the HBM roofline.
+// Toeplitz fast path (T[s0][s1] == s0 + s1 — every Sum-N fold step and the sum sweep):
+// the short input lives in registers and the long one streams through a register window,
+// so a combination costs one FFMA and the kernels are HBM-bound.
+//
+// All launches use programmatic dependent launch (PDL): a kernel's CTAs are scheduled
+// while the previous kernel drains and wait on `griddepcontrol.wait` before touching
+// global memory, hiding the launch gap between the short per-apply kernels.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace sg {
 
+struct Rows {
+  const float* p;
+  int64_t sr;  // stride between rows (symbols)
+  int64_t sb;  // stride between samples (0 = broadcast)
+  __device__ __forceinline__ float ld(int64_t r, int64_t b) const { return __ldg(p + r * sr + b * sb); }
+};
+
+struct WRows {
+  float* p;
+  int64_t sr;
+  int64_t sb;
+  __device__ __forceinline__ void st(int64_t r, int64_t b, float v) const { p[r * sr + b * sb] = v; }
+};
+
+__host__ __forceinline__ Rows rows_of(const sg_rows& r) { return Rows{r.ptr, r.stride_row, r.stride_b}; }
+__host__ __forceinline__ WRows wrows_of(const sg_rows& r) { return WRows{r.ptr, r.stride_row, r.stride_b}; }
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+static bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("SG_NO_PDL");
+    on = (e && e[0] == '1') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                          Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+// ------------------------------- generic segmented sum of products -------------------
 struct SegsumK {
-  const float* ops[SG_MAX_ARITY];
+  Rows ops[SG_MAX_ARITY];
   int32_t op_off[SG_MAX_ARITY];  // row offset of operand i inside the shared tile
   int32_t op_rows[SG_MAX_ARITY];
-  int32_t n_ops;
   int32_t clamp;
-  int32_t total_rows;
   int64_t B;
   const int32_t* recs;
   const int32_t* items;
   const int32_t* blk;
-  float* out;
+  WRows out;
   float* scratch;
 };
 
@@ -43,38 +96,43 @@ __global__ void __launch_bounds__(256) k_segsum(const SegsumK a) {
   const int64_t b = (int64_t)blockIdx.x * kWarp + lane;
   const bool bval = b < a.B;
   const int64_t bs = bval ? b : (a.B - 1);
+  pdl_wait();
 
   if constexpr (STAGED) {
 #pragma unroll
     for (int i = 0; i < NOPS; ++i) {
-      const float* __restrict__ src = a.ops[i] + bs;
+      const Rows src = a.ops[i];
       float* dst = tile + (size_t)a.op_off[i] * kWarp + lane;
       const int rows = a.op_rows[i];
       int r = warp;
       for (; r + 3 * nwarps < rows; r += 4 * nwarps) {
-        float v0 = __ldg(src + (size_t)r * a.B);
-        float v1 = __ldg(src + (size_t)(r + nwarps) * a.B);
-        float v2 = __ldg(src + (size_t)(r + 2 * nwarps) * a.B);
-        float v3 = __ldg(src + (size_t)(r + 3 * nwarps) * a.B);
+        float v0 = src.ld(r, bs);
+        float v1 = src.ld(r + nwarps, bs);
+        float v2 = src.ld(r + 2 * nwarps, bs);
+        float v3 = src.ld(r + 3 * nwarps, bs);
         dst[(size_t)r * kWarp] = v0;
         dst[(size_t)(r + nwarps) * kWarp] = v1;
         dst[(size_t)(r + 2 * nwarps) * kWarp] = v2;
         dst[(size_t)(r + 3 * nwarps) * kWarp] = v3;
       }
-      for (; r < rows; r += nwarps) dst[(size_t)r * kWarp] = __ldg(src + (size_t)r * a.B);
+      for (; r < rows; r += nwarps) dst[(size_t)r * kWarp] = src.ld(r, bs);
     }
     __syncthreads();
   }
 
   const float* opbase[NOPS];
+  int64_t ostride[NOPS];
 #pragma unroll
   for (int i = 0; i < NOPS; ++i) {
-    if constexpr (STAGED)
+    if constexpr (STAGED) {
       opbase[i] = tile + (size_t)a.op_off[i] * kWarp + lane;
-    else
-      opbase[i] = a.ops[i] + bs;
+      ostride[i] = kWarp;
+    } else {
+      opbase[i] = a.ops[i].p + bs * a.ops[i].sb;
+      ostride[i] = a.ops[i].sr;
+    }
   }
-  const int64_t rstride = STAGED ? kWarp : a.B;
+#define SG_VAL(i, row) (STAGED ? opbase[i][(row) * kWarp] : __ldg(opbase[i] + (int64_t)(row) * ostride[i]))
 
   const int it0 = __ldg(a.blk + blockIdx.y);
   const int it1 = __ldg(a.blk + blockIdx.y + 1);
@@ -86,44 +144,45 @@ __global__ void __launch_bounds__(256) k_segsum(const SegsumK a) {
     for (; c + 1 < item.z; c += 2, rp += 2 * RW) {
       Rec<RW> r0 = load_rec<RW>(rp);
       Rec<RW> r1 = load_rec<RW>(rp + RW);
-      float q0 = STAGED ? opbase[0][r0.v[0] * rstride] : __ldg(opbase[0] + (size_t)r0.v[0] * rstride);
-      float q1 = STAGED ? opbase[0][r1.v[0] * rstride] : __ldg(opbase[0] + (size_t)r1.v[0] * rstride);
+      float q0 = SG_VAL(0, r0.v[0]);
+      float q1 = SG_VAL(0, r1.v[0]);
 #pragma unroll
       for (int i = 1; i < NOPS; ++i) {
-        q0 *= STAGED ? opbase[i][r0.v[i] * rstride] : __ldg(opbase[i] + (size_t)r0.v[i] * rstride);
-        q1 *= STAGED ? opbase[i][r1.v[i] * rstride] : __ldg(opbase[i] + (size_t)r1.v[i] * rstride);
+        q0 *= SG_VAL(i, r0.v[i]);
+        q1 *= SG_VAL(i, r1.v[i]);
       }
       acc0 += q0;
       acc1 += q1;
     }
     if (c < item.z) {
       Rec<RW> r0 = load_rec<RW>(rp);
-      float q0 = STAGED ? opbase[0][r0.v[0] * rstride] : __ldg(opbase[0] + (size_t)r0.v[0] * rstride);
+      float q0 = SG_VAL(0, r0.v[0]);
 #pragma unroll
-      for (int i = 1; i < NOPS; ++i)
-        q0 *= STAGED ? opbase[i][r0.v[i] * rstride] : __ldg(opbase[i] + (size_t)r0.v[i] * rstride);
+      for (int i = 1; i < NOPS; ++i) q0 *= SG_VAL(i, r0.v[i]);
       acc0 += q0;
     }
-    float acc = acc0 + acc1;
+    const float acc = acc0 + acc1;
     if (bval) {
       if (item.w < 0)
-        a.out[(size_t)item.x * a.B + b] = a.clamp ? clamp01(acc) : acc;
+        a.out.st(item.x, b, a.clamp ? clamp01(acc) : acc);
       else
         a.scratch[(size_t)item.w * a.B + b] = acc;
     }
   }
+#undef SG_VAL
 }
 
 // Deterministic finish of segments spread over several items (pieces summed in order).
 __global__ void k_segsum_fixup(const int32_t* __restrict__ split, int n_split, const float* __restrict__ scratch,
-                               int64_t B, int clamp, float* __restrict__ out) {
+                               int64_t B, int clamp, WRows out) {
+  pdl_wait();
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   for (int s = blockIdx.y; s < n_split; s += gridDim.y) {
     const int seg = __ldg(split + 3 * s), p0 = __ldg(split + 3 * s + 1), p1 = __ldg(split + 3 * s + 2);
     float acc = 0.f;
     for (int q = p0; q < p1; ++q) acc += scratch[(size_t)q * B + b];
-    out[(size_t)seg * B + b] = clamp ? clamp01(acc) : acc;
+    out.st(seg, b, clamp ? clamp01(acc) : acc);
   }
 }
 
@@ -135,9 +194,8 @@ static int launch_segsum_t(const SegsumK& k, int n_blocks, size_t smem, cudaStre
                                          (int)smem);
     if (e != cudaSuccess) return (int)e;
   }
-  k_segsum<NOPS, RW, STAGED><<<grid, 256, STAGED ? smem : 0, st>>>(k);
-  SG_LAUNCH_CHECK();
-  return 0;
+  cudaError_t e = launch(k_segsum<NOPS, RW, STAGED>, grid, dim3(256), STAGED ? smem : 0, st, k);
+  return (int)e;
 }
 
 template <int NOPS, int RW>
@@ -148,27 +206,25 @@ static int launch_segsum_s(const SegsumK& k, bool staged, int n_blocks, size_t s
 
 static constexpr size_t kMaxStageBytes = 200 * 1024;
 
-static int run_segsum(const sg_segsum* p, const float* const* ops, const int32_t* op_rows, int n_ops, int64_t B,
-                      int clamp, float* out, float* scratch, cudaStream_t st) {
+static int run_segsum(const sg_segsum* p, const sg_rows* ops, const int32_t* op_rows, int n_ops, int64_t B, int clamp,
+                      sg_rows out, float* scratch, cudaStream_t st) {
   SG_RETURN_IF(n_ops < 1 || n_ops > SG_MAX_ARITY, cudaErrorInvalidValue);
   SG_RETURN_IF(p->rec_words < n_ops, cudaErrorInvalidValue);
   if (B <= 0 || p->n_seg <= 0) return 0;
   SegsumK k{};
   int total = 0;
   for (int i = 0; i < n_ops; ++i) {
-    k.ops[i] = ops[i];
+    k.ops[i] = rows_of(ops[i]);
     k.op_rows[i] = op_rows[i];
     k.op_off[i] = total;
     total += op_rows[i];
   }
-  k.n_ops = n_ops;
   k.clamp = clamp;
-  k.total_rows = total;
   k.B = B;
   k.recs = p->recs;
   k.items = p->items;
   k.blk = p->blk;
-  k.out = out;
+  k.out = wrows_of(out);
   k.scratch = scratch;
   const size_t smem = (size_t)total * kWarp * sizeof(float);
   const bool staged = p->staged && smem <= kMaxStageBytes;
@@ -190,37 +246,37 @@ static int run_segsum(const sg_segsum* p, const float* const* ops, const int32_t
   }
   if (p->n_split > 0) {
     dim3 grid(ceil_div(B, 128), p->n_split < 65535 ? p->n_split : 65535);
-    k_segsum_fixup<<<grid, 128, 0, st>>>(p->split, p->n_split, scratch, B, clamp, out);
-    SG_LAUNCH_CHECK();
+    cudaError_t e = launch(k_segsum_fixup, grid, dim3(128), 0, st, p->split, p->n_split, (const float*)scratch, B,
+                           clamp, wrows_of(out));
+    if (e != cudaSuccess) return (int)e;
   }
   return 0;
 }
 
 // ------------------------------- Toeplitz fast path -----------------------------------
 // out[o][b] = clamp01( sum_{j<KF} L[o-j][b] * S[j][b] ),  o in [0, nL + KF - 1)
-// Thread = (sample b, tile of R outputs). S lives in KF registers, L in a window of
-// R + KF - 1 registers: R*KF FFMA per (R + 2KF - 1) coalesced loads.
-constexpr int kConvR = 16;
-
-template <int KF>
-__global__ void __launch_bounds__(128) k_conv_fwd(const float* __restrict__ L, int nL, const float* __restrict__ S,
-                                                  float* __restrict__ out, int n_out, int64_t B, int n_tiles) {
+// Thread = (sample b, tile of R outputs): S in KF registers, L in a register window of
+// R + KF - 1 values; R * KF FFMA per (R + 2 KF - 1) loads.
+template <int KF, int R>
+__global__ void __launch_bounds__(128) k_conv_fwd(const Rows L, int nL, const Rows S, float* __restrict__ out,
+                                                  int n_out, int64_t B, int n_tiles) {
   const int lane = threadIdx.x;
   const int t = blockIdx.y * blockDim.y + threadIdx.y;
   const int64_t b = (int64_t)blockIdx.x * kWarp + lane;
+  pdl_wait();
   if (b >= B || t >= n_tiles) return;
-  constexpr int R = kConvR;
   constexpr int WN = R + KF - 1;
   const int o0 = t * R;
   float f[KF];
 #pragma unroll
-  for (int j = 0; j < KF; ++j) f[j] = __ldg(S + (size_t)j * B + b);
+  for (int j = 0; j < KF; ++j) f[j] = S.ld(j, b);
   float w[WN];
 #pragma unroll
   for (int i = 0; i < WN; ++i) {
     const int s = o0 - (KF - 1) + i;
-    w[i] = (s >= 0 && s < nL) ? __ldg(L + (size_t)s * B + b) : 0.f;
+    w[i] = (s >= 0 && s < nL) ? L.ld(s, b) : 0.f;
   }
+  pdl_trigger();
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     float acc = 0.f;
@@ -234,10 +290,9 @@ __global__ void __launch_bounds__(128) k_conv_fwd(const float* __restrict__ L, i
 // dL[s][b] = sum_j g[s+j][b] * S[j][b];   dS[j][b] = sum_s g[s+j][b] * L[s][b]
 // CTA = 32 samples x NW warps; warps stride over tiles of R positions of L, dS partials
 // are reduced across warps in shared memory in a fixed order (deterministic, no atomics).
-template <int KF>
-__global__ void __launch_bounds__(256) k_conv_bwd(const float* __restrict__ g, int n_out, const float* __restrict__ L,
-                                                  int nL, const float* __restrict__ S, float* __restrict__ dL,
-                                                  float* __restrict__ dS, int64_t B, int n_tiles) {
+template <int KF, int R>
+__global__ void __launch_bounds__(256) k_conv_bwd(const float* __restrict__ g, int n_out, const Rows L, int nL,
+                                                  const Rows S, WRows dL, WRows dS, int64_t B, int n_tiles) {
   __shared__ float red[8][KF][kWarp];
   const int lane = threadIdx.x;
   const int warp = threadIdx.y;
@@ -245,12 +300,12 @@ __global__ void __launch_bounds__(256) k_conv_bwd(const float* __restrict__ g, i
   const int64_t b0 = (int64_t)blockIdx.x * kWarp + lane;
   const bool bval = b0 < B;
   const int64_t b = bval ? b0 : B - 1;
-  constexpr int R = kConvR;
   constexpr int WN = R + KF - 1;
+  pdl_wait();
   float f[KF], d2[KF];
 #pragma unroll
   for (int j = 0; j < KF; ++j) {
-    f[j] = __ldg(S + (size_t)j * B + b);
+    f[j] = S.ld(j, b);
     d2[j] = 0.f;
   }
   for (int t = warp; t < n_tiles; t += nw) {
@@ -265,7 +320,7 @@ __global__ void __launch_bounds__(256) k_conv_bwd(const float* __restrict__ g, i
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int s = s0 + r;
-      pv[r] = (s < nL) ? __ldg(L + (size_t)s * B + b) : 0.f;
+      pv[r] = (s < nL) ? L.ld(s, b) : 0.f;
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -273,7 +328,7 @@ __global__ void __launch_bounds__(256) k_conv_bwd(const float* __restrict__ g, i
 #pragma unroll
       for (int j = 0; j < KF; ++j) acc = fmaf(gw[r + j], f[j], acc);
       const int s = s0 + r;
-      if (dL != nullptr && bval && s < nL) dL[(size_t)s * B + b] = acc;
+      if (bval && s < nL) dL.st(s, b, acc);
     }
 #pragma unroll
     for (int j = 0; j < KF; ++j) {
@@ -283,7 +338,7 @@ __global__ void __launch_bounds__(256) k_conv_bwd(const float* __restrict__ g, i
       d2[j] = acc;
     }
   }
-  if (dS == nullptr) return;
+  pdl_trigger();
 #pragma unroll
   for (int j = 0; j < KF; ++j) red[warp][j][lane] = d2[j];
   __syncthreads();
@@ -292,36 +347,40 @@ __global__ void __launch_bounds__(256) k_conv_bwd(const float* __restrict__ g, i
     for (int j = 0; j < KF; ++j) {
       float acc = red[0][j][lane];
       for (int w = 1; w < nw; ++w) acc += red[w][j][lane];
-      dS[(size_t)j * B + b] = acc;
+      dS.st(j, b, acc);
     }
   }
 }
 
 template <int KF>
-static int conv_fwd_t(const float* L, int nL, const float* S, float* out, int n_out, int64_t B, cudaStream_t st) {
-  const int n_tiles = ceil_div(n_out, kConvR);
+static int conv_fwd_t(const Rows& L, int nL, const Rows& S, float* out, int n_out, int64_t B, cudaStream_t st) {
+  constexpr int R = 16;
+  const int n_tiles = ceil_div(n_out, R);
   dim3 block(kWarp, 4);
   dim3 grid(ceil_div(B, kWarp), ceil_div(n_tiles, 4));
-  k_conv_fwd<KF><<<grid, block, 0, st>>>(L, nL, S, out, n_out, B, n_tiles);
-  SG_LAUNCH_CHECK();
-  return 0;
+  return (int)launch(k_conv_fwd<KF, R>, grid, block, 0, st, L, nL, S, out, n_out, B, n_tiles);
 }
 
 template <int KF>
-static int conv_bwd_t(const float* g, int n_out, const float* L, int nL, const float* S, float* dL, float* dS,
-                      int64_t B, cudaStream_t st) {
-  const int n_tiles = ceil_div(nL, kConvR);
+static int conv_bwd_t(const float* g, int n_out, const Rows& L, int nL, const Rows& S, const WRows& dL,
+                      const WRows& dS, int64_t B, cudaStream_t st) {
+  if (nL <= 64) {
+    constexpr int R = 8;
+    const int n_tiles = ceil_div(nL, R);
+    const int nw = n_tiles < 8 ? n_tiles : 8;
+    return (int)launch(k_conv_bwd<KF, R>, dim3(ceil_div(B, kWarp)), dim3(kWarp, nw), 0, st, g, n_out, L, nL, S, dL,
+                       dS, B, n_tiles);
+  }
+  constexpr int R = 16;
+  const int n_tiles = ceil_div(nL, R);
   const int nw = n_tiles < 8 ? n_tiles : 8;
-  dim3 block(kWarp, nw);
-  dim3 grid(ceil_div(B, kWarp));
-  k_conv_bwd<KF><<<grid, block, 0, st>>>(g, n_out, L, nL, S, dL, dS, B, n_tiles);
-  SG_LAUNCH_CHECK();
-  return 0;
+  return (int)launch(k_conv_bwd<KF, R>, dim3(ceil_div(B, kWarp)), dim3(kWarp, nw), 0, st, g, n_out, L, nL, S, dL, dS,
+                     B, n_tiles);
 }
 
 #define SG_CONV_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
 
-static int conv_fwd(int kf, const float* L, int nL, const float* S, float* out, int n_out, int64_t B, cudaStream_t st) {
+static int conv_fwd(int kf, const Rows& L, int nL, const Rows& S, float* out, int n_out, int64_t B, cudaStream_t st) {
   switch (kf) {
 #define X(K) \
   case K: return conv_fwd_t<K>(L, nL, S, out, n_out, B, st);
@@ -331,8 +390,8 @@ static int conv_fwd(int kf, const float* L, int nL, const float* S, float* out, 
   }
 }
 
-static int conv_bwd(int kf, const float* g, int n_out, const float* L, int nL, const float* S, float* dL, float* dS,
-                    int64_t B, cudaStream_t st) {
+static int conv_bwd(int kf, const float* g, int n_out, const Rows& L, int nL, const Rows& S, const WRows& dL,
+                    const WRows& dS, int64_t B, cudaStream_t st) {
   switch (kf) {
 #define X(K) \
   case K: return conv_bwd_t<K>(g, n_out, L, nL, S, dL, dS, B, st);
@@ -342,25 +401,98 @@ static int conv_bwd(int kf, const float* g, int n_out, const float* L, int nL, c
   }
 }
 
-// ------------------------------- row kernels ----------------------------------------
-__global__ void k_rows_add(const float* __restrict__ A, const int32_t* __restrict__ ia, const float* __restrict__ Bm,
+// ------------------------------- union / disjunction --------------------------------
+__global__ void k_rows_add(const Rows A, const int32_t* __restrict__ ia, const Rows Bm,
                            const int32_t* __restrict__ ib, int64_t n_rows, int64_t B, int clamp,
                            float* __restrict__ out) {
+  pdl_wait();
   for (int64_t r = blockIdx.y; r < n_rows; r += gridDim.y) {
-    const int xa = ia ? __ldg(ia + r) : -1;
-    const int xb = ib ? __ldg(ib + r) : -1;
+    const int xa = __ldg(ia + r);
+    const int xb = __ldg(ib + r);
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
       float v = 0.f;
-      if (xa >= 0) v += __ldg(A + (size_t)xa * B + b);
-      if (xb >= 0) v += __ldg(Bm + (size_t)xb * B + b);
+      if (xa >= 0) v += A.ld(xa, b);
+      if (xb >= 0) v += Bm.ld(xb, b);
       out[(size_t)r * B + b] = clamp ? clamp01(v) : v;
     }
   }
 }
 
+// ------------------------------- fused loss_nll -------------------------------------
+constexpr int kNllThreads = 256;
+
+__device__ __forceinline__ double nll_sample(const Rows& p, int n, int64_t b, int64_t t, double& s, double& pt) {
+  s = 0.0;
+  for (int r = 0; r < n; ++r) s += (double)p.ld(r, b);
+  pt = t >= 0 ? (double)p.ld(t, b) : 0.0;
+  const double norm = pt / (s + 1e-8);
+  const double fl = fmax(norm, 1e-12);
+  const double picked = t >= 0 ? fl : 0.0;
+  return fmax(picked, 1e-12);
+}
+
+__global__ void __launch_bounds__(kNllThreads) k_nll_fwd(const Rows p, int n, int64_t B,
+                                                         const int64_t* __restrict__ targets, double* __restrict__ loss,
+                                                         double* __restrict__ partial, unsigned* __restrict__ counter) {
+  __shared__ double red[kNllThreads / 32];
+  __shared__ bool last;
+  pdl_wait();
+  double acc = 0.0;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
+    double s, pt;
+    acc += log(nll_sample(p, n, b, __ldg(targets + b), s, pt));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w = 0; w < kNllThreads / 32; ++w) v += red[w];
+    partial[blockIdx.x] = v;
+    __threadfence();
+    const unsigned ticket = atomicAdd(counter, 1u);
+    last = ticket == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double v = 0.0;
+    for (unsigned i = 0; i < gridDim.x; ++i) v += ((volatile double*)partial)[i];
+    *loss = -v / (double)B;
+    *counter = 0u;  // self-reset for the next launch / graph replay
+  }
+}
+
+__global__ void __launch_bounds__(kNllThreads) k_nll_bwd(const Rows p, int n, int64_t B,
+                                                         const int64_t* __restrict__ targets,
+                                                         const double* __restrict__ gloss, WRows grad) {
+  pdl_wait();
+  const double g = *gloss;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = __ldg(targets + b);
+    double s, pt;
+    const double c = nll_sample(p, n, b, t, s, pt);
+    const double den = s + 1e-8;
+    const double coef = t >= 0 ? -(g / (double)B) / c : 0.0;
+    const double common = -pt / (den * den);
+    for (int r = 0; r < n; ++r) {
+      const double d = (r == t ? 1.0 / den : 0.0) + common;
+      grad.st(r, b, (float)(coef * d));
+    }
+  }
+}
+
+static int nll_grid(int64_t B) {
+  int g = ceil_div(B, kNllThreads);
+  return g < 1 ? 1 : (g > 148 * 4 ? 148 * 4 : g);
+}
+
+// ------------------------------- row gather / layout ---------------------------------
 template <typename V>
 __global__ void k_rows_gather(const V* __restrict__ src, const int32_t* __restrict__ idx, int64_t n_rows,
                               int64_t row_vecs, V* __restrict__ dst) {
+  pdl_wait();
   for (int64_t r = blockIdx.y; r < n_rows; r += gridDim.y) {
     const int x = __ldg(idx + r);
     V* d = dst + (size_t)r * row_vecs;
@@ -374,7 +506,6 @@ __global__ void k_rows_gather(const V* __restrict__ src, const int32_t* __restri
   }
 }
 
-// ------------------------------- layout kernels -------------------------------------
 template <typename T>
 __device__ __forceinline__ float to_f(T v) { return (float)v; }
 template <>
@@ -388,11 +519,12 @@ __device__ __forceinline__ __half from_f<__half>(float v) { return __float2half_
 template <>
 __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
-// dst[n][B] fp32 <- src(B, n) strided (32x32 tile transpose, both sides coalesced when possible)
+// dst[n][B] fp32 <- src(B, n) strided (32x32 tile transpose, both sides coalesced)
 template <typename T>
 __global__ void k_to_symbol_major(const T* __restrict__ src, int64_t B, int64_t n, int64_t sb, int64_t sn,
                                   float* __restrict__ dst) {
   __shared__ float t[32][33];
+  pdl_wait();
   const int64_t b0 = (int64_t)blockIdx.x * 32, n0 = (int64_t)blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int64_t bb = b0 + i, nn = n0 + threadIdx.x;
@@ -409,6 +541,7 @@ template <typename T>
 __global__ void k_from_symbol_major(const float* __restrict__ src, int64_t B, int64_t n, T* __restrict__ dst,
                                     int64_t sb, int64_t sn) {
   __shared__ float t[32][33];
+  pdl_wait();
   const int64_t b0 = (int64_t)blockIdx.x * 32, n0 = (int64_t)blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int64_t nn = n0 + i, bb = b0 + threadIdx.x;
@@ -427,7 +560,7 @@ using namespace sg;
 
 extern "C" {
 
-int sg_version(void) { return 1; }
+int sg_version(void) { return 2; }
 
 int sg_device_sm_count(int device) {
   int v = 0;
@@ -435,38 +568,42 @@ int sg_device_sm_count(int device) {
   return v;
 }
 
-int sg_segsum_run(const sg_segsum* prob, const float* const* ops, const int32_t* op_rows, int32_t n_ops, int64_t B,
-                  int32_t clamp01_, float* out, float* scratch, sg_stream_t stream) {
+int sg_segsum_run(const sg_segsum* prob, const sg_rows* ops, const int32_t* op_rows, int32_t n_ops, int64_t B,
+                  int32_t clamp01_, sg_rows out, float* scratch, sg_stream_t stream) {
   return run_segsum(prob, ops, op_rows, n_ops, B, clamp01_, out, scratch, (cudaStream_t)stream);
 }
 
-int sg_damp_apply_fwd(const sg_damp_plan* plan, const float* const* inputs, int64_t B, float* out, float* scratch,
+int sg_damp_apply_fwd(const sg_damp_plan* plan, const sg_rows* inputs, int64_t B, float* out, float* scratch,
                       sg_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   SG_RETURN_IF(plan->arity < 1 || plan->arity > SG_MAX_ARITY, cudaErrorInvalidValue);
+  if (B <= 0 || plan->n_out <= 0) return 0;
   if (plan->conv) {
     const int sh = plan->conv_short, lo = 1 - sh;
-    return conv_fwd(plan->sizes[sh], inputs[lo], plan->sizes[lo], inputs[sh], out, plan->n_out, B, st);
+    return conv_fwd(plan->sizes[sh], rows_of(inputs[lo]), plan->sizes[lo], rows_of(inputs[sh]), out, plan->n_out, B,
+                    st);
   }
-  return run_segsum(&plan->fwd, inputs, plan->sizes, plan->arity, B, 1, out, scratch, st);
+  sg_rows o{out, B, 1};
+  return run_segsum(&plan->fwd, inputs, plan->sizes, plan->arity, B, 1, o, scratch, st);
 }
 
-int sg_damp_apply_bwd(const sg_damp_plan* plan, const float* const* inputs, const float* grad_out, int64_t B,
-                      float* const* grad_in, float* scratch, sg_stream_t stream) {
+int sg_damp_apply_bwd(const sg_damp_plan* plan, const sg_rows* inputs, const float* grad_out, int64_t B,
+                      const sg_rows* grad_in, float* scratch, sg_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int n = plan->arity;
   SG_RETURN_IF(n < 1 || n > SG_MAX_ARITY, cudaErrorInvalidValue);
+  if (B <= 0) return 0;
   if (plan->conv) {
     const int sh = plan->conv_short, lo = 1 - sh;
-    if (grad_in[0] == nullptr && grad_in[1] == nullptr) return 0;
-    return conv_bwd(plan->sizes[sh], grad_out, plan->n_out, inputs[lo], plan->sizes[lo], inputs[sh], grad_in[lo],
-                    grad_in[sh], B, st);
+    SG_RETURN_IF(grad_in[0].ptr == nullptr || grad_in[1].ptr == nullptr, cudaErrorInvalidValue);
+    return conv_bwd(plan->sizes[sh], grad_out, plan->n_out, rows_of(inputs[lo]), plan->sizes[lo], rows_of(inputs[sh]),
+                    wrows_of(grad_in[lo]), wrows_of(grad_in[sh]), B, st);
   }
   for (int k = 0; k < n; ++k) {
-    if (grad_in[k] == nullptr) continue;
-    const float* ops[SG_MAX_ARITY];
+    if (grad_in[k].ptr == nullptr) continue;
+    sg_rows ops[SG_MAX_ARITY];
     int32_t rows[SG_MAX_ARITY];
-    ops[0] = grad_out;
+    ops[0] = sg_rows{const_cast<float*>(grad_out), B, 1};
     rows[0] = plan->n_out;
     int m = 1;
     for (int j = 0; j < n; ++j) {
@@ -481,16 +618,34 @@ int sg_damp_apply_bwd(const sg_damp_plan* plan, const float* const* inputs, cons
   return 0;
 }
 
-int sg_damp_rows_add(const float* A, const int32_t* ia, const float* Bm, const int32_t* ib, int64_t n_rows, int64_t B,
-                     int32_t clamp01_, float* out, sg_stream_t stream) {
+int sg_damp_rows_add(const sg_rows A, const int32_t* ia, const sg_rows Bm, const int32_t* ib, int64_t n_rows,
+                     int64_t B, int32_t clamp01_, float* out, sg_stream_t stream) {
   if (n_rows <= 0 || B <= 0) return 0;
   const int threads = 256;
   int gx = ceil_div(B, threads);
   if (gx > 64) gx = 64;
   dim3 grid(gx, n_rows < 65535 ? (unsigned)n_rows : 65535u);
-  k_rows_add<<<grid, threads, 0, (cudaStream_t)stream>>>(A, ia, Bm, ib, n_rows, B, clamp01_, out);
-  SG_LAUNCH_CHECK();
-  return 0;
+  return (int)launch(k_rows_add, grid, dim3(threads), 0, (cudaStream_t)stream, rows_of(A), ia, rows_of(Bm), ib,
+                     n_rows, B, (int)clamp01_, out);
+}
+
+int64_t sg_nll_scratch_bytes(int64_t B) { return (int64_t)(nll_grid(B) + 1) * (int64_t)sizeof(double); }
+
+int sg_nll_fwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, double* loss, void* scratch,
+               sg_stream_t stream) {
+  if (B <= 0) return 0;
+  const int grid = nll_grid(B);
+  double* partial = (double*)scratch;
+  unsigned* counter = (unsigned*)(partial + grid);
+  return (int)launch(k_nll_fwd, dim3(grid), dim3(kNllThreads), 0, (cudaStream_t)stream, rows_of(probs), (int)n, B,
+                     targets, loss, partial, counter);
+}
+
+int sg_nll_bwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, const double* grad_loss, sg_rows grad,
+               sg_stream_t stream) {
+  if (B <= 0) return 0;
+  return (int)launch(k_nll_bwd, dim3(nll_grid(B)), dim3(kNllThreads), 0, (cudaStream_t)stream, rows_of(probs), (int)n,
+                     B, targets, grad_loss, wrows_of(grad));
 }
 
 int sg_rows_gather(const void* src, const int32_t* idx, int64_t n_rows, int64_t row_bytes, void* dst,
@@ -500,20 +655,22 @@ int sg_rows_gather(const void* src, const int32_t* idx, int64_t n_rows, int64_t 
   const uintptr_t al = (uintptr_t)src | (uintptr_t)dst;
   dim3 grid(1, n_rows < 65535 ? (unsigned)n_rows : 65535u);
   const int threads = 256;
+  cudaError_t e;
   if (row_bytes % 16 == 0 && al % 16 == 0) {
     const int64_t v = row_bytes / 16;
     grid.x = ceil_div(v, threads) < 32 ? ceil_div(v, threads) : 32;
-    k_rows_gather<uint4><<<grid, threads, 0, st>>>((const uint4*)src, idx, n_rows, v, (uint4*)dst);
+    e = launch(k_rows_gather<uint4>, grid, dim3(threads), 0, st, (const uint4*)src, idx, n_rows, v, (uint4*)dst);
   } else if (row_bytes % 4 == 0 && al % 4 == 0) {
     const int64_t v = row_bytes / 4;
     grid.x = ceil_div(v, threads) < 32 ? ceil_div(v, threads) : 32;
-    k_rows_gather<uint32_t><<<grid, threads, 0, st>>>((const uint32_t*)src, idx, n_rows, v, (uint32_t*)dst);
+    e = launch(k_rows_gather<uint32_t>, grid, dim3(threads), 0, st, (const uint32_t*)src, idx, n_rows, v,
+               (uint32_t*)dst);
   } else {
     grid.x = ceil_div(row_bytes, threads) < 32 ? ceil_div(row_bytes, threads) : 32;
-    k_rows_gather<uint8_t><<<grid, threads, 0, st>>>((const uint8_t*)src, idx, n_rows, row_bytes, (uint8_t*)dst);
+    e = launch(k_rows_gather<uint8_t>, grid, dim3(threads), 0, st, (const uint8_t*)src, idx, n_rows, row_bytes,
+               (uint8_t*)dst);
   }
-  SG_LAUNCH_CHECK();
-  return 0;
+  return (int)e;
 }
 
 int sg_to_symbol_major(const void* src, int32_t src_dtype, int64_t B, int64_t n, int64_t stride_b, int64_t stride_n,
@@ -522,17 +679,16 @@ int sg_to_symbol_major(const void* src, int32_t src_dtype, int64_t B, int64_t n,
   dim3 block(32, 8), grid(ceil_div(B, 32), ceil_div(n, 32));
   cudaStream_t st = (cudaStream_t)stream;
   switch (src_dtype) {
-    case 0: k_to_symbol_major<float><<<grid, block, 0, st>>>((const float*)src, B, n, stride_b, stride_n, dst); break;
-    case 1: k_to_symbol_major<double><<<grid, block, 0, st>>>((const double*)src, B, n, stride_b, stride_n, dst); break;
-    case 2: k_to_symbol_major<__half><<<grid, block, 0, st>>>((const __half*)src, B, n, stride_b, stride_n, dst); break;
-    case 3:
-      k_to_symbol_major<__nv_bfloat16><<<grid, block, 0, st>>>((const __nv_bfloat16*)src, B, n, stride_b, stride_n,
-                                                                 dst);
-      break;
+    case 0: return (int)launch(k_to_symbol_major<float>, grid, block, 0, st, (const float*)src, B, n, stride_b,
+                               stride_n, dst);
+    case 1: return (int)launch(k_to_symbol_major<double>, grid, block, 0, st, (const double*)src, B, n, stride_b,
+                               stride_n, dst);
+    case 2: return (int)launch(k_to_symbol_major<__half>, grid, block, 0, st, (const __half*)src, B, n, stride_b,
+                               stride_n, dst);
+    case 3: return (int)launch(k_to_symbol_major<__nv_bfloat16>, grid, block, 0, st, (const __nv_bfloat16*)src, B, n,
+                               stride_b, stride_n, dst);
     default: return (int)cudaErrorInvalidValue;
   }
-  SG_LAUNCH_CHECK();
-  return 0;
 }
 
 int sg_from_symbol_major(const float* src, int64_t B, int64_t n, void* dst, int32_t dst_dtype, int64_t stride_b,
@@ -541,16 +697,16 @@ int sg_from_symbol_major(const float* src, int64_t B, int64_t n, void* dst, int3
   dim3 block(32, 8), grid(ceil_div(B, 32), ceil_div(n, 32));
   cudaStream_t st = (cudaStream_t)stream;
   switch (dst_dtype) {
-    case 0: k_from_symbol_major<float><<<grid, block, 0, st>>>(src, B, n, (float*)dst, stride_b, stride_n); break;
-    case 1: k_from_symbol_major<double><<<grid, block, 0, st>>>(src, B, n, (double*)dst, stride_b, stride_n); break;
-    case 2: k_from_symbol_major<__half><<<grid, block, 0, st>>>(src, B, n, (__half*)dst, stride_b, stride_n); break;
-    case 3:
-      k_from_symbol_major<__nv_bfloat16><<<grid, block, 0, st>>>(src, B, n, (__nv_bfloat16*)dst, stride_b, stride_n);
-      break;
+    case 0: return (int)launch(k_from_symbol_major<float>, grid, block, 0, st, src, B, n, (float*)dst, stride_b,
+                               stride_n);
+    case 1: return (int)launch(k_from_symbol_major<double>, grid, block, 0, st, src, B, n, (double*)dst, stride_b,
+                               stride_n);
+    case 2: return (int)launch(k_from_symbol_major<__half>, grid, block, 0, st, src, B, n, (__half*)dst, stride_b,
+                               stride_n);
+    case 3: return (int)launch(k_from_symbol_major<__nv_bfloat16>, grid, block, 0, st, src, B, n,
+                               (__nv_bfloat16*)dst, stride_b, stride_n);
     default: return (int)cudaErrorInvalidValue;
   }
-  SG_LAUNCH_CHECK();
-  return 0;
 }
 
 }  // extern "C"

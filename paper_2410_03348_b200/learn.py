@@ -1,0 +1,79 @@
+"""Training-side callers of the hot path: the reference loss convention and a LeNet
+perception model for data-parallel training over NCCL.
+
+``loss_nll`` follows learn.py:92-119 exactly, including its gradient convention: both
+floors are ``clamp`` with a pass-through backward (tensor.py:275-287), which plain
+``torch.clamp`` would mask.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.nn as nn
+import torch.nn.functional as F
+
+__all__ = ["PassClamp", "loss_nll", "loss_nll_torch", "LeNet"]
+
+
+class PassClamp(torch.autograd.Function):
+    """clamp(x, lo, hi) whose backward is the identity everywhere (tensor.py:275-287)."""
+
+    @staticmethod
+    def forward(ctx, x, lo, hi):
+        return x.clamp(lo, hi)
+
+    @staticmethod
+    def backward(ctx, g):
+        return g, None, None
+
+
+def loss_nll(probs: torch.Tensor, targets) -> torch.Tensor:
+    """Mean negative log-likelihood of normalised program outputs (learn.py:92-119).
+
+    ``probs`` is ``get_probs(out)`` (batch, n); ``targets`` holds the output-symbol index
+    per sample, -1 for "no mass" (None in the reference), which contributes the floor's
+    log penalty.  Runs as one fused sm_100a kernel forward and one backward (fp64 inside,
+    float64 scalar loss).
+    """
+    from . import ops
+
+    if not isinstance(targets, torch.Tensor):
+        targets = torch.as_tensor([(-1 if t is None else int(t)) for t in targets], dtype=torch.int64)
+    targets = targets.to(device=probs.device, dtype=torch.int64).contiguous()
+    if probs.dtype != torch.float32:
+        probs = probs.float()
+    return ops.NllLoss.apply(probs.t(), targets)
+
+
+def loss_nll_torch(probs: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+    """The same loss composed from torch ops (reference check for the fused kernel)."""
+    b, n = probs.shape
+    p = probs.double()
+    rowsum = p.sum(dim=1, keepdim=True)
+    norm = p / (rowsum + 1e-8)
+    floored = PassClamp.apply(norm, 1e-12, float("inf"))
+    valid = targets >= 0
+    idx = targets.clamp(min=0).long().view(b, 1)
+    picked = floored.gather(1, idx).view(b) * valid.to(p.dtype)
+    total = torch.log(PassClamp.apply(picked, 1e-12, float("inf"))).sum()
+    return total * (-1.0 / b)
+
+
+class LeNet(nn.Module):
+    """LeNet-5 style digit/token classifier for 28x28 inputs, softmax output."""
+
+    def __init__(self, n_classes: int = 10):
+        super().__init__()
+        self.conv1 = nn.Conv2d(1, 6, 5, padding=2)
+        self.conv2 = nn.Conv2d(6, 16, 5)
+        self.fc1 = nn.Linear(16 * 5 * 5, 120)
+        self.fc2 = nn.Linear(120, 84)
+        self.fc3 = nn.Linear(84, n_classes)
+
+    def forward(self, x):
+        x = F.max_pool2d(F.relu(self.conv1(x)), 2)
+        x = F.max_pool2d(F.relu(self.conv2(x)), 2)
+        x = x.flatten(1)
+        x = F.relu(self.fc1(x))
+        x = F.relu(self.fc2(x))
+        return F.softmax(self.fc3(x), dim=1)

@@ -33,13 +33,13 @@ def _lib():
 
 def _check_operand(t: torch.Tensor, what: str):
     N.require_cuda(t, what)
-    if t.dtype != F32 or not t.is_contiguous():
-        raise N.NativeError(f"{what}: expected contiguous float32 [rows][B], got {t.dtype} {tuple(t.shape)}")
+    if t.dtype != F32 or t.ndim != 2:
+        raise N.NativeError(f"{what}: expected a float32 (rows, B) view, got {t.dtype} {tuple(t.shape)}")
 
 
 # ------------------------------------------------------------------------ layout
 class ToSymbolMajor(torch.autograd.Function):
-    """(B, n) user probabilities (any float dtype/strides) -> [n][B] fp32 (Damp.input_tags)."""
+    """(B, n) any float dtype/strides -> contiguous [n][B] fp32 (explicit re-layout)."""
 
     @staticmethod
     def forward(ctx, x: torch.Tensor):
@@ -69,13 +69,21 @@ def to_symbol_major(x: torch.Tensor) -> torch.Tensor:
     return ToSymbolMajor.apply(x)
 
 
+def symbol_view(probs: torch.Tensor) -> torch.Tensor:
+    """A user (B, n) block as the (n, B) operand view the kernels read in place (fp32)."""
+    N.require_cuda(probs, "probabilities")
+    if probs.dtype != F32:
+        probs = probs.float()
+    return probs.t()
+
+
 def expand_batch(x: torch.Tensor, B: int) -> torch.Tensor:
-    """[rows][1] -> [rows][B] (torch sums the gradient back over the batch)."""
+    """(rows, 1) -> (rows, B) stride-0 view (torch sums the gradient back over the batch)."""
     if x.shape[1] == B:
         return x
     if x.shape[1] != 1:
         raise ValueError(f"cannot broadcast batch {x.shape[1]} to {B}")
-    return x.expand(x.shape[0], B).contiguous()
+    return x.expand(x.shape[0], B)
 
 
 # ------------------------------------------------------------------------ DAMP apply
@@ -90,19 +98,19 @@ class DampApply(torch.autograd.Function):
         dplan = kplan.device(dev)
         out = torch.empty((kplan.n_out, B), device=dev, dtype=F32)
         st = N.stream_ptr(dev)
+        ops_ = N.rows_array(inputs)
         if kplan.clamp:
             s = dplan.damp_struct(B)
             scratch = None
             if not kplan.conv and s.fwd.n_partial:
                 scratch = torch.empty((s.fwd.n_partial, B), device=dev, dtype=F32)
-            rc = _lib().sg_damp_apply_fwd(ctypes.byref(s), N.ptr_array(inputs), B, out.data_ptr(), N.ptr(scratch), st)
+            rc = _lib().sg_damp_apply_fwd(ctypes.byref(s), ops_, B, out.data_ptr(), N.ptr(scratch), st)
             N.check(rc, "sg_damp_apply_fwd")
         else:
             seg = dplan.fwd().struct(B)
             scratch = torch.empty((seg.n_partial, B), device=dev, dtype=F32) if seg.n_partial else None
             rows = (ctypes.c_int32 * N.MAX_ARITY)(*kplan.sizes)
-            rc = _lib().sg_segsum_run(ctypes.byref(seg), N.ptr_array(inputs), rows, kplan.arity, B, 0, out.data_ptr(),
-                                      N.ptr(scratch), st)
+            rc = _lib().sg_segsum_run(ctypes.byref(seg), ops_, rows, kplan.arity, B, 0, N.rows(out), N.ptr(scratch), st)
             N.check(rc, "sg_segsum_run")
         ctx.kplan = kplan
         ctx.B = B
@@ -120,18 +128,14 @@ class DampApply(torch.autograd.Function):
         grads = [None] * len(inputs)
         if need:
             dplan = kplan.device(dev)
-            for i in need:
+            alloc = range(2) if kplan.conv else need  # the fused Toeplitz backward writes both
+            for i in alloc:
                 grads[i] = torch.empty_like(inputs[i])
-            if kplan.conv:
-                # the fused Toeplitz backward writes both gradients in one pass
-                for i in range(2):
-                    if grads[i] is None:
-                        grads[i] = torch.empty_like(inputs[i])
             s = dplan.damp_struct(B, need_bwd=() if kplan.conv else need)
             n_partial = 0 if kplan.conv else max((s.bwd[i].n_partial for i in need), default=0)
             scratch = torch.empty((n_partial, B), device=dev, dtype=F32) if n_partial else None
-            rc = _lib().sg_damp_apply_bwd(ctypes.byref(s), N.ptr_array(inputs), g.data_ptr(), B, N.ptr_array(grads),
-                                          N.ptr(scratch), N.stream_ptr(dev))
+            rc = _lib().sg_damp_apply_bwd(ctypes.byref(s), N.rows_array(inputs), g.data_ptr(), B,
+                                          N.rows_array(grads), N.ptr(scratch), N.stream_ptr(dev))
             N.check(rc, "sg_damp_apply_bwd")
             if kplan.conv:
                 grads = [gr if ctx.needs_input_grad[2 + i] else None for i, gr in enumerate(grads)]
@@ -159,6 +163,7 @@ class _IndexMap:
 
 
 _MAP_CACHE: "dict[tuple, _IndexMap]" = {}
+_GATHER_CACHE: "dict[tuple, KernelPlan]" = {}
 
 
 def index_map(indices, n_src: int, device) -> _IndexMap:
@@ -173,6 +178,20 @@ def index_map(indices, n_src: int, device) -> _IndexMap:
     return m
 
 
+def gather_plan(indices, n_src: int) -> KernelPlan:
+    """out[r] = src[idx[r]] (0 for idx -1) as an arity-1 segmented plan (backward: scatter-add)."""
+    arr = np.asarray(indices, dtype=np.int32).reshape(-1)
+    key = (int(n_src), arr.tobytes())
+    kp = _GATHER_CACHE.get(key)
+    if kp is None:
+        if len(_GATHER_CACHE) > 4096:
+            _GATHER_CACHE.clear()
+        keep = np.nonzero(arr >= 0)[0].astype(np.int32)
+        kp = KernelPlan(arr[keep].reshape(-1, 1), keep, len(arr), (int(n_src),), clamp=False)
+        _GATHER_CACHE[key] = kp
+    return kp
+
+
 def scatter_rows_sum(g: torch.Tensor, imap: _IndexMap) -> torch.Tensor:
     return DampApply.apply(imap.bwd, g.shape[1], g.contiguous())
 
@@ -184,11 +203,10 @@ class DampRowsAdd(torch.autograd.Function):
     def forward(ctx, A, Bm, ma: _IndexMap, mb: _IndexMap, clamp: bool):
         _check_operand(A, "disj lhs")
         _check_operand(Bm, "disj rhs")
-        B = A.shape[1]
+        B = max(A.shape[1], Bm.shape[1])
         n = int(ma.idx.numel())
         out = torch.empty((n, B), device=A.device, dtype=F32)
-        rc = _lib().sg_damp_rows_add(A.data_ptr() if A.numel() else None, ma.idx.data_ptr(),
-                                     Bm.data_ptr() if Bm.numel() else None, mb.idx.data_ptr(), n, B,
+        rc = _lib().sg_damp_rows_add(N.rows(A), ma.idx.data_ptr(), N.rows(Bm), mb.idx.data_ptr(), n, B,
                                      1 if clamp else 0, out.data_ptr(), N.stream_ptr(A.device))
         N.check(rc, "sg_damp_rows_add")
         ctx.maps = (ma, mb)
@@ -202,25 +220,36 @@ class DampRowsAdd(torch.autograd.Function):
         return ga, gb, None, None, None
 
 
-class RowsGather(torch.autograd.Function):
-    """Symbol-axis gather of DAMP rows (filter / gather / placement)."""
+class NllLoss(torch.autograd.Function):
+    """Fused get_probs -> loss_nll (learn.py:92-119) over an (n, B) probability view."""
 
     @staticmethod
-    def forward(ctx, x, imap: _IndexMap):
-        _check_operand(x, "gather source")
-        n = int(imap.idx.numel())
-        out = torch.empty((n, x.shape[1]), device=x.device, dtype=F32)
-        rows_gather(x, imap.idx, out)
-        ctx.imap = imap
-        return out
+    def forward(ctx, probs_nb: torch.Tensor, targets: torch.Tensor):
+        _check_operand(probs_nb, "loss probabilities")
+        n, B = probs_nb.shape
+        dev = probs_nb.device
+        loss = torch.empty((), device=dev, dtype=torch.float64)
+        scratch = torch.zeros(int(_lib().sg_nll_scratch_bytes(B)), device=dev, dtype=torch.uint8)
+        rc = _lib().sg_nll_fwd(N.rows(probs_nb), n, B, targets.data_ptr(), loss.data_ptr(), scratch.data_ptr(),
+                               N.stream_ptr(dev))
+        N.check(rc, "sg_nll_fwd")
+        ctx.save_for_backward(probs_nb, targets)
+        return loss
 
     @staticmethod
-    def backward(ctx, g):
-        return scatter_rows_sum(g, ctx.imap), None
+    def backward(ctx, gloss):
+        probs_nb, targets = ctx.saved_tensors
+        n, B = probs_nb.shape
+        g = gloss.detach().to(torch.float64).reshape(()).contiguous()
+        grad = torch.empty_like(probs_nb)
+        rc = _lib().sg_nll_bwd(N.rows(probs_nb), n, B, targets.data_ptr(), g.data_ptr(), N.rows(grad),
+                               N.stream_ptr(probs_nb.device))
+        N.check(rc, "sg_nll_bwd")
+        return grad, None
 
 
 def rows_gather(src: torch.Tensor, idx: torch.Tensor, out: torch.Tensor):
-    """Copy whole symbol rows (any tag kind): out[r] = src[idx[r]] or zeros for -1."""
+    """Copy whole contiguous symbol rows (DTKP tags): out[r] = src[idx[r]] or zeros for -1."""
     n = int(idx.numel())
     if n == 0 or out.numel() == 0:
         return out

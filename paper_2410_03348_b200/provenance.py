@@ -110,7 +110,7 @@ class InputRegistry:
             raise ProvenanceError("registry holds no input symbols")
         b = self.batch
         parts = [ops.expand_batch(p, b) for p in self._parts]
-        out = parts[0] if len(parts) == 1 else torch.cat(parts, dim=0)
+        out = parts[0].contiguous() if len(parts) == 1 else torch.cat(parts, dim=0)
         if self._frozen:
             self._prob_cache = out
         return out
@@ -139,7 +139,7 @@ class DampTags:
             v = _as_probs(value, _default_device())
             if v.ndim != 2:
                 raise ValueError("DampTags value must be (batch, n)")
-            sm = ops.to_symbol_major(v)
+            sm = ops.symbol_view(v)
         self.sm = sm
 
     @property
@@ -166,7 +166,8 @@ class Damp:
     k = None
 
     def input_tags(self, registry, ids, probs) -> DampTags:
-        sm = ops.to_symbol_major(_as_probs(probs, registry._dev()))
+        """The classifier block is read in place as an (n, B) view — no layout copy."""
+        sm = ops.symbol_view(_as_probs(probs, registry._dev()))
         registry.add_block(ids, sm)
         return _damp(sm)
 
@@ -177,8 +178,7 @@ class Damp:
         return _damp(torch.ones((n, b), device=registry._dev(), dtype=torch.float32))
 
     def gather(self, tags: DampTags, indices) -> DampTags:
-        imap = ops.index_map(indices, tags.count, tags.sm.device)
-        return _damp(ops.RowsGather.apply(tags.sm, imap))
+        return _damp(ops.damp_apply(ops.gather_plan(indices, tags.count), [tags.sm], tags.batch))
 
     def conj(self, a: DampTags, b: DampTags) -> DampTags:
         n = max(a.count, b.count)
@@ -219,8 +219,7 @@ class Damp:
         return tags.sm.detach().t().double().cpu().numpy()
 
     def placed(self, tags: DampTags, placement: np.ndarray) -> DampTags:
-        return _damp(ops.RowsGather.apply(tags.sm, ops.index_map(_placement_src(placement), tags.count,
-                                                                  tags.sm.device)))
+        return _damp(ops.damp_apply(ops.gather_plan(_placement_src(placement), tags.count), [tags.sm], tags.batch))
 
     def stack_parts(self, parts) -> DampTags:
         return _damp(torch.cat([p.sm for p in parts], dim=1))
@@ -405,7 +404,7 @@ class DtkpAm:
 
     # ---- construction ----------------------------------------------------------------
     def input_tags(self, registry, ids, probs) -> DtkpTags:
-        sm = ops.to_symbol_major(_as_probs(probs, registry._dev()))
+        sm = ops.symbol_view(_as_probs(probs, registry._dev()))
         start = registry.add_block(ids, sm)
         n, b = sm.shape
         W = _words(registry.size)
