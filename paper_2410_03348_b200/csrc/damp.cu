@@ -255,16 +255,20 @@ static int run_segsum(const sg_segsum* p, const sg_rows* ops, const int32_t* op_
 
 // ------------------------------- Toeplitz fast path -----------------------------------
 // out[o][b] = clamp01( sum_{j<KF} L[o-j][b] * S[j][b] ),  o in [0, nL + KF - 1)
-// Thread = (sample b, tile of R outputs): S in KF registers, L in a register window of
-// R + KF - 1 values; R * KF FFMA per (R + 2 KF - 1) loads.
+// Warp = (32 samples, tile of R outputs); the grid is 1-D over (sample group, tile) pairs
+// so the launch is a single full wave (no wave quantisation at B = 16384).  S lives in KF
+// registers, L in a register window of R + KF - 1 values: R * KF FFMA per R + 2 KF - 1
+// coalesced loads, every load issued before the first FFMA (memory-level parallelism).
 template <int KF, int R>
-__global__ void __launch_bounds__(128) k_conv_fwd(const Rows L, int nL, const Rows S, float* __restrict__ out,
-                                                  int n_out, int64_t B, int n_tiles) {
-  const int lane = threadIdx.x;
-  const int t = blockIdx.y * blockDim.y + threadIdx.y;
-  const int64_t b = (int64_t)blockIdx.x * kWarp + lane;
+__global__ void __launch_bounds__(128, 8) k_conv_fwd(const Rows L, int nL, const Rows S, float* __restrict__ out,
+                                                     int n_out, int64_t B, int n_tiles, int n_pairs) {
+  const int lane = threadIdx.x & 31;
+  const int pair = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   pdl_wait();
-  if (b >= B || t >= n_tiles) return;
+  if (pair >= n_pairs) return;
+  const int grp = pair / n_tiles, t = pair - grp * n_tiles;
+  const int64_t b = (int64_t)grp * kWarp + lane;
+  if (b >= B) return;
   constexpr int WN = R + KF - 1;
   const int o0 = t * R;
   float f[KF];
@@ -288,12 +292,15 @@ __global__ void __launch_bounds__(128) k_conv_fwd(const Rows L, int nL, const Ro
 }
 
 // dL[s][b] = sum_j g[s+j][b] * S[j][b];   dS[j][b] = sum_s g[s+j][b] * L[s][b]
-// CTA = 32 samples x NW warps; warps stride over tiles of R positions of L, dS partials
-// are reduced across warps in shared memory in a fixed order (deterministic, no atomics).
+// CTA = one group of 32 samples, one warp per tile of R positions of L (warps loop when
+// there are more than 16 tiles).  S is staged once per CTA in shared memory; the dS
+// partials of the tiles are reduced across warps in a fixed order (deterministic, no
+// atomics) and written by warp 0.
 template <int KF, int R>
-__global__ void __launch_bounds__(256) k_conv_bwd(const float* __restrict__ g, int n_out, const Rows L, int nL,
-                                                  const Rows S, WRows dL, WRows dS, int64_t B, int n_tiles) {
-  __shared__ float red[8][KF][kWarp];
+__global__ void __launch_bounds__(512, 2) k_conv_bwd(const float* __restrict__ g, int n_out, const Rows L, int nL,
+                                                     const Rows S, WRows dL, WRows dS, int64_t B, int n_tiles) {
+  __shared__ float sS[KF][kWarp];
+  __shared__ float red[16][KF][kWarp];
   const int lane = threadIdx.x;
   const int warp = threadIdx.y;
   const int nw = blockDim.y;
@@ -302,10 +309,12 @@ __global__ void __launch_bounds__(256) k_conv_bwd(const float* __restrict__ g, i
   const int64_t b = bval ? b0 : B - 1;
   constexpr int WN = R + KF - 1;
   pdl_wait();
+  for (int j = warp; j < KF; j += nw) sS[j][lane] = S.ld(j, b);
+  __syncthreads();
   float f[KF], d2[KF];
 #pragma unroll
   for (int j = 0; j < KF; ++j) {
-    f[j] = S.ld(j, b);
+    f[j] = sS[j][lane];
     d2[j] = 0.f;
   }
   for (int t = warp; t < n_tiles; t += nw) {
@@ -342,13 +351,10 @@ __global__ void __launch_bounds__(256) k_conv_bwd(const float* __restrict__ g, i
 #pragma unroll
   for (int j = 0; j < KF; ++j) red[warp][j][lane] = d2[j];
   __syncthreads();
-  if (warp == 0 && bval) {
-#pragma unroll
-    for (int j = 0; j < KF; ++j) {
-      float acc = red[0][j][lane];
-      for (int w = 1; w < nw; ++w) acc += red[w][j][lane];
-      dS.st(j, b, acc);
-    }
+  for (int j = warp; j < KF; j += nw) {
+    float acc = red[0][j][lane];
+    for (int w = 1; w < nw; ++w) acc += red[w][j][lane];
+    if (bval) dS.st(j, b, acc);
   }
 }
 
@@ -356,24 +362,17 @@ template <int KF>
 static int conv_fwd_t(const Rows& L, int nL, const Rows& S, float* out, int n_out, int64_t B, cudaStream_t st) {
   constexpr int R = 16;
   const int n_tiles = ceil_div(n_out, R);
-  dim3 block(kWarp, 4);
-  dim3 grid(ceil_div(B, kWarp), ceil_div(n_tiles, 4));
-  return (int)launch(k_conv_fwd<KF, R>, grid, block, 0, st, L, nL, S, out, n_out, B, n_tiles);
+  const int n_pairs = ceil_div(B, kWarp) * n_tiles;
+  return (int)launch(k_conv_fwd<KF, R>, dim3(ceil_div(n_pairs, 4)), dim3(128), 0, st, L, nL, S, out, n_out, B,
+                     n_tiles, n_pairs);
 }
 
 template <int KF>
 static int conv_bwd_t(const float* g, int n_out, const Rows& L, int nL, const Rows& S, const WRows& dL,
                       const WRows& dS, int64_t B, cudaStream_t st) {
-  if (nL <= 64) {
-    constexpr int R = 8;
-    const int n_tiles = ceil_div(nL, R);
-    const int nw = n_tiles < 8 ? n_tiles : 8;
-    return (int)launch(k_conv_bwd<KF, R>, dim3(ceil_div(B, kWarp)), dim3(kWarp, nw), 0, st, g, n_out, L, nL, S, dL,
-                       dS, B, n_tiles);
-  }
-  constexpr int R = 16;
+  constexpr int R = 8;
   const int n_tiles = ceil_div(nL, R);
-  const int nw = n_tiles < 8 ? n_tiles : 8;
+  const int nw = n_tiles < 16 ? n_tiles : 16;
   return (int)launch(k_conv_bwd<KF, R>, dim3(ceil_div(B, kWarp)), dim3(kWarp, nw), 0, st, g, n_out, L, nL, S, dL, dS,
                      B, n_tiles);
 }

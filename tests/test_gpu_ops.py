@@ -145,16 +145,23 @@ def test_dtkp_operator_kats(cuda):
 
 
 def test_equality_toy_contrasts_provenances(cuda):
+    """test_acceptance.py:86-110: DTKP (k >= n) gives exactly 1, DAMP gives sum p^2."""
     S = sg()
     from paper_2410_03348_b200.programs import equality_toy
 
-    row = np.array([[0.5, 0.3, 0.2]])
-    ctx = S.ProgramContext(S.DtkpAm(2))
-    out = equality_toy(ctx, S.make_distribution(ctx, row, ["a", "b", "c"]))
-    assert probs_of(out)[True] == pytest.approx(1.0, abs=1e-6)
-    ctx = S.ProgramContext(S.Damp())
-    out = equality_toy(ctx, S.make_distribution(ctx, row, ["a", "b", "c"]))
-    assert probs_of(out)[True] == pytest.approx(float((row ** 2).sum()), abs=1e-6)
+    rng = np.random.default_rng(0)
+    for _ in range(10):
+        n = int(rng.integers(2, 7))
+        k = int(rng.integers(n, n + 3))
+        row = rng.uniform(0.05, 1.0, size=n)
+        row /= row.sum()
+        ctx = S.ProgramContext(S.DtkpAm(min(k, 8)))
+        out = equality_toy(ctx, S.make_distribution(ctx, row.reshape(1, -1), list(range(n))))
+        assert probs_of(out)[True] == pytest.approx(1.0, abs=1e-6)
+        ctx = S.ProgramContext(S.Damp())
+        out = equality_toy(ctx, S.make_distribution(ctx, row.reshape(1, -1), list(range(n))))
+        r32 = row.astype(np.float32).astype(np.float64)
+        assert probs_of(out)[True] == pytest.approx(float((r32 ** 2).sum()), abs=1e-6)
 
 
 # ------------------------------------------------------------------ decomposed operators
@@ -329,7 +336,7 @@ def test_sum15_full_batch_properties(cuda):
     out = P.sum_n(ctx, [S.make_distribution(ctx, lf, range(10)) for lf in leaves])
     assert out.symbols == tuple(range(136))
     probs = S.get_probs(out)
-    mass = probs.double().sum(dim=1).cpu().numpy()
+    mass = probs.detach().double().sum(dim=1).cpu().numpy()
     np.testing.assert_allclose(mass, 1.0, atol=2e-5)
     w = rng.uniform(-1, 1, size=(B, 136))
     (probs.double() * torch.as_tensor(w, device=cuda)).sum().backward()
