@@ -418,43 +418,62 @@ __global__ void k_rows_add(const Rows A, const int32_t* __restrict__ ia, const R
 }
 
 // ------------------------------- fused loss_nll -------------------------------------
-constexpr int kNllThreads = 256;
+// CTA = 32 samples (lanes) x 8 warps; warp w sums rows w, w+8, ... in fp64, the row sums
+// are combined in shared memory in a fixed order.  Forward: per-CTA partial of the log
+// terms, the last CTA to finish (ticket counter) sums the partials in CTA order and
+// resets the counter (deterministic, graph-replay safe).
+constexpr int kNllWarps = 8;
 
-__device__ __forceinline__ double nll_sample(const Rows& p, int n, int64_t b, int64_t t, double& s, double& pt) {
-  s = 0.0;
-  for (int r = 0; r < n; ++r) s += (double)p.ld(r, b);
-  pt = t >= 0 ? (double)p.ld(t, b) : 0.0;
-  const double norm = pt / (s + 1e-8);
-  const double fl = fmax(norm, 1e-12);
-  const double picked = t >= 0 ? fl : 0.0;
-  return fmax(picked, 1e-12);
+__device__ __forceinline__ void nll_rowsum(const Rows& p, int n, int64_t b, double (&red)[kNllWarps][kWarp],
+                                           double& s) {
+  const int lane = threadIdx.x, warp = threadIdx.y;
+  double acc0 = 0.0, acc1 = 0.0;
+  int r = warp;
+  for (; r + kNllWarps < n; r += 2 * kNllWarps) {
+    acc0 += (double)p.ld(r, b);
+    acc1 += (double)p.ld(r + kNllWarps, b);
+  }
+  if (r < n) acc0 += (double)p.ld(r, b);
+  red[warp][lane] = acc0 + acc1;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < kNllWarps; ++w) t += red[w][lane];
+  s = t;
 }
 
-__global__ void __launch_bounds__(kNllThreads) k_nll_fwd(const Rows p, int n, int64_t B,
-                                                         const int64_t* __restrict__ targets, double* __restrict__ loss,
-                                                         double* __restrict__ partial, unsigned* __restrict__ counter) {
-  __shared__ double red[kNllThreads / 32];
+__device__ __forceinline__ double nll_picked(double s, double pt, int64_t t) {
+  const double norm = pt / (s + 1e-8);
+  const double fl = fmax(norm, 1e-12);
+  return fmax(t >= 0 ? fl : 0.0, 1e-12);
+}
+
+__global__ void __launch_bounds__(256) k_nll_fwd(const Rows p, int n, int64_t B, const int64_t* __restrict__ targets,
+                                                 double* __restrict__ loss, double* __restrict__ partial,
+                                                 unsigned* __restrict__ counter) {
+  __shared__ double red[kNllWarps][kWarp];
   __shared__ bool last;
+  const int lane = threadIdx.x, warp = threadIdx.y;
+  const int64_t b0 = (int64_t)blockIdx.x * kWarp + lane;
+  const bool bval = b0 < B;
+  const int64_t b = bval ? b0 : B - 1;
   pdl_wait();
-  double acc = 0.0;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
-    double s, pt;
-    acc += log(nll_sample(p, n, b, __ldg(targets + b), s, pt));
-  }
+  double s;
+  nll_rowsum(p, n, b, red, s);
+  if (warp == 0) {
+    const int64_t t = __ldg(targets + b);
+    const double pt = t >= 0 ? (double)p.ld(t, b) : 0.0;
+    double v = bval ? log(nll_picked(s, pt, t)) : 0.0;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double v = 0.0;
-    for (int w = 0; w < kNllThreads / 32; ++w) v += red[w];
-    partial[blockIdx.x] = v;
-    __threadfence();
-    const unsigned ticket = atomicAdd(counter, 1u);
-    last = ticket == gridDim.x - 1;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) {
+      partial[blockIdx.x] = v;
+      __threadfence();
+      last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last && warp == 0 && lane == 0) {
     __threadfence();
     double v = 0.0;
     for (unsigned i = 0; i < gridDim.x; ++i) v += ((volatile double*)partial)[i];
@@ -463,28 +482,27 @@ __global__ void __launch_bounds__(kNllThreads) k_nll_fwd(const Rows p, int n, in
   }
 }
 
-__global__ void __launch_bounds__(kNllThreads) k_nll_bwd(const Rows p, int n, int64_t B,
-                                                         const int64_t* __restrict__ targets,
-                                                         const double* __restrict__ gloss, WRows grad) {
+__global__ void __launch_bounds__(256) k_nll_bwd(const Rows p, int n, int64_t B, const int64_t* __restrict__ targets,
+                                                 const double* __restrict__ gloss, WRows grad) {
+  __shared__ double red[kNllWarps][kWarp];
+  const int lane = threadIdx.x, warp = threadIdx.y;
+  const int64_t b0 = (int64_t)blockIdx.x * kWarp + lane;
+  const bool bval = b0 < B;
+  const int64_t b = bval ? b0 : B - 1;
   pdl_wait();
-  const double g = *gloss;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = __ldg(targets + b);
-    double s, pt;
-    const double c = nll_sample(p, n, b, t, s, pt);
-    const double den = s + 1e-8;
-    const double coef = t >= 0 ? -(g / (double)B) / c : 0.0;
-    const double common = -pt / (den * den);
-    for (int r = 0; r < n; ++r) {
-      const double d = (r == t ? 1.0 / den : 0.0) + common;
-      grad.st(r, b, (float)(coef * d));
-    }
+  double s;
+  nll_rowsum(p, n, b, red, s);
+  const int64_t t = __ldg(targets + b);
+  const double pt = t >= 0 ? (double)p.ld(t, b) : 0.0;
+  const double c = nll_picked(s, pt, t);
+  const double den = s + 1e-8;
+  const double coef = t >= 0 ? -(*gloss / (double)B) / c : 0.0;
+  const double common = -pt / (den * den);
+  if (!bval) return;
+  for (int r = warp; r < n; r += kNllWarps) {
+    const double d = (r == t ? 1.0 / den : 0.0) + common;
+    grad.st(r, b, (float)(coef * d));
   }
-}
-
-static int nll_grid(int64_t B) {
-  int g = ceil_div(B, kNllThreads);
-  return g < 1 ? 1 : (g > 148 * 4 ? 148 * 4 : g);
 }
 
 // ------------------------------- row gather / layout ---------------------------------
@@ -628,23 +646,23 @@ int sg_damp_rows_add(const sg_rows A, const int32_t* ia, const sg_rows Bm, const
                      n_rows, B, (int)clamp01_, out);
 }
 
-int64_t sg_nll_scratch_bytes(int64_t B) { return (int64_t)(nll_grid(B) + 1) * (int64_t)sizeof(double); }
+int64_t sg_nll_scratch_bytes(int64_t B) { return (int64_t)(ceil_div(B, kWarp) + 1) * (int64_t)sizeof(double); }
 
 int sg_nll_fwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, double* loss, void* scratch,
                sg_stream_t stream) {
   if (B <= 0) return 0;
-  const int grid = nll_grid(B);
+  const int grid = ceil_div(B, kWarp);
   double* partial = (double*)scratch;
   unsigned* counter = (unsigned*)(partial + grid);
-  return (int)launch(k_nll_fwd, dim3(grid), dim3(kNllThreads), 0, (cudaStream_t)stream, rows_of(probs), (int)n, B,
-                     targets, loss, partial, counter);
+  return (int)launch(k_nll_fwd, dim3(grid), dim3(kWarp, kNllWarps), 0, (cudaStream_t)stream, rows_of(probs), (int)n,
+                     B, targets, loss, partial, counter);
 }
 
 int sg_nll_bwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, const double* grad_loss, sg_rows grad,
                sg_stream_t stream) {
   if (B <= 0) return 0;
-  return (int)launch(k_nll_bwd, dim3(nll_grid(B)), dim3(kNllThreads), 0, (cudaStream_t)stream, rows_of(probs), (int)n,
-                     B, targets, grad_loss, wrows_of(grad));
+  return (int)launch(k_nll_bwd, dim3(ceil_div(B, kWarp)), dim3(kWarp, kNllWarps), 0, (cudaStream_t)stream,
+                     rows_of(probs), (int)n, B, targets, grad_loss, wrows_of(grad));
 }
 
 int sg_rows_gather(const void* src, const int32_t* idx, int64_t n_rows, int64_t row_bytes, void* dst,

@@ -220,6 +220,22 @@ class DampRowsAdd(torch.autograd.Function):
         return ga, gb, None, None, None
 
 
+_NLL_SCRATCH: "dict[tuple, torch.Tensor]" = {}
+
+
+def _nll_scratch(dev, B: int) -> torch.Tensor:
+    """Per (device, stream) zero-initialised scratch; the kernel resets its counter itself,
+    so the buffer is reused across calls and CUDA-graph replays without a memset."""
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    nbytes = int(_lib().sg_nll_scratch_bytes(B))
+    buf = _NLL_SCRATCH.get(key)
+    if buf is None or buf.numel() < nbytes:
+        # under CUDA-graph capture this allocates from the graph pool (memset captured once)
+        buf = torch.zeros(max(nbytes, 4096), device=dev, dtype=torch.uint8)
+        _NLL_SCRATCH[key] = buf
+    return buf
+
+
 class NllLoss(torch.autograd.Function):
     """Fused get_probs -> loss_nll (learn.py:92-119) over an (n, B) probability view."""
 
@@ -229,7 +245,7 @@ class NllLoss(torch.autograd.Function):
         n, B = probs_nb.shape
         dev = probs_nb.device
         loss = torch.empty((), device=dev, dtype=torch.float64)
-        scratch = torch.zeros(int(_lib().sg_nll_scratch_bytes(B)), device=dev, dtype=torch.uint8)
+        scratch = _nll_scratch(dev, B)
         rc = _lib().sg_nll_fwd(N.rows(probs_nb), n, B, targets.data_ptr(), loss.data_ptr(), scratch.data_ptr(),
                                N.stream_ptr(dev))
         N.check(rc, "sg_nll_fwd")

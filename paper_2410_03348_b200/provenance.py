@@ -452,7 +452,7 @@ class DtkpAm:
 
     # ---- protocol ----------------------------------------------------------------------
     def gather(self, tags: DtkpTags, indices) -> DtkpTags:
-        idx = ops.index_tensor(indices, tags.pm.device)
+        idx = ops.index_map(indices, tags.count, tags.pm.device).idx
         n = int(idx.numel())
         pm = torch.empty((n, *tags.pm.shape[1:]), device=tags.pm.device, dtype=torch.int64)
         pp = torch.empty((n, *tags.pp.shape[1:]), device=tags.pp.device, dtype=torch.uint8)
@@ -505,7 +505,7 @@ class DtkpAm:
 
     def placed(self, tags: DtkpTags, placement: np.ndarray) -> DtkpTags:
         src = _placement_src(placement)
-        idx = torch.as_tensor(src, device=tags.pm.device)
+        idx = ops.index_map(src, tags.count, tags.pm.device).idx
         n = len(src)
         pm = torch.empty((n, *tags.pm.shape[1:]), device=tags.pm.device, dtype=torch.int64)
         pp = torch.empty((n, *tags.pp.shape[1:]), device=tags.pp.device, dtype=torch.uint8)

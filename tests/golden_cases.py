@@ -65,6 +65,28 @@ def _path(api, P, ctx, d):
     return P.path_closure(ctx, d[0])
 
 
+def _clutrr(api, P, ctx, d):
+    """CLUTRR-style kinship closure (BASELINE config 4 pattern) written against the
+    reference API: apply_if(kinship_compose, chain_link) + union to a fixpoint."""
+    from paper_2410_03348_b200.programs import _chain_link, kinship_compose_with
+
+    compose = kinship_compose_with(api.UNDEFINED)
+    derived = facts = d[0]
+    while True:
+        new = api.apply_if(compose, _chain_link, derived, facts)
+        merged = api.union(derived, new)
+        if set(merged.symbols) == set(derived.symbols):
+            return merged
+        derived = merged
+
+
+def clutrr_facts(n_entities, rels=None):
+    from paper_2410_03348_b200.programs import KINSHIP_RELATIONS, Fact
+
+    rels = KINSHIP_RELATIONS if rels is None else rels
+    return [Fact(i, i + 1, r) for i in range(n_entities - 1) for r in rels]
+
+
 def _edges(seed, nodes, prob):
     rng = np.random.default_rng(seed)
     return [(i, j) for i in range(nodes) for j in range(nodes) if i != j and rng.uniform() < prob]
@@ -112,6 +134,11 @@ CASES = {
     "dtkp_path_k5": ("dtkp", 5, _path, lambda P: [[P.Coord(*e) for e in _edges(21, 5, 0.45)]],
                      lambda rng: [rng.uniform(0.05, 0.95, size=(4, len(_edges(21, 5, 0.45)))).astype(np.float32)
                                   .astype(np.float64)], 19),
+    "dtkp_clutrr_k5": ("dtkp", 5, _clutrr, lambda P: [clutrr_facts(4)],
+                       lambda rng: [rng.uniform(0.05, 0.95, size=(3, 60)).astype(np.float32).astype(np.float64)], 21),
+    "dtkp_clutrr_k3_e5": ("dtkp", 3, _clutrr, lambda P: [clutrr_facts(5, ("father", "mother", "son", "daughter",
+                                                                          "brother", "sister", "husband", "wife"))],
+                          lambda rng: [rng.uniform(0.05, 0.95, size=(2, 32)).astype(np.float32).astype(np.float64)], 22),
     "damp_path": ("damp", None, _path, lambda P: [[P.Coord(*e) for e in _edges(22, 4, 0.5)]],
                   lambda rng: [rng.uniform(0.05, 0.5, size=(4, len(_edges(22, 4, 0.5)))).astype(np.float32)
                                .astype(np.float64)], 20),

@@ -21,6 +21,7 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT / "tests"))
+sys.path.insert(0, str(ROOT))
 for cand in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
     if (cand / "symgrad").exists():
         sys.path.insert(0, str(cand))
