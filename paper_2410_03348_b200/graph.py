@@ -1,0 +1,66 @@
+"""Whole-step CUDA-graph capture for fixed-shape programs (public API).
+
+A neurosymbolic training step runs the same program on every batch: the symbol lists,
+hence the memoised plans, and all tensor shapes are fixed.  ``GraphedStep`` captures the
+step — every ``apply`` / ``filter`` / ``union`` kernel, the loss and the backward — in
+one CUDA graph after an eager warm-up (which builds and uploads the plans), so each later
+call costs one graph launch plus the copies of the new inputs into the captured buffers
+(from pinned host memory they are asynchronous H2D copies on the same stream).
+
+This is the B200 replacement for per-op host dispatch: CUDA graphs, not a tracing
+compiler.  The step function must be pure in its tensor inputs and may not read tensor
+values on the host (no ``.item()``, no ``forward_probs`` inside the step).
+"""
+
+from __future__ import annotations
+
+from typing import Callable, Sequence
+
+import torch
+
+__all__ = ["GraphedStep"]
+
+
+class GraphedStep:
+    """Capture ``step_fn(*inputs) -> outputs`` once; ``__call__`` replays it on new inputs.
+
+    ``example_inputs`` are device tensors with the shapes/dtypes of every future call;
+    inputs that require grad are re-created as leaves so the step can differentiate
+    w.r.t. them (e.g. ``torch.autograd.grad(loss, inputs)``).  Returned outputs are the
+    captured static tensors (overwritten by the next call).
+    """
+
+    def __init__(self, step_fn: Callable, example_inputs: Sequence[torch.Tensor], warmup: int = 3):
+        if not example_inputs:
+            raise ValueError("GraphedStep needs at least one example input")
+        self.device = example_inputs[0].device
+        if self.device.type != "cuda":
+            raise ValueError("GraphedStep captures CUDA work; inputs must live on a CUDA device")
+        self.static_inputs = []
+        for x in example_inputs:
+            s = x.detach().clone()
+            if x.requires_grad:
+                s.requires_grad_(True)
+            self.static_inputs.append(s)
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            for _ in range(max(1, warmup)):
+                step_fn(*self.static_inputs)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            out = step_fn(*self.static_inputs)
+        self.static_outputs = out
+        torch.cuda.synchronize(self.device)
+
+    def __call__(self, *inputs: torch.Tensor):
+        if len(inputs) != len(self.static_inputs):
+            raise ValueError(f"expected {len(self.static_inputs)} inputs, got {len(inputs)}")
+        with torch.no_grad():
+            for s, x in zip(self.static_inputs, inputs):
+                if x is not s:
+                    s.copy_(x, non_blocking=True)
+        self.graph.replay()
+        return self.static_outputs

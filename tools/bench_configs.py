@@ -51,7 +51,7 @@ def timed(step, iters=20, graph=True):
             mode = "cuda_graph"
         except Exception as exc:  # noqa: BLE001 - report and fall back to eager timing
             g = None
-            mode = f"eager (capture failed: {type(exc).__name__})"
+            mode = f"eager (capture failed: {type(exc).__name__}: {str(exc)[:160]})"
             torch.cuda.synchronize(DEV)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
