@@ -4,6 +4,11 @@
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "../../include/sgb200.h"
 
 #define SG_RETURN_IF(cond, err) \
@@ -50,5 +55,23 @@ __device__ __forceinline__ Rec<RW> load_rec(const int32_t* __restrict__ p) {
 }
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// Raise a kernel's dynamic shared-memory limit once per (device, kernel): repeated
+// cudaFuncSetAttribute calls are avoided so launches stay legal inside CUDA-graph capture.
+inline cudaError_t ensure_smem(const void* fn, size_t smem) {
+  if (smem <= 48 * 1024) return cudaSuccess;
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_pair(dev, fn);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= smem) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess) done[key] = 227 * 1024;
+  return e;
+}
 
 }  // namespace sg

@@ -189,9 +189,8 @@ __global__ void k_segsum_fixup(const int32_t* __restrict__ split, int n_split, c
 template <int NOPS, int RW, bool STAGED>
 static int launch_segsum_t(const SegsumK& k, int n_blocks, size_t smem, cudaStream_t st) {
   dim3 grid(ceil_div(k.B, kWarp), n_blocks);
-  if (STAGED && smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_segsum<NOPS, RW, STAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+  if (STAGED) {
+    cudaError_t e = ensure_smem((const void*)k_segsum<NOPS, RW, STAGED>, smem);
     if (e != cudaSuccess) return (int)e;
   }
   cudaError_t e = launch(k_segsum<NOPS, RW, STAGED>, grid, dim3(256), STAGED ? smem : 0, st, k);

@@ -290,8 +290,7 @@ int sg_dtkp_probs_fwd(const uint64_t* member, const uint8_t* present, int32_t N,
   const size_t smem = (size_t)I * kWarp * (mode == 2 ? sizeof(double) : sizeof(float));
 #define SG_PF(WT)                                                                                        \
   do {                                                                                                   \
-    if (smem > 48 * 1024)                                                                                \
-      cudaFuncSetAttribute(k_dtkp_probs_fwd<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    ensure_smem((const void*)k_dtkp_probs_fwd<WT>, smem);                                                \
     k_dtkp_probs_fwd<WT><<<grid, nw * 32, smem, st>>>(member, present, N, K, W, p, I, B, rows_per, out);  \
   } while (0)
   if (W <= 1) SG_PF(1);
@@ -329,8 +328,7 @@ int sg_dtkp_probs_bwd(const uint64_t* member, const uint8_t* present, int32_t N,
   double* scr = (double*)scratch;
 #define SG_PB(WT)                                                                                                  \
   do {                                                                                                             \
-    if (smem > 48 * 1024)                                                                                          \
-      cudaFuncSetAttribute(k_dtkp_probs_bwd<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+    ensure_smem((const void*)k_dtkp_probs_bwd<WT>, smem);                                                          \
     k_dtkp_probs_bwd<WT><<<grid, nw * 32, smem, st>>>(member, present, N, K, W, p, I, B, rows_per, grad_out, scr); \
   } while (0)
   if (W <= 1) SG_PB(1);

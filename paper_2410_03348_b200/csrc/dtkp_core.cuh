@@ -261,9 +261,8 @@ static int launch_apply_kw(const DtkpK& k, int n_blocks, cudaStream_t st) {
   if (mode == 0) return (int)cudaErrorNotSupported;
   const size_t smem = (size_t)k.I * kWarp * (mode == 2 ? sizeof(double) : sizeof(float));
   dim3 grid(ceil_div(k.B, kWarp), n_blocks);
-  if (smem > 48 * 1024) {
-    cudaError_t e =
-        cudaFuncSetAttribute(k_dtkp_apply<K, WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = ensure_smem((const void*)k_dtkp_apply<K, WT>, smem);
     if (e != cudaSuccess) return (int)e;
   }
   k_dtkp_apply<K, WT><<<grid, 128, smem, st>>>(k);

@@ -50,7 +50,7 @@ class GraphedStep:
         torch.cuda.current_stream(self.device).wait_stream(side)
         torch.cuda.synchronize(self.device)
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
+        with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
             out = step_fn(*self.static_inputs)
         self.static_outputs = out
         torch.cuda.synchronize(self.device)

@@ -44,7 +44,7 @@ def timed(step, iters=20, graph=True):
     if graph:
         try:
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
                 step()
             g.replay()
             torch.cuda.synchronize(DEV)
