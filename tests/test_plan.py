@@ -1,0 +1,144 @@
+"""CPU: the host map/shuffle stage (plan builder) and the device work-list layout.
+
+The plan must be bit-exact with the reference's apply_if host part
+(distribution.py:244-260) — checked against the oracle restatement and the golden
+symbol orders — and the segmented work lists must cover every record exactly once.
+"""
+
+import numpy as np
+import pytest
+
+import golden_cases as G
+from runners import load_golden
+
+
+def plan_mod():
+    from paper_2410_03348_b200 import plan
+
+    return plan
+
+
+def test_plan_matches_oracle_map_shuffle():
+    P = plan_mod()
+    from oracle.algebra import map_shuffle
+
+    cases = [
+        (lambda x, y: x + y, None, [tuple(range(10))] * 2),
+        (lambda x, y: P.UNDEFINED if (x * y) % 5 == 3 else (x - y) % 4, lambda x, y: x != y, [tuple(range(9)), tuple(range(7))]),
+        (lambda x, y, z: (x, y % 2, z > 1), None, [tuple("abc"), tuple(range(4)), tuple(range(3))]),
+        (lambda s: s % 2, None, [(3, 1, 2, 0)]),
+    ]
+    for f, cond, lists in cases:
+        plan = P.build_plan(f, cond, lists)
+        syms, combos, idx = map_shuffle(f, cond, lists, P.UNDEFINED)
+        assert plan.out_symbols == syms
+        np.testing.assert_array_equal(plan.combos, combos)
+        np.testing.assert_array_equal(plan.out_idx, idx)
+    assert P.build_plan(lambda s: s % 2, None, [(3, 1, 2, 0)]).out_symbols == (1, 0)  # first derivation
+
+
+@pytest.mark.parametrize("name", [n for n in G.CASES if n.startswith("damp_sum") or n.startswith("damp_sweep")])
+def test_plan_output_order_matches_reference_golden(name):
+    P = plan_mod()
+    from paper_2410_03348_b200 import programs as PR
+
+    gold = load_golden(name)
+    prov, k, prog, syms_fn, _, _ = G.CASES[name]
+    lists = syms_fn(PR)
+    if name.startswith("damp_sum"):
+        res = tuple(lists[0])
+        for s in lists[1:]:
+            res = P.build_plan(PR._add, None, [res, tuple(s)]).out_symbols
+        got = res
+    else:
+        got = P.build_plan(lambda *xs: sum(xs), None, [tuple(s) for s in lists]).out_symbols
+    assert [repr(s) for s in got] == gold["symbols"]
+
+
+def test_table_and_undefined():
+    P = plan_mod()
+    plan = P.build_plan(lambda x, y: P.UNDEFINED if x == y else x * y, None, [tuple(range(3))] * 2)
+    t = plan.table.reshape(3, 3)
+    assert (np.diag(t) == -1).all()
+    assert t[1, 2] == plan.out_symbols.index(2)
+    assert plan.n_kept == 6 and plan.n_enumerated == 9
+
+
+def test_symbol_function_errors_carry_the_tuple():
+    P = plan_mod()
+    with pytest.raises(P.SymbolFunctionError) as err:
+        P.build_plan(lambda x, y: x / y, None, [(0, 1), (0, 1)])
+    assert err.value.symbols == (0, 0)
+
+
+def test_memo_hits_same_code_and_closure():
+    P = plan_mod()
+    P.plan_cache_clear()
+
+    def make(k):
+        return lambda x, y: (x + y) % k
+
+    lists = [tuple(range(5))] * 2
+    a = P.build_plan(make(3), None, lists)
+    b = P.build_plan(make(3), None, [tuple(range(5)), tuple(range(5))])
+    c = P.build_plan(make(4), None, lists)
+    assert a is b and a is not c
+    info = P.plan_cache_info()
+    assert info["hits"] == 1 and info["misses"] == 2
+    # typed symbol keys: 1 and 1.0 are different input lists
+    d = P.build_plan(lambda x: type(x).__name__, None, [(1, 2)])
+    e = P.build_plan(lambda x: type(x).__name__, None, [(1.0, 2.0)])
+    assert d.out_symbols == ("int",) and e.out_symbols == ("float",)
+
+
+def test_plan_outputs_are_canonical_for_chaining():
+    P = plan_mod()
+    from paper_2410_03348_b200.programs import _add
+
+    p1 = P.build_plan(_add, None, [tuple(range(10))] * 2)
+    p2 = P.build_plan(_add, None, [p1.out_symbols, tuple(range(10))])
+    p2b = P.build_plan(_add, None, [p1.out_symbols, tuple(range(10))])
+    assert p2 is p2b
+    assert P.canonical_symbols(p1.out_symbols) is p1.out_symbols
+
+
+def test_toeplitz_detection():
+    P = plan_mod()
+    kp = P.build_plan(lambda x, y: x + y, None, [tuple(range(30)), tuple(range(10))]).kernel_plan()
+    assert kp.conv and kp.conv_short == 1
+    kp = P.build_plan(lambda x, y: x + y, None, [tuple(range(4)), tuple(range(30))]).kernel_plan()
+    assert kp.conv and kp.conv_short == 0
+    assert not P.build_plan(lambda x, y: x * y, None, [tuple(range(4))] * 2).kernel_plan().conv
+    assert not P.build_plan(lambda x, y: x + y, None, [tuple(range(40))] * 2).kernel_plan().conv  # filter > 16
+    assert not P.build_plan(lambda x, y: x + y, None, [(0, 2, 1), (0, 1)]).kernel_plan().conv  # not index-additive
+
+
+@pytest.mark.parametrize("max_item", [1, 3, 128])
+def test_segsum_items_cover_every_record_once(max_item):
+    P = plan_mod()
+    rng = np.random.default_rng(max_item)
+    n_seg = 50
+    lens = rng.integers(0, 400, size=n_seg)
+    lens[3] = 0
+    off = np.concatenate([[0], np.cumsum(lens)])
+    recs = rng.integers(0, 1000, size=(off[-1], 3)).astype(np.int32)
+    h = P.HostSegsum(off, recs, max_item)
+    vals = rng.uniform(size=off[-1])
+    out = np.full(n_seg, np.nan)
+    partial = np.zeros(h.n_partial)
+    seen = np.zeros(off[-1], dtype=int)
+    for seg, rb, re, dest in h.items:
+        seen[rb:re] += 1
+        v = vals[rb:re].sum()
+        if dest < 0:
+            out[seg] = v
+        else:
+            partial[dest] = v
+    for seg, pb, pe in h.split:
+        out[seg] = partial[pb:pe].sum()
+    assert (seen == 1).all()
+    ref = np.array([vals[off[i]:off[i + 1]].sum() for i in range(n_seg)])
+    np.testing.assert_allclose(out, ref)
+    for nb in (1, 2, 7, 64):
+        blk = h.blocks(nb)
+        assert blk[0] == 0 and blk[-1] == len(h.items) and (np.diff(blk) >= 0).all()

@@ -50,6 +50,9 @@ def timed(step, iters=20, graph=True):
             torch.cuda.synchronize(DEV)
             mode = "cuda_graph"
         except Exception as exc:  # noqa: BLE001 - report and fall back to eager timing
+            import traceback
+
+            traceback.print_exc(limit=15)
             g = None
             mode = f"eager (capture failed: {type(exc).__name__}: {str(exc)[:160]})"
             torch.cuda.synchronize(DEV)
@@ -108,6 +111,7 @@ def hwf7(B, iters):
     torch.cuda.synchronize(DEV)
     first = time.perf_counter() - t0
     n_out = len(out)
+    del out, ctx  # drop the first call's autograd graph (its AccumulateGrad nodes live on the default stream)
     targets = torch.tensor(rng.integers(0, n_out, size=B), device=DEV)
     combos = 0
     from paper_2410_03348_b200.plan import plan_cache_info
@@ -142,6 +146,8 @@ def clutrr(B, iters, n_entities=5, k=5):
     torch.cuda.synchronize(DEV)
     first = time.perf_counter() - t0
     targets = torch.tensor(rng.integers(0, len(out), size=B), device=DEV)
+    n_derived = len(out)
+    del out, ctx
 
     def step():
         c = sg.ProgramContext(sg.DtkpAm(k), device=DEV)
@@ -152,7 +158,7 @@ def clutrr(B, iters, n_entities=5, k=5):
     ms, mode = timed(step, iters)
     emit({"config": f"CLUTRR-style kinship closure, {n_entities} entities x 20 relations, DTKP k={k} "
                     "(BASELINE configs[3])", "metric": "samples/s (symbolic fwd+bwd)", "value": B / (ms * 1e-3),
-          "ms_per_step": ms, "batch": B, "mode": mode, "derived_facts": len(out), "input_facts": len(facts),
+          "ms_per_step": ms, "batch": B, "mode": mode, "derived_facts": n_derived, "input_facts": len(facts),
           "first_call_s_incl_host_plans": first})
 
 

@@ -93,7 +93,8 @@ def main():
 
         fb = 4 * B * (s1 + s2 + kp.n_out)
         bb = 4 * B * (kp.n_out + 2 * (s1 + s2))
-        csrc = [torch.rand(fb // 4, device=dev) for _ in range(max(2, int(400e6 // (2 * fb)) + 1))]
+        # a copy of fb/2 bytes moves fb bytes (read + write): same traffic as the forward
+        csrc = [torch.rand(fb // 8, device=dev) for _ in range(max(2, int(400e6 // fb) + 1))]
         cdst = [torch.empty_like(c) for c in csrc]
 
         def copy(j):
@@ -104,7 +105,7 @@ def main():
         tc = graph_time(copy, args.reps, dev)
         row = {"step": i, "S1": s1, "n_out": kp.n_out, "fwd_us": tf, "fwd_gbs": fb / tf / 1e3, "fwd_frac": fb / tf / 1e3 / hbm,
                "bwd_us": tb, "bwd_gbs": bb / tb / 1e3, "bwd_frac": bb / tb / 1e3 / hbm,
-               "copy_us_same_bytes_as_fwd": tc, "copy_frac": fb / tc / 1e3 / hbm}
+               "copy_us_same_traffic_as_fwd": tc, "copy_frac": fb / tc / 1e3 / hbm}
         results.append(row)
         print(json.dumps(row), flush=True)
         del sets, csrc, cdst
