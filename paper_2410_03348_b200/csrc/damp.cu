@@ -271,13 +271,20 @@ __global__ void __launch_bounds__(128, 8) k_conv_fwd(const Rows L, int nL, const
   constexpr int WN = R + KF - 1;
   const int o0 = t * R;
   float f[KF];
+  {
+    const float* q = S.p + b * S.sb;
 #pragma unroll
-  for (int j = 0; j < KF; ++j) f[j] = S.ld(j, b);
+    for (int j = 0; j < KF; ++j, q += S.sr) f[j] = __ldg(q);
+  }
   float w[WN];
+  {
+    const int s_first = o0 - (KF - 1);
+    const float* q = L.p + b * L.sb + (int64_t)s_first * L.sr;
 #pragma unroll
-  for (int i = 0; i < WN; ++i) {
-    const int s = o0 - (KF - 1) + i;
-    w[i] = (s >= 0 && s < nL) ? L.ld(s, b) : 0.f;
+    for (int i = 0; i < WN; ++i, q += L.sr) {
+      const int s = s_first + i;
+      w[i] = (s >= 0 && s < nL) ? __ldg(q) : 0.f;
+    }
   }
   pdl_trigger();
 #pragma unroll
@@ -296,10 +303,10 @@ __global__ void __launch_bounds__(128, 8) k_conv_fwd(const Rows L, int nL, const
 // partials of the tiles are reduced across warps in a fixed order (deterministic, no
 // atomics) and written by warp 0.
 template <int KF, int R>
-__global__ void __launch_bounds__(512, 2) k_conv_bwd(const float* __restrict__ g, int n_out, const Rows L, int nL,
+__global__ void __launch_bounds__(128, 4) k_conv_bwd(const float* __restrict__ g, int n_out, const Rows L, int nL,
                                                      const Rows S, WRows dL, WRows dS, int64_t B, int n_tiles) {
   __shared__ float sS[KF][kWarp];
-  __shared__ float red[16][KF][kWarp];
+  __shared__ float red[4][KF][kWarp];
   const int lane = threadIdx.x;
   const int warp = threadIdx.y;
   const int nw = blockDim.y;
@@ -310,40 +317,42 @@ __global__ void __launch_bounds__(512, 2) k_conv_bwd(const float* __restrict__ g
   pdl_wait();
   for (int j = warp; j < KF; j += nw) sS[j][lane] = S.ld(j, b);
   __syncthreads();
-  float f[KF], d2[KF];
+  float d2[KF];
 #pragma unroll
-  for (int j = 0; j < KF; ++j) {
-    f[j] = sS[j][lane];
-    d2[j] = 0.f;
-  }
+  for (int j = 0; j < KF; ++j) d2[j] = 0.f;
   for (int t = warp; t < n_tiles; t += nw) {
     const int s0 = t * R;
     float gw[WN];
+    {
+      const float* q = g + (size_t)s0 * B + b;
 #pragma unroll
-    for (int i = 0; i < WN; ++i) {
-      const int o = s0 + i;
-      gw[i] = (o < n_out) ? __ldg(g + (size_t)o * B + b) : 0.f;
+      for (int i = 0; i < WN; ++i, q += B) gw[i] = (s0 + i < n_out) ? __ldg(q) : 0.f;
     }
-    float pv[R];
+    {  // dS partials first: live = window + L tile + accumulators
+      float pv[R];
+      const float* q = L.p + b * L.sb + (int64_t)s0 * L.sr;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int s = s0 + r;
-      pv[r] = (s < nL) ? L.ld(s, b) : 0.f;
+      for (int r = 0; r < R; ++r, q += L.sr) pv[r] = (s0 + r < nL) ? __ldg(q) : 0.f;
+#pragma unroll
+      for (int j = 0; j < KF; ++j) {
+        float acc = d2[j];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc = fmaf(gw[r + j], pv[r], acc);
+        d2[j] = acc;
+      }
     }
+    {  // then dL: live = window + filter (re-read from shared memory)
+      float f[KF];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      float acc = 0.f;
+      for (int j = 0; j < KF; ++j) f[j] = sS[j][lane];
+      float* q = dL.p + b * dL.sb + (int64_t)s0 * dL.sr;
 #pragma unroll
-      for (int j = 0; j < KF; ++j) acc = fmaf(gw[r + j], f[j], acc);
-      const int s = s0 + r;
-      if (bval && s < nL) dL.st(s, b, acc);
-    }
+      for (int r = 0; r < R; ++r, q += dL.sr) {
+        float acc = 0.f;
 #pragma unroll
-    for (int j = 0; j < KF; ++j) {
-      float acc = d2[j];
-#pragma unroll
-      for (int r = 0; r < R; ++r) acc = fmaf(gw[r + j], pv[r], acc);
-      d2[j] = acc;
+        for (int j = 0; j < KF; ++j) acc = fmaf(gw[r + j], f[j], acc);
+        if (bval && s0 + r < nL) *q = acc;
+      }
     }
   }
   pdl_trigger();
@@ -369,9 +378,9 @@ static int conv_fwd_t(const Rows& L, int nL, const Rows& S, float* out, int n_ou
 template <int KF>
 static int conv_bwd_t(const float* g, int n_out, const Rows& L, int nL, const Rows& S, const WRows& dL,
                       const WRows& dS, int64_t B, cudaStream_t st) {
-  constexpr int R = 8;
+  constexpr int R = 32;
   const int n_tiles = ceil_div(nL, R);
-  const int nw = n_tiles < 16 ? n_tiles : 16;
+  const int nw = n_tiles < 4 ? n_tiles : 4;
   return (int)launch(k_conv_bwd<KF, R>, dim3(ceil_div(B, kWarp)), dim3(kWarp, nw), 0, st, g, n_out, L, nL, S, dL, dS,
                      B, n_tiles);
 }
