@@ -375,14 +375,23 @@ static int conv_fwd_t(const Rows& L, int nL, const Rows& S, float* out, int n_ou
                      n_tiles, n_pairs);
 }
 
-template <int KF>
-static int conv_bwd_t(const float* g, int n_out, const Rows& L, int nL, const Rows& S, const WRows& dL,
+template <int KF, int R>
+static int conv_bwd_r(const float* g, int n_out, const Rows& L, int nL, const Rows& S, const WRows& dL,
                       const WRows& dS, int64_t B, cudaStream_t st) {
-  constexpr int R = 32;
   const int n_tiles = ceil_div(nL, R);
   const int nw = n_tiles < 4 ? n_tiles : 4;
   return (int)launch(k_conv_bwd<KF, R>, dim3(ceil_div(B, kWarp)), dim3(kWarp, nw), 0, st, g, n_out, L, nL, S, dL, dS,
                      B, n_tiles);
+}
+
+// Tile width by the length of L: narrow tiles keep short rows from wasting lanes of work,
+// 32-wide tiles keep a 512-group batch in one wave of 4-warp CTAs for long rows.
+template <int KF>
+static int conv_bwd_t(const float* g, int n_out, const Rows& L, int nL, const Rows& S, const WRows& dL,
+                      const WRows& dS, int64_t B, cudaStream_t st) {
+  if (nL <= 16) return conv_bwd_r<KF, 8>(g, n_out, L, nL, S, dL, dS, B, st);
+  if (nL <= 64) return conv_bwd_r<KF, 16>(g, n_out, L, nL, S, dL, dS, B, st);
+  return conv_bwd_r<KF, 32>(g, n_out, L, nL, S, dL, dS, B, st);
 }
 
 #define SG_CONV_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
