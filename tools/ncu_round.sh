@@ -7,8 +7,11 @@ TAG=${TAG:-r01}
 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   --cache-control none --csv --log-file gpurun_out/${TAG}_step_launches.csv \
   python bench.py --quick --steps 2 --warmup 1 > gpurun_out/${TAG}_ncu_quick.out 2>&1; echo "launches rc=$?"
-for K in k_conv_bwd k_conv_fwd k_nll_fwd; do
-  timeout 300 ncu --set full --clock-control none --import-source on -k regex:$K -s 40 -c 1 \
+# skip counts land on the largest launch of a step: the first backward conv (step 14)
+# and the last forward conv (step 14) of the 4th captured/eager step
+for KS in k_conv_bwd:42 k_conv_fwd:55 k_nll_fwd:3; do
+  K=${KS%%:*}; S=${KS##*:}
+  timeout 300 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 \
     -o gpurun_out/${TAG}_full_$K -f python bench.py --quick --steps 2 --warmup 1 > gpurun_out/${TAG}_ncu_$K.out 2>&1
   echo "$K rc=$?"
 done
