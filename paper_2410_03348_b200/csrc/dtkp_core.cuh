@@ -147,6 +147,43 @@ __device__ __forceinline__ bool row_present(const sg_dtkp_operand& op, int K, in
   return __ldg(op.present + ((size_t)r * K + q) * B + b) != 0;
 }
 
+// All K proof rows of one tag (one symbol, one sample) in registers, loaded with
+// K * (WT + 1) independent loads and no data-dependent branch (memory-level parallelism).
+template <int K, int WT>
+struct TagRows {
+  uint64_t m[K][WT];
+  uint32_t pres;  // bit q = row q present
+
+  __device__ __forceinline__ void load(const sg_dtkp_operand& op, int64_t B, int64_t b, int r) {
+    const uint8_t* pp = op.present + (size_t)r * K * B + b;
+    const unsigned long long* base =
+        reinterpret_cast<const unsigned long long*>(op.member) + (size_t)r * K * (size_t)op.W * B + b;
+    uint32_t p = 0;
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      p |= (__ldg(pp + (size_t)q * B) != 0 ? 1u : 0u) << q;
+#pragma unroll
+      for (int w = 0; w < WT; ++w) m[q][w] = (w < op.W) ? __ldg(base + ((size_t)q * op.W + w) * B) : 0ull;
+    }
+    pres = p;
+  }
+
+  // Row q (runtime index) without local memory: unrolled select.
+  __device__ __forceinline__ void row(int q, uint64_t (&mm)[WT]) const {
+#pragma unroll
+    for (int w = 0; w < WT; ++w) mm[w] = m[0][w];
+#pragma unroll
+    for (int i = 1; i < K; ++i) {
+      if (i == q) {
+#pragma unroll
+        for (int w = 0; w < WT; ++w) mm[w] = m[i][w];
+      }
+    }
+  }
+};
+
+__device__ __forceinline__ int rec_row(const DtkpK& a, int c, int i) { return __ldg(a.recs + (size_t)c * a.rec_words + i); }
+
 template <int K, int WT>
 __global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
   extern __shared__ __align__(16) unsigned char ptile_raw[];
@@ -164,39 +201,55 @@ __global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
     const int4 item = __ldg(reinterpret_cast<const int4*>(a.items) + it);
     TopK<K, WT> S;
     S.clear();
-    for (int c = item.y; c < item.z; ++c) {
-      const int32_t* rec = a.recs + (size_t)c * a.rec_words;
-      if (a.arity == 1) {
-        // group_disj / union / merge: stream the stored rows as they are
-        int r = __ldg(rec);
-        const sg_dtkp_operand* op = &a.ops[0];
-        if (r >= a.ops[0].rows) {
-          r -= a.ops[0].rows;
-          op = &a.tail;
-        }
+    if (a.arity == 1) {
+      // group_disj / union / merge: stream the stored rows of every record, in order;
+      // the next record's rows are loaded before the current one is ranked.
+      TagRows<K, WT> cur, nxt;
+      auto fetch = [&](int c, TagRows<K, WT>& t) {
+        int r = rec_row(a, c, 0);
+        if (r >= a.ops[0].rows)
+          t.load(a.tail, a.B, b, r - a.ops[0].rows);
+        else
+          t.load(a.ops[0], a.B, b, r);
+      };
+      if (item.y < item.z) fetch(item.y, cur);
+      for (int c = item.y; c < item.z; ++c) {
+        const bool more = c + 1 < item.z;
+        if (more) fetch(c + 1, nxt);
 #pragma unroll 1
         for (int q = 0; q < K; ++q) {
-          if (row_present(*op, K, a.B, b, r, q)) {
-            uint64_t mm[WT];
-            load_row<WT>(*op, K, a.B, b, r, q, mm);
-            S.insert(mm, proof_key<WT>(mm, pc), 0);
-          }
+          if (!((cur.pres >> q) & 1u)) continue;
+          uint64_t mm[WT];
+          cur.row(q, mm);
+          S.insert(mm, proof_key<WT>(mm, pc), 0);
         }
-      } else {
-        // conj fold, normalised after every step (candidate order ra*kb + rb)
+        if (more) cur = nxt;
+      }
+    } else {
+      // conj fold, normalised after every step (candidate order ra*kb + rb)
+      TagRows<K, WT> A, Bt, An, Bn;
+      if (item.y < item.z) {
+        A.load(a.ops[0], a.B, b, rec_row(a, item.y, 0));
+        Bt.load(a.ops[1], a.B, b, rec_row(a, item.y, 1));
+      }
+      for (int c = item.y; c < item.z; ++c) {
+        const bool more = c + 1 < item.z;
+        if (more) {
+          An.load(a.ops[0], a.B, b, rec_row(a, c + 1, 0));
+          Bn.load(a.ops[1], a.B, b, rec_row(a, c + 1, 1));
+        }
         TopK<K, WT> T;
         T.clear();
-        const int r0 = __ldg(rec), r1 = __ldg(rec + 1);
 #pragma unroll 1
         for (int qa = 0; qa < K; ++qa) {
-          if (!row_present(a.ops[0], K, a.B, b, r0, qa)) continue;
+          if (!((A.pres >> qa) & 1u)) continue;
           uint64_t ma[WT];
-          load_row<WT>(a.ops[0], K, a.B, b, r0, qa, ma);
+          A.row(qa, ma);
 #pragma unroll 1
           for (int qb = 0; qb < K; ++qb) {
-            if (!row_present(a.ops[1], K, a.B, b, r1, qb)) continue;
+            if (!((Bt.pres >> qb) & 1u)) continue;
             uint64_t mm[WT];
-            load_row<WT>(a.ops[1], K, a.B, b, r1, qb, mm);
+            Bt.row(qb, mm);
 #pragma unroll
             for (int w = 0; w < WT; ++w) mm[w] |= ma[w];
             T.insert(mm, proof_key<WT>(mm, pc), 0);
@@ -204,7 +257,8 @@ __global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
         }
 #pragma unroll 1
         for (int i = 2; i < a.arity; ++i) {
-          const int ri = __ldg(rec + i);
+          TagRows<K, WT> Ci;
+          Ci.load(a.ops[i], a.B, b, rec_row(a, c, i));
           TopK<K, WT> U;
           U.clear();
 #pragma unroll 1
@@ -214,9 +268,9 @@ __global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
             T.get(qa, ma, ka);
 #pragma unroll 1
             for (int qb = 0; qb < K; ++qb) {
-              if (!row_present(a.ops[i], K, a.B, b, ri, qb)) continue;
+              if (!((Ci.pres >> qb) & 1u)) continue;
               uint64_t mm[WT];
-              load_row<WT>(a.ops[i], K, a.B, b, ri, qb, mm);
+              Ci.row(qb, mm);
 #pragma unroll
               for (int w = 0; w < WT; ++w) mm[w] |= ma[w];
               U.insert(mm, proof_key<WT>(mm, pc), 0);
@@ -230,6 +284,10 @@ __global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
           double kk;
           T.get(q, mm, kk);
           S.insert(mm, kk, 0);  // same mask, same p -> same key as a recomputation
+        }
+        if (more) {
+          A = An;
+          Bt = Bn;
         }
       }
     }
