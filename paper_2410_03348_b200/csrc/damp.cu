@@ -435,28 +435,50 @@ __global__ void k_rows_add(const Rows A, const int32_t* __restrict__ ia, const R
 }
 
 // ------------------------------- fused loss_nll -------------------------------------
-// CTA = 32 samples (lanes) x 8 warps; warp w sums rows w, w+8, ... in fp64, the row sums
-// are combined in shared memory in a fixed order.  Forward: per-CTA partial of the log
-// terms, the last CTA to finish (ticket counter) sums the partials in CTA order and
-// resets the counter (deterministic, graph-replay safe).
+// Row sums are computed in parallel over (sample tile, row chunk) — chunks are added
+// when the batch alone cannot fill the GPU (HWF: B = 64, 8332 output symbols) — into
+// fp64 partials [chunks][B]; a second pass finishes per sample.  Forward: per-CTA log
+// terms, the last CTA to finish (ticket counter, self-resetting) sums them in CTA order.
+// Backward: one pass writes every gradient row of its chunk.  Deterministic throughout.
 constexpr int kNllWarps = 8;
 
-__device__ __forceinline__ void nll_rowsum(const Rows& p, int n, int64_t b, double (&red)[kNllWarps][kWarp],
-                                           double& s) {
+static int nll_chunks(int64_t n, int64_t B) {
+  const int tiles = ceil_div(B, kWarp);
+  int want = ceil_div(2 * 148, tiles);
+  const int max_chunks = ceil_div(n, 4 * kNllWarps);
+  if (want > max_chunks) want = max_chunks;
+  return want < 1 ? 1 : want;
+}
+
+__global__ void __launch_bounds__(256) k_nll_partial(const Rows p, int n, int64_t B, int rows_per,
+                                                     double* __restrict__ part) {
+  __shared__ double red[kNllWarps][kWarp];
   const int lane = threadIdx.x, warp = threadIdx.y;
+  const int64_t b0 = (int64_t)blockIdx.x * kWarp + lane;
+  const int64_t b = b0 < B ? b0 : B - 1;
+  pdl_wait();
+  const int r0 = blockIdx.y * rows_per, r1 = min(n, r0 + rows_per);
   double acc0 = 0.0, acc1 = 0.0;
-  int r = warp;
-  for (; r + kNllWarps < n; r += 2 * kNllWarps) {
+  int r = r0 + warp;
+  for (; r + kNllWarps < r1; r += 2 * kNllWarps) {
     acc0 += (double)p.ld(r, b);
     acc1 += (double)p.ld(r + kNllWarps, b);
   }
-  if (r < n) acc0 += (double)p.ld(r, b);
+  if (r < r1) acc0 += (double)p.ld(r, b);
   red[warp][lane] = acc0 + acc1;
   __syncthreads();
-  double t = 0.0;
+  if (warp == 0 && b0 < B) {
+    double t = 0.0;
 #pragma unroll
-  for (int w = 0; w < kNllWarps; ++w) t += red[w][lane];
-  s = t;
+    for (int w = 0; w < kNllWarps; ++w) t += red[w][lane];
+    part[(size_t)blockIdx.y * B + b0] = t;
+  }
+}
+
+__device__ __forceinline__ double nll_rowsum(const double* __restrict__ part, int chunks, int64_t B, int64_t b) {
+  double s = 0.0;
+  for (int c = 0; c < chunks; ++c) s += part[(size_t)c * B + b];
+  return s;
 }
 
 __device__ __forceinline__ double nll_picked(double s, double pt, int64_t t) {
@@ -465,58 +487,58 @@ __device__ __forceinline__ double nll_picked(double s, double pt, int64_t t) {
   return fmax(t >= 0 ? fl : 0.0, 1e-12);
 }
 
-__global__ void __launch_bounds__(256) k_nll_fwd(const Rows p, int n, int64_t B, const int64_t* __restrict__ targets,
-                                                 double* __restrict__ loss, double* __restrict__ partial,
+__global__ void __launch_bounds__(256) k_nll_fwd(const Rows p, int64_t B, const int64_t* __restrict__ targets,
+                                                 const double* __restrict__ part, int chunks,
+                                                 double* __restrict__ loss, double* __restrict__ blocks,
                                                  unsigned* __restrict__ counter) {
-  __shared__ double red[kNllWarps][kWarp];
+  __shared__ double red[8];
   __shared__ bool last;
-  const int lane = threadIdx.x, warp = threadIdx.y;
-  const int64_t b0 = (int64_t)blockIdx.x * kWarp + lane;
-  const bool bval = b0 < B;
-  const int64_t b = bval ? b0 : B - 1;
+  const int64_t b0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   pdl_wait();
-  double s;
-  nll_rowsum(p, n, b, red, s);
-  if (warp == 0) {
-    const int64_t t = __ldg(targets + b);
-    const double pt = t >= 0 ? (double)p.ld(t, b) : 0.0;
-    double v = bval ? log(nll_picked(s, pt, t)) : 0.0;
+  double v = 0.0;
+  if (b0 < B) {
+    const int64_t t = __ldg(targets + b0);
+    const double s = nll_rowsum(part, chunks, B, b0);
+    const double pt = t >= 0 ? (double)p.ld(t, b0) : 0.0;
+    v = log(nll_picked(s, pt, t));
+  }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if (lane == 0) {
-      partial[blockIdx.x] = v;
-      __threadfence();
-      last = atomicAdd(counter, 1u) == gridDim.x - 1;
-    }
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    blocks[blockIdx.x] = t;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && warp == 0 && lane == 0) {
+  if (last && threadIdx.x == 0) {
     __threadfence();
-    double v = 0.0;
-    for (unsigned i = 0; i < gridDim.x; ++i) v += ((volatile double*)partial)[i];
-    *loss = -v / (double)B;
+    double t = 0.0;
+    for (unsigned i = 0; i < gridDim.x; ++i) t += ((volatile double*)blocks)[i];
+    *loss = -t / (double)B;
     *counter = 0u;  // self-reset for the next launch / graph replay
   }
 }
 
 __global__ void __launch_bounds__(256) k_nll_bwd(const Rows p, int n, int64_t B, const int64_t* __restrict__ targets,
-                                                 const double* __restrict__ gloss, WRows grad) {
-  __shared__ double red[kNllWarps][kWarp];
+                                                 const double* __restrict__ gloss, const double* __restrict__ part,
+                                                 int chunks, int rows_per, WRows grad) {
   const int lane = threadIdx.x, warp = threadIdx.y;
-  const int64_t b0 = (int64_t)blockIdx.x * kWarp + lane;
-  const bool bval = b0 < B;
-  const int64_t b = bval ? b0 : B - 1;
+  const int64_t b = (int64_t)blockIdx.x * kWarp + lane;
   pdl_wait();
-  double s;
-  nll_rowsum(p, n, b, red, s);
+  if (b >= B) return;
   const int64_t t = __ldg(targets + b);
+  const double s = nll_rowsum(part, chunks, B, b);
   const double pt = t >= 0 ? (double)p.ld(t, b) : 0.0;
   const double c = nll_picked(s, pt, t);
   const double den = s + 1e-8;
   const double coef = t >= 0 ? -(*gloss / (double)B) / c : 0.0;
   const double common = -pt / (den * den);
-  if (!bval) return;
-  for (int r = warp; r < n; r += kNllWarps) {
+  const int r0 = blockIdx.y * rows_per, r1 = min(n, r0 + rows_per);
+  for (int r = r0 + warp; r < r1; r += kNllWarps) {
     const double d = (r == t ? 1.0 / den : 0.0) + common;
     grad.st(r, b, (float)(coef * d));
   }
@@ -663,23 +685,45 @@ int sg_damp_rows_add(const sg_rows A, const int32_t* ia, const sg_rows Bm, const
                      n_rows, B, (int)clamp01_, out);
 }
 
-int64_t sg_nll_scratch_bytes(int64_t B) { return (int64_t)(ceil_div(B, kWarp) + 1) * (int64_t)sizeof(double); }
+int64_t sg_nll_scratch_bytes(int64_t n, int64_t B) {
+  const int chunks = nll_chunks(n, B);
+  const int blocks = ceil_div(B, 256);
+  return (int64_t)(2 + blocks + (int64_t)chunks * B) * (int64_t)sizeof(double);
+}
 
+// scratch layout (doubles): [0] ticket counter (zero-initialised once, self-resetting),
+// [2, 2 + blocks) per-CTA log-term partials, then [chunks][B] row-sum partials.
 int sg_nll_fwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, double* loss, void* scratch,
                sg_stream_t stream) {
   if (B <= 0) return 0;
-  const int grid = ceil_div(B, kWarp);
-  double* partial = (double*)scratch;
-  unsigned* counter = (unsigned*)(partial + grid);
-  return (int)launch(k_nll_fwd, dim3(grid), dim3(kWarp, kNllWarps), 0, (cudaStream_t)stream, rows_of(probs), (int)n,
-                     B, targets, loss, partial, counter);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int chunks = nll_chunks(n, B);
+  const int rows_per = ceil_div(n, chunks);
+  const int blocks = ceil_div(B, 256);
+  double* base = (double*)scratch;
+  unsigned* counter = (unsigned*)base;
+  double* blk = base + 2;
+  double* part = base + 2 + blocks;
+  cudaError_t e = launch(k_nll_partial, dim3(ceil_div(B, kWarp), chunks), dim3(kWarp, kNllWarps), 0, st,
+                         rows_of(probs), (int)n, B, rows_per, part);
+  if (e != cudaSuccess) return (int)e;
+  return (int)launch(k_nll_fwd, dim3(blocks), dim3(256), 0, st, rows_of(probs), B, targets, (const double*)part, chunks,
+                     loss, blk, counter);
 }
 
 int sg_nll_bwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, const double* grad_loss, sg_rows grad,
-               sg_stream_t stream) {
+               void* scratch, sg_stream_t stream) {
   if (B <= 0) return 0;
-  return (int)launch(k_nll_bwd, dim3(ceil_div(B, kWarp)), dim3(kWarp, kNllWarps), 0, (cudaStream_t)stream,
-                     rows_of(probs), (int)n, B, targets, grad_loss, wrows_of(grad));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int chunks = nll_chunks(n, B);
+  const int rows_per = ceil_div(n, chunks);
+  const int blocks = ceil_div(B, 256);
+  double* part = (double*)scratch + 2 + blocks;
+  cudaError_t e = launch(k_nll_partial, dim3(ceil_div(B, kWarp), chunks), dim3(kWarp, kNllWarps), 0, st,
+                         rows_of(probs), (int)n, B, rows_per, part);
+  if (e != cudaSuccess) return (int)e;
+  return (int)launch(k_nll_bwd, dim3(ceil_div(B, kWarp), chunks), dim3(kWarp, kNllWarps), 0, st, rows_of(probs),
+                     (int)n, B, targets, grad_loss, (const double*)part, chunks, rows_per, wrows_of(grad));
 }
 
 int sg_rows_gather(const void* src, const int32_t* idx, int64_t n_rows, int64_t row_bytes, void* dst,

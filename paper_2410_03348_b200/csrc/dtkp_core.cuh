@@ -103,6 +103,9 @@ __device__ __forceinline__ PCol stage_pcol(void* tile, const float* __restrict__
 }
 
 // fp64 product of member probabilities in ascending column order (_dtkpcore.pyx:53-57).
+// Set bits are consumed four at a time: the four shared-memory loads are issued together
+// and the products are taken in ascending order; missing slots multiply by 1.0, which is
+// exact in IEEE arithmetic, so the result is bit-identical to the one-bit-at-a-time loop.
 template <int WT>
 __device__ __forceinline__ double proof_key(const uint64_t (&mm)[WT], const PCol& pc) {
   double prod = 1.0;
@@ -110,9 +113,19 @@ __device__ __forceinline__ double proof_key(const uint64_t (&mm)[WT], const PCol
   for (int w = 0; w < WT; ++w) {
     uint64_t x = mm[w];
     while (x) {
-      const int j = __ffsll((long long)x) - 1;
-      prod *= pc(w * 64 + j);
-      x &= x - 1;
+      int j[4];
+      bool ok[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ok[u] = x != 0;
+        j[u] = ok[u] ? (w * 64 + __ffsll((long long)x) - 1) : 0;
+        x &= x - 1;
+      }
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = pc(j[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) prod *= ok[u] ? v[u] : 1.0;
     }
   }
   return prod;

@@ -223,11 +223,11 @@ class DampRowsAdd(torch.autograd.Function):
 _NLL_SCRATCH: "dict[tuple, torch.Tensor]" = {}
 
 
-def _nll_scratch(dev, B: int) -> torch.Tensor:
+def _nll_scratch(dev, n: int, B: int) -> torch.Tensor:
     """Per (device, stream) zero-initialised scratch; the kernel resets its counter itself,
     so the buffer is reused across calls and CUDA-graph replays without a memset."""
     key = (dev, torch.cuda.current_stream(dev).cuda_stream)
-    nbytes = int(_lib().sg_nll_scratch_bytes(B))
+    nbytes = int(_lib().sg_nll_scratch_bytes(n, B))
     buf = _NLL_SCRATCH.get(key)
     if buf is None or buf.numel() < nbytes:
         # under CUDA-graph capture this allocates from the graph pool (memset captured once)
@@ -245,7 +245,7 @@ class NllLoss(torch.autograd.Function):
         n, B = probs_nb.shape
         dev = probs_nb.device
         loss = torch.empty((), device=dev, dtype=torch.float64)
-        scratch = _nll_scratch(dev, B)
+        scratch = _nll_scratch(dev, n, B)
         rc = _lib().sg_nll_fwd(N.rows(probs_nb), n, B, targets.data_ptr(), loss.data_ptr(), scratch.data_ptr(),
                                N.stream_ptr(dev))
         N.check(rc, "sg_nll_fwd")
@@ -258,8 +258,9 @@ class NllLoss(torch.autograd.Function):
         n, B = probs_nb.shape
         g = gloss.detach().to(torch.float64).reshape(()).contiguous()
         grad = torch.empty_like(probs_nb)
+        scratch = torch.empty(int(_lib().sg_nll_scratch_bytes(n, B)), device=probs_nb.device, dtype=torch.uint8)
         rc = _lib().sg_nll_bwd(N.rows(probs_nb), n, B, targets.data_ptr(), g.data_ptr(), N.rows(grad),
-                               N.stream_ptr(probs_nb.device))
+                               scratch.data_ptr(), N.stream_ptr(probs_nb.device))
         N.check(rc, "sg_nll_bwd")
         return grad, None
 

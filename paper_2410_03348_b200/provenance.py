@@ -178,6 +178,9 @@ class Damp:
         return _damp(torch.ones((n, b), device=registry._dev(), dtype=torch.float32))
 
     def gather(self, tags: DampTags, indices) -> DampTags:
+        rng = _as_range(indices)
+        if rng is not None:  # e.g. HWF's digit / operator filters: a zero-copy row view
+            return _damp(tags.sm[rng[0]:rng[1]])
         return _damp(ops.damp_apply(ops.gather_plan(indices, tags.count), [tags.sm], tags.batch))
 
     def conj(self, a: DampTags, b: DampTags) -> DampTags:
@@ -238,6 +241,17 @@ class Damp:
                 ops.index_map(uplan.ib, b.count, dev), True,
             )
         )
+
+
+def _as_range(indices):
+    """(start, stop) when indices are one ascending contiguous run (gather = a view)."""
+    idx = np.asarray(indices, dtype=np.int64).reshape(-1)
+    if idx.size == 0:
+        return None
+    a = int(idx[0])
+    if a >= 0 and np.array_equal(idx, np.arange(a, a + idx.size)):
+        return a, a + idx.size
+    return None
 
 
 def _placement_src(placement: np.ndarray) -> np.ndarray:
@@ -468,6 +482,9 @@ class DtkpAm:
 
     # ---- protocol ----------------------------------------------------------------------
     def gather(self, tags: DtkpTags, indices) -> DtkpTags:
+        rng = _as_range(indices)
+        if rng is not None:  # contiguous symbol rows: a zero-copy view of both tensors
+            return DtkpTags(tags.pm[rng[0]:rng[1]], tags.pp[rng[0]:rng[1]], tags.registry)
         idx = ops.index_map(indices, tags.count, tags.pm.device).idx
         n = int(idx.numel())
         pm = torch.empty((n, *tags.pm.shape[1:]), device=tags.pm.device, dtype=torch.int64)
