@@ -336,11 +336,12 @@ class HostSegsum:
 class DeviceSegsum:
     """HostSegsum uploaded to one device, with per-grid block partitions cached."""
 
-    def __init__(self, host: HostSegsum, device, staged: bool, min_chunk_work: int):
+    def __init__(self, host: HostSegsum, device, staged: bool, min_chunk_work: int, target_ctas: int = 2 * 148):
         self.host = host
         self.device = device
         self.staged = staged
         self.min_chunk_work = min_chunk_work
+        self.target_ctas = target_ctas
         self.recs = torch.from_numpy(np.ascontiguousarray(host.recs.reshape(-1))).to(device)
         self.items = torch.from_numpy(np.ascontiguousarray(host.items.reshape(-1))).to(device)
         self.split = torch.from_numpy(np.ascontiguousarray(host.split.reshape(-1))).to(device)
@@ -349,7 +350,7 @@ class DeviceSegsum:
 
     def struct(self, B: int) -> N.SgSegsum:
         tiles = max(1, -(-B // 32))
-        want = max(1, -(-2 * 148 // tiles))
+        want = max(1, -(-self.target_ctas // tiles))
         cap = max(1, self.total_work // max(1, self.min_chunk_work))
         nb = 1
         while nb < min(want, cap):
@@ -488,14 +489,15 @@ class DevicePlan:
     def dtkp(self):
         if self._dtkp is None:
             host = self.kp.dtkp_host()
-            self._dtkp = DeviceSegsum(host, self.device, True, 64)
+            # DTKP items are latency-bound per warp: ask for ~8 resident CTAs per SM
+            self._dtkp = DeviceSegsum(host, self.device, True, 16, target_ctas=148 * 8)
             if len(host.split):
                 off = np.concatenate([[0], host.split[:, 2]]).astype(np.int64)
                 merge_recs = np.arange(host.n_partial, dtype=np.int32).reshape(-1, 1)
                 mh = HostSegsum(off, merge_recs, 1 << 30)
                 # merge items write the original output segment
                 mh.items[:, 0] = host.split[:, 0]
-                self._dtkp_merge = DeviceSegsum(mh, self.device, True, 64)
+                self._dtkp_merge = DeviceSegsum(mh, self.device, True, 16, target_ctas=148 * 8)
         return self._dtkp, self._dtkp_merge
 
     def damp_struct(self, B: int, need_bwd=()) -> N.SgDampPlan:
