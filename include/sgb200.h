@@ -20,6 +20,8 @@
  *   sg_damp_apply_bwd   tensor.py:287 clamp bw, :415 affine bw, :240 mul bw, :386-391 select_rows bw
  *   sg_segsum_run       provenance.py:242-253 Damp.group_disj (and select_rows bw scatter-add)
  *   sg_damp_rows_add    provenance.py:239-240 Damp.disj; distribution.py:279-297 union
+ *   sg_chain_fwd/bwd    a left fold of Toeplitz applies (programs.py:42-49 sum_n) as one
+ *                       launch each way; per step the same as sg_damp_apply_fwd/bwd
  *   sg_nll_fwd/bwd      learn.py:92-119 loss_nll (the caller right after get_probs)
  *   sg_rows_gather      provenance.py:233-234 / :320-326 gather (filter, distribution.py:158-169)
  *   sg_to_symbol_major  provenance.py:223-225 Damp.input_tags (layout + fp32 cast of the block)
@@ -108,6 +110,28 @@ int sg_damp_apply_bwd(const sg_damp_plan* plan, const sg_rows* inputs,
  * index -1 contributes 0. */
 int sg_damp_rows_add(const sg_rows A, const int32_t* ia, const sg_rows Bm, const int32_t* ib,
                      int64_t n_rows, int64_t B, int32_t clamp01, float* out, sg_stream_t stream);
+
+/* ---- fused Toeplitz apply chains ---------------------------------------------------
+ * v_i = clamp01(v_{i-1} (*) S_i), i = 1..m — a left fold of Toeplitz applies (every Sum-N
+ * fold step) as ONE forward and ONE backward launch; per-step arithmetic is the one of
+ * sg_damp_apply_fwd/bwd.  All filters have kf rows; v_i has n0 + i (kf - 1) rows.
+ * states: [sg_chain_states_rows(n0, kf, m)][B] floats, written by fwd, read by bwd. */
+#define SG_CHAIN_MAX_STEPS 32
+typedef struct sg_chain {
+  sg_rows base;
+  int32_t n0;
+  int32_t kf;
+  int32_t m;
+  int32_t pad_;
+  int64_t B;
+  sg_rows filters[SG_CHAIN_MAX_STEPS];
+  float* states;
+} sg_chain;
+
+int64_t sg_chain_states_rows(int32_t n0, int32_t kf, int32_t m);
+int sg_chain_fwd(const sg_chain* chain, float* out, sg_stream_t stream);
+int sg_chain_bwd(const sg_chain* chain, const float* grad_out, sg_rows grad_base,
+                 const sg_rows* grad_filters, sg_stream_t stream);
 
 /* ---- fused get_probs -> loss_nll (learn.py:92-119, pass-through clamps) ---------------
  * loss = -(1/B) sum_b log(max(max(p[t_b][b] / (sum_n p[n][b] + 1e-8), 1e-12), 1e-12)),

@@ -37,6 +37,7 @@ def _units():
     """(object name, source, extra flags) for every translation unit."""
     units = [
         ("damp.o", CSRC / "damp.cu", []),
+        ("chain.o", CSRC / "chain.cu", []),
         ("dtkp.o", CSRC / "dtkp.cu", []),
     ]
     for k in range(1, 9):

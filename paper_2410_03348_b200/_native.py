@@ -44,6 +44,22 @@ class SgRows(Structure):
     _fields_ = [("ptr", c_void_p), ("stride_row", c_int64), ("stride_b", c_int64)]
 
 
+CHAIN_MAX_STEPS = 32
+
+
+class SgChain(Structure):
+    _fields_ = [
+        ("base", SgRows),
+        ("n0", c_int32),
+        ("kf", c_int32),
+        ("m", c_int32),
+        ("pad_", c_int32),
+        ("B", c_int64),
+        ("filters", SgRows * CHAIN_MAX_STEPS),
+        ("states", c_void_p),
+    ]
+
+
 class SgDampPlan(Structure):
     _fields_ = [
         ("arity", c_int32),
@@ -103,6 +119,9 @@ EXPORTS = {
         c_int32,
         [SgRows, c_void_p, SgRows, c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p],
     ),
+    "sg_chain_states_rows": (c_int64, [c_int32, c_int32, c_int32]),
+    "sg_chain_fwd": (c_int32, [POINTER(SgChain), c_void_p, c_void_p]),
+    "sg_chain_bwd": (c_int32, [POINTER(SgChain), c_void_p, SgRows, POINTER(SgRows), c_void_p]),
     "sg_nll_scratch_bytes": (c_int64, [c_int64, c_int64]),
     "sg_nll_fwd": (c_int32, [SgRows, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "sg_nll_bwd": (c_int32, [SgRows, c_int64, c_int64, c_void_p, c_void_p, SgRows, c_void_p, c_void_p]),

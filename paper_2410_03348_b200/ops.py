@@ -147,6 +147,57 @@ def damp_apply(kplan: KernelPlan, inputs, B: int) -> torch.Tensor:
     return DampApply.apply(kplan, B, *inputs)
 
 
+class ConvChainFn(torch.autograd.Function):
+    """A left fold of Toeplitz applies v_i = clamp01(v_{i-1} (*) S_i) as one fused forward
+    and one fused backward launch (csrc/chain.cu); identical per-step arithmetic to
+    DampApply on the Toeplitz path."""
+
+    @staticmethod
+    def forward(ctx, n0: int, kf: int, B: int, base, *filters):
+        m = len(filters)
+        dev = base.device
+        _check_operand(base, "chain base")
+        for f in filters:
+            _check_operand(f, "chain filter")
+        rows = int(_lib().sg_chain_states_rows(n0, kf, m))
+        states = torch.empty((max(rows, 1), B), device=dev, dtype=F32)
+        out = torch.empty((n0 + m * (kf - 1), B), device=dev, dtype=F32)
+        c = _chain_struct(n0, kf, B, base, filters, states)
+        rc = _lib().sg_chain_fwd(ctypes.byref(c), out.data_ptr(), N.stream_ptr(dev))
+        N.check(rc, "sg_chain_fwd")
+        ctx.meta = (n0, kf, B)
+        ctx.save_for_backward(base, states, *filters)
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        base, states, *filters = ctx.saved_tensors
+        n0, kf, B = ctx.meta
+        g = g.contiguous()
+        gbase = torch.empty_like(base)
+        gfilt = [torch.empty_like(f) for f in filters]
+        c = _chain_struct(n0, kf, B, base, filters, states)
+        arr = (N.SgRows * N.CHAIN_MAX_STEPS)()
+        for i, t in enumerate(gfilt):
+            arr[i] = N.rows(t)
+        rc = _lib().sg_chain_bwd(ctypes.byref(c), g.data_ptr(), N.rows(gbase), arr, N.stream_ptr(g.device))
+        N.check(rc, "sg_chain_bwd")
+        return (None, None, None, gbase, *gfilt)
+
+
+def _chain_struct(n0, kf, B, base, filters, states) -> N.SgChain:
+    c = N.SgChain()
+    c.base = N.rows(base)
+    c.n0 = n0
+    c.kf = kf
+    c.m = len(filters)
+    c.B = B
+    for i, f in enumerate(filters):
+        c.filters[i] = N.rows(f)
+    c.states = states.data_ptr()
+    return c
+
+
 class _IndexMap:
     """Host index list -> device index tensor + the scatter-sum plan of its backward."""
 

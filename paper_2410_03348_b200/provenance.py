@@ -14,6 +14,8 @@ Tag storage (symbol-major, batch innermost — see include/sgb200.h):
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -129,18 +131,69 @@ class InputRegistry:
 
 
 # ================================================================================== DAMP
+class _ConvChain:
+    """A pending left fold of Toeplitz applies (every Sum-N fold step).
+
+    ``Damp.apply_plan`` extends the chain instead of launching a kernel per apply; the
+    first consumer of the values (``get_probs``, another non-Toeplitz op, a host read)
+    materialises it with ONE fused forward launch, and autograd runs ONE fused backward
+    (ops.ConvChainFn).  Results equal the per-apply kernels step for step."""
+
+    __slots__ = ("base", "filters", "kf", "B", "n_out", "first_plan")
+    MAX_STEPS = 32
+    MAX_ROWS = 384  # two [rows][32] fp32 buffers per warp, two warps per CTA, in shared memory
+
+    def __init__(self, base, filters, kf, B, n_out, first_plan):
+        self.base, self.filters, self.kf, self.B, self.n_out = base, filters, kf, B, n_out
+        self.first_plan = first_plan
+
+    def can_extend(self, kf: int, B: int, n_out: int) -> bool:
+        return (kf == self.kf and B == self.B and len(self.filters) < self.MAX_STEPS
+                and n_out <= self.MAX_ROWS and n_out == self.n_out + kf - 1)
+
+    def extend(self, short_sm: torch.Tensor, n_out: int) -> "_ConvChain":
+        return _ConvChain(self.base, self.filters + [short_sm], self.kf, self.B, n_out, self.first_plan)
+
+    def materialize(self) -> torch.Tensor:
+        if len(self.filters) == 1:  # a single apply: the per-apply Toeplitz kernel
+            return ops.damp_apply(self.first_plan, _conv_operands(self.first_plan, self.base, self.filters[0]),
+                                  self.B)
+        return ops.ConvChainFn.apply(self.base.shape[0], self.kf, self.B, ops.expand_batch(self.base, self.B),
+                                     *[ops.expand_batch(f, self.B) for f in self.filters])
+
+
+def _conv_operands(kp, long_sm, short_sm):
+    ops_ = [None, None]
+    ops_[kp.conv_short] = short_sm
+    ops_[1 - kp.conv_short] = long_sm
+    return ops_
+
+
 class DampTags:
-    """Probability tags for a whole symbol list: symbol-major fp32 [n][b] on the device."""
+    """Probability tags for a whole symbol list: symbol-major fp32 [n][b] on the device
+    (possibly a pending Toeplitz chain, materialised on first access of ``sm``)."""
 
-    __slots__ = ("sm",)
+    __slots__ = ("_sm", "_chain")
 
-    def __init__(self, value=None, *, sm: torch.Tensor | None = None):
-        if sm is None:
+    def __init__(self, value=None, *, sm: torch.Tensor | None = None, chain: _ConvChain | None = None):
+        if sm is None and chain is None:
             v = _as_probs(value, _default_device())
             if v.ndim != 2:
                 raise ValueError("DampTags value must be (batch, n)")
             sm = ops.symbol_view(v)
-        self.sm = sm
+        self._sm = sm
+        self._chain = chain
+
+    @property
+    def sm(self) -> torch.Tensor:
+        if self._sm is None:
+            self._sm = self._chain.materialize()
+            self._chain = None
+        return self._sm
+
+    @property
+    def pending(self) -> bool:
+        return self._sm is None
 
     @property
     def value(self) -> torch.Tensor:
@@ -148,15 +201,11 @@ class DampTags:
 
     @property
     def batch(self) -> int:
-        return self.sm.shape[1]
+        return self._chain.B if self._sm is None else self._sm.shape[1]
 
     @property
     def count(self) -> int:
-        return self.sm.shape[0]
-
-
-def _damp(sm: torch.Tensor) -> DampTags:
-    return DampTags(sm=sm)
+        return self._chain.n_out if self._sm is None else self._sm.shape[0]
 
 
 class Damp:
@@ -228,9 +277,24 @@ class Damp:
         return _damp(torch.cat([p.sm for p in parts], dim=1))
 
     # ---- fused entry points ---------------------------------------------------------
+    fuse_chains = os.environ.get("SG_FUSE_CHAINS", "1") != "0"
+
     def apply_plan(self, tags_list, plan: SymbolPlan, batch: int) -> DampTags:
-        """K1 (+K2 through autograd): gather -> conj fold -> group_disj in one kernel."""
-        return _damp(ops.damp_apply(plan.kernel_plan(), [t.sm for t in tags_list], batch))
+        """K1 (+K2 through autograd): gather -> conj fold -> group_disj in one kernel.
+
+        Toeplitz applies whose long operand is the previous apply's output are deferred
+        into a fused chain (``_ConvChain``) and run as one launch each way."""
+        kp = plan.kernel_plan()
+        if self.fuse_chains and kp.conv and len(tags_list) == 2:
+            long_t, short_t = tags_list[1 - kp.conv_short], tags_list[kp.conv_short]
+            kf = kp.sizes[kp.conv_short]
+            if short_t.batch in (1, batch) and long_t.batch in (1, batch) and kp.n_out <= _ConvChain.MAX_ROWS:
+                ch = long_t._chain
+                if ch is not None and ch.can_extend(kf, batch, kp.n_out):
+                    return DampTags(chain=ch.extend(short_t.sm, kp.n_out))
+                if ch is None or not ch.can_extend(kf, batch, kp.n_out):
+                    return DampTags(chain=_ConvChain(long_t.sm, [short_t.sm], kf, batch, kp.n_out, kp))
+        return _damp(ops.damp_apply(kp, [t.sm for t in tags_list], batch))
 
     def union_tags(self, a: DampTags, b: DampTags, uplan) -> DampTags:
         B = max(a.batch, b.batch)

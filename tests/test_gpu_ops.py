@@ -348,3 +348,68 @@ def test_sum15_full_batch_properties(cuda):
     ogr = OP.grad_inputs(oout, w[rows])
     for lf, gr in zip(leaves, ogr):
         assert_close_rel(lf.grad.cpu().numpy()[rows], gr, 1e-5, 1e-6, what="grad")
+
+
+# ------------------------------------------------------------------ fused Toeplitz chains
+@pytest.mark.parametrize("n_digits,B", [(3, 100), (15, 4096), (33, 64)])
+def test_fused_chain_equals_per_apply_kernels(cuda, n_digits, B):
+    """sum_n through the fused chain kernels vs the per-apply Toeplitz kernels: forward
+    bit-identical, gradients within fp32 rounding; intermediates can still be read."""
+    S = sg()
+    from paper_2410_03348_b200 import programs as P
+    from paper_2410_03348_b200.provenance import Damp
+
+    rng = np.random.default_rng(n_digits)
+    xs = [G.rows(rng, B, 10) for _ in range(n_digits)]
+    w = rng.uniform(-1, 1, size=(B, 9 * n_digits + 1))
+
+    def run(fuse):
+        old = Damp.fuse_chains
+        Damp.fuse_chains = fuse
+        try:
+            ctx = S.ProgramContext(S.Damp())
+            leaves = [torch.tensor(x, device=cuda, dtype=torch.float32, requires_grad=True) for x in xs]
+            out = P.sum_n(ctx, [S.make_distribution(ctx, lf, range(10)) for lf in leaves])
+            if fuse and n_digits > 2:
+                assert out.tags.pending  # nothing launched until the values are needed
+            probs = S.get_probs(out)
+            (probs.double() * torch.as_tensor(w, device=cuda)).sum().backward()
+            return probs.detach().cpu().numpy(), [lf.grad.cpu().numpy() for lf in leaves]
+        finally:
+            Damp.fuse_chains = old
+
+    p1, g1 = run(True)
+    p0, g0 = run(False)
+    np.testing.assert_array_equal(p1, p0)
+    for a, b in zip(g1, g0):
+        assert_close_rel(a, b, 1e-5, 1e-6)
+
+
+def test_fused_chain_intermediate_and_reuse(cuda):
+    S = sg()
+    rng = np.random.default_rng(1)
+    B = 70
+    xs = [G.rows(rng, B, 10) for _ in range(5)]
+    ctx = S.ProgramContext(S.Damp())
+    leaves = [torch.tensor(x, device=cuda, dtype=torch.float32, requires_grad=True) for x in xs]
+    d = [S.make_distribution(ctx, lf, range(10)) for lf in leaves]
+    mid = S.apply(lambda a, b: a + b, S.apply(lambda a, b: a + b, d[0], d[1]), d[2])
+    end = S.apply(lambda a, b: a + b, S.apply(lambda a, b: a + b, mid, d[3]), d[4])
+    branch = S.apply(lambda a, b: a + b, mid, d[0])  # the same pending prefix used twice
+    loss = S.get_probs(end).sum() + 2.0 * S.get_probs(mid).sum() + S.get_probs(branch)[:, 3].sum()
+    loss.backward()
+    from oracle import programs as OP
+
+    octx = OP.OContext("damp", None, undefined=S.UNDEFINED)
+    od = [OP.make_distribution(octx, x, list(range(10))) for x in xs]
+    f = lambda a, b: a + b  # noqa: E731
+    omid = OP.apply(f, OP.apply(f, od[0], od[1]), od[2])
+    oend = OP.apply(f, OP.apply(f, omid, od[3]), od[4])
+    obr = OP.apply(f, omid, od[0])
+    ge = OP.grad_inputs(oend, np.ones((B, 37)))
+    gm = OP.grad_inputs(omid, 2.0 * np.ones((B, 19 + 9)))
+    wb = np.zeros((B, len(obr.symbols)))
+    wb[:, 3] = 1.0
+    gb = OP.grad_inputs(obr, wb)
+    for i, lf in enumerate(leaves):
+        assert_close_rel(lf.grad.cpu().numpy(), ge[i] + gm[i] + gb[i], 1e-5, 1e-6, what=f"leaf {i}")
