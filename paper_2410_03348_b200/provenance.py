@@ -208,6 +208,10 @@ class DampTags:
         return self._chain.n_out if self._sm is None else self._sm.shape[0]
 
 
+def _damp(sm: torch.Tensor) -> DampTags:
+    return DampTags(sm=sm)
+
+
 class Damp:
     """Add-mult probabilities: conj = product, disj = clamped sum (provenance.py:217-271)."""
 
