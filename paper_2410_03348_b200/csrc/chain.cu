@@ -12,14 +12,15 @@
 // Reference semantics per step: provenance.py:233-253 (gather, conj, group_disj + clamp);
 // backward tensor.py:287 (clamp pass-through), :415, :240, :386-391.
 //
-// Mapping: lane == sample, a warp owns 32 samples for the whole chain, each warp has a
-// private ping-pong pair of [n_max][32] shared-memory buffers (conflict-free lane access).
+// Mapping: lane == sample; a CTA owns 32 samples for the whole chain and its warps split
+// each step's output tiles; the state is a CTA-shared ping-pong pair of [n_max][32]
+// shared-memory buffers (conflict-free lane access).
 #include "common.cuh"
 
 namespace sg {
 
 constexpr int kChainMaxSteps = 32;
-constexpr int kChainWarps = 2;  // warps per CTA
+constexpr int kChainWarps = 4;  // warps per CTA (one CTA per 32 samples)
 
 struct CRows {
   const float* p;
@@ -45,22 +46,24 @@ struct ChainArgs {
 
 __device__ __forceinline__ void pdl_wait_c() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// CTA = 32 samples (lanes) x kChainWarps warps.  The running state of the 32 samples
+// lives in a CTA-shared ping-pong pair of [n_max][32] buffers; within a step the warps
+// split the output tiles (R outputs each), and one __syncthreads separates the steps.
 template <int KF, int R>
 __global__ void __launch_bounds__(kChainWarps * 32) k_chain_fwd(const ChainArgs a) {
   extern __shared__ float smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t b0 = ((int64_t)blockIdx.x * kChainWarps + warp) * kWarp + lane;
+  const int64_t b0 = (int64_t)blockIdx.x * kWarp + lane;
   pdl_wait_c();
-  if (((int64_t)blockIdx.x * kChainWarps + warp) * kWarp >= a.B) return;  // whole warp out of range
   const bool bval = b0 < a.B;
   const int64_t b = bval ? b0 : a.B - 1;
-  float* bufA = smem + (size_t)warp * 2 * a.n_max * kWarp + lane;
+  float* bufA = smem + lane;
   float* bufB = bufA + (size_t)a.n_max * kWarp;
   {
     const float* q = a.base.p + b * a.base.sb;
-    for (int s = 0; s < a.n[0]; ++s) bufA[s * kWarp] = __ldg(q + (int64_t)s * a.base.sr);
+    for (int s = warp; s < a.n[0]; s += kChainWarps) bufA[s * kWarp] = __ldg(q + (int64_t)s * a.base.sr);
   }
-  __syncwarp();
+  __syncthreads();
   for (int i = 1; i <= a.m; ++i) {
     float f[KF];
     {
@@ -72,7 +75,7 @@ __global__ void __launch_bounds__(kChainWarps * 32) k_chain_fwd(const ChainArgs 
     const int nin = a.n[i - 1], nout = a.n[i];
     const bool last = i == a.m;
     float* gdst = last ? a.out : a.states + (size_t)a.state_off[i] * a.B;
-    for (int o0 = 0; o0 < nout; o0 += R) {
+    for (int o0 = warp * R; o0 < nout; o0 += kChainWarps * R) {
       float w[R + KF - 1];
 #pragma unroll
       for (int u = 0; u < R + KF - 1; ++u) {
@@ -92,7 +95,7 @@ __global__ void __launch_bounds__(kChainWarps * 32) k_chain_fwd(const ChainArgs 
         }
       }
     }
-    __syncwarp();
+    __syncthreads();
     float* t = bufA;
     bufA = bufB;
     bufB = t;
@@ -102,16 +105,16 @@ __global__ void __launch_bounds__(kChainWarps * 32) k_chain_fwd(const ChainArgs 
 template <int KF, int R>
 __global__ void __launch_bounds__(kChainWarps * 32) k_chain_bwd(const ChainArgs a) {
   extern __shared__ float smem[];
+  __shared__ float red[kChainWarps][KF][kWarp];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t b0 = ((int64_t)blockIdx.x * kChainWarps + warp) * kWarp + lane;
+  const int64_t b0 = (int64_t)blockIdx.x * kWarp + lane;
   pdl_wait_c();
-  if (((int64_t)blockIdx.x * kChainWarps + warp) * kWarp >= a.B) return;
   const bool bval = b0 < a.B;
   const int64_t b = bval ? b0 : a.B - 1;
-  float* G = smem + (size_t)warp * 2 * a.n_max * kWarp + lane;
+  float* G = smem + lane;
   float* Gn = G + (size_t)a.n_max * kWarp;
-  for (int s = 0; s < a.n[a.m]; ++s) G[s * kWarp] = __ldg(a.g_out + (size_t)s * a.B + b);
-  __syncwarp();
+  for (int s = warp; s < a.n[a.m]; s += kChainWarps) G[s * kWarp] = __ldg(a.g_out + (size_t)s * a.B + b);
+  __syncthreads();
   for (int i = a.m; i >= 1; --i) {
     float f[KF], d2[KF];
     {
@@ -124,8 +127,7 @@ __global__ void __launch_bounds__(kChainWarps * 32) k_chain_bwd(const ChainArgs 
       }
     }
     const int nin = a.n[i - 1], nout = a.n[i];
-    // v_{i-1}: the base for i == 1, else the stored clamped state
-    const float* prev;
+    const float* prev;  // v_{i-1}: the base for i == 1, else the stored clamped state
     int64_t psr;
     if (i == 1) {
       prev = a.base.p + b * a.base.sb;
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(kChainWarps * 32) k_chain_bwd(const ChainArgs 
       prev = a.states + (size_t)a.state_off[i - 1] * a.B + b;
       psr = a.B;
     }
-    for (int s0 = 0; s0 < nin; s0 += R) {
+    for (int s0 = warp * R; s0 < nin; s0 += kChainWarps * R) {
       float gw[R + KF - 1];
 #pragma unroll
       for (int u = 0; u < R + KF - 1; ++u) {
@@ -165,12 +167,17 @@ __global__ void __launch_bounds__(kChainWarps * 32) k_chain_bwd(const ChainArgs 
         }
       }
     }
-    if (bval) {
-      float* q = a.dfilt_p[i - 1] + b0 * a.dfilt_sb[i - 1];
 #pragma unroll
-      for (int j = 0; j < KF; ++j) q[(int64_t)j * a.dfilt_sr[i - 1]] = d2[j];
+    for (int j = 0; j < KF; ++j) red[warp][j][lane] = d2[j];
+    __syncthreads();
+    // fixed-order reduction of the warps' dS partials; warps split the KF rows
+    for (int j = warp; j < KF; j += kChainWarps) {
+      float acc = red[0][j][lane];
+#pragma unroll
+      for (int w = 1; w < kChainWarps; ++w) acc += red[w][j][lane];
+      if (bval) a.dfilt_p[i - 1][(int64_t)j * a.dfilt_sr[i - 1] + b0 * a.dfilt_sb[i - 1]] = acc;
     }
-    __syncwarp();
+    __syncthreads();
     float* t = G;
     G = Gn;
     Gn = t;
@@ -179,11 +186,11 @@ __global__ void __launch_bounds__(kChainWarps * 32) k_chain_bwd(const ChainArgs 
 
 template <typename... KArgs>
 static cudaError_t launch_chain(void (*kernel)(KArgs...), const ChainArgs& a, cudaStream_t st) {
-  const size_t smem = (size_t)kChainWarps * 2 * a.n_max * kWarp * sizeof(float);
+  const size_t smem = (size_t)2 * a.n_max * kWarp * sizeof(float);
   cudaError_t e = ensure_smem((const void*)kernel, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(ceil_div(ceil_div(a.B, kWarp), kChainWarps));
+  cfg.gridDim = dim3(ceil_div(a.B, kWarp));
   cfg.blockDim = dim3(kChainWarps * kWarp);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -238,8 +245,8 @@ int sg_chain_fwd(const sg_chain* c, float* out, sg_stream_t stream) {
   if (rc) return rc;
   if (c->B <= 0) return 0;
   a.out = out;
-  const size_t smem = (size_t)kChainWarps * 2 * a.n_max * kWarp * sizeof(float);
-  SG_RETURN_IF(smem > 227 * 1024, cudaErrorNotSupported);
+  const size_t smem = (size_t)2 * a.n_max * kWarp * sizeof(float);
+  SG_RETURN_IF(smem > 200 * 1024, cudaErrorNotSupported);
   cudaStream_t st = (cudaStream_t)stream;
   switch (c->kf) {
 #define X(K) \
@@ -265,8 +272,8 @@ int sg_chain_bwd(const sg_chain* c, const float* grad_out, sg_rows grad_base, co
     a.dfilt_sr[i] = grad_filters[i].stride_row;
     a.dfilt_sb[i] = grad_filters[i].stride_b;
   }
-  const size_t smem = (size_t)kChainWarps * 2 * a.n_max * kWarp * sizeof(float);
-  SG_RETURN_IF(smem > 227 * 1024, cudaErrorNotSupported);
+  const size_t smem = (size_t)2 * a.n_max * kWarp * sizeof(float);
+  SG_RETURN_IF(smem > 200 * 1024, cudaErrorNotSupported);
   cudaStream_t st = (cudaStream_t)stream;
   switch (c->kf) {
 #define X(K) \
