@@ -56,8 +56,9 @@ __device__ __forceinline__ Rec<RW> load_rec(const int32_t* __restrict__ p) {
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
-// Raise a kernel's dynamic shared-memory limit once per (device, kernel): repeated
-// cudaFuncSetAttribute calls are avoided so launches stay legal inside CUDA-graph capture.
+// Raise a kernel's dynamic shared-memory limit (to the largest request seen so far) once
+// per (device, kernel): repeated cudaFuncSetAttribute calls are avoided so launches stay
+// legal inside CUDA-graph capture.
 inline cudaError_t ensure_smem(const void* fn, size_t smem) {
   if (smem <= 48 * 1024) return cudaSuccess;
   static std::mutex mu;
@@ -69,8 +70,8 @@ inline cudaError_t ensure_smem(const void* fn, size_t smem) {
   auto key = std::make_pair(dev, fn);
   auto it = done.find(key);
   if (it != done.end() && it->second >= smem) return cudaSuccess;
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  if (e == cudaSuccess) done[key] = 227 * 1024;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) done[key] = smem;
   return e;
 }
 
