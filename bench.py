@@ -177,74 +177,97 @@ def build_step(torch, sg, device):
     return step
 
 
-def kernel_roofline(torch, sg, device, B, hbm_gbs, reps=16):
-    """Per-launch time of the Sum-15 apply kernels, measured with CUDA events around a
-    CUDA-graph replay of the 14 forward (or 14 backward) launches of one step, rotating
-    over two full buffer sets (>= 2x L2 apart), so every launch streams from HBM."""
+def chain_bytes(B, n0=10, kf=10, m=N_DIGITS - 1):
+    """Algorithmic HBM bytes of one fused Sum-N chain launch (K1c/K2c):
+    fwd reads v_0 and the m filters and writes the m-1 clamped states and v_m; bwd reads
+    g_out, the filters, the states and v_0 and writes dS_1..m and dv_0."""
+    states = sum(n0 + i * (kf - 1) for i in range(1, m))
+    n_out = n0 + m * (kf - 1)
+    fwd = 4 * B * (n0 + m * kf + states + n_out)
+    bwd = 4 * B * (n_out + m * kf + states + n0 + m * kf + n0)
+    return fwd, bwd
+
+
+def kernel_roofline(torch, device, B, hbm_gbs, reps=12):
+    """Per-launch time of the fused Sum-15 chain kernels (the step's two dominant
+    launches), measured with CUDA events around a CUDA-graph replay of back-to-back
+    launches that rotate over buffer sets totalling > 2x L2, so every launch streams its
+    operands from HBM (cold), on the stream the kernels are launched on."""
     import ctypes
 
     from paper_2410_03348_b200 import _native as N
-    from paper_2410_03348_b200.plan import build_plan
-    from paper_2410_03348_b200.programs import _add
+    from paper_2410_03348_b200 import ops
 
     lib = N.load()
-    syms = tuple(DIGITS)
-    steps = []
-    for i in range(1, N_DIGITS):
-        kp = build_plan(_add, None, [syms if i == 1 else tuple(range(9 * (i - 1) + 10)), syms]).kernel_plan()
-        steps.append((kp, kp.device(device).damp_struct(B)))
+    n0, kf, m = 10, 10, N_DIGITS - 1
+    rows = int(lib.sg_chain_states_rows(n0, kf, m))
+    n_out = n0 + m * (kf - 1)
+    fwd_bytes, bwd_bytes = chain_bytes(B, n0, kf, m)
+    per_set = 4 * B * (n0 + 2 * m * kf + rows + 2 * n_out + n0)
+    nsets = max(2, -(-2 * 126 * 2**20 // per_set) + 1)
     sets = []
-    for _ in range(2):
-        bufs = []
-        for kp, _ in steps:
-            s1, s2 = kp.sizes
-            a = torch.rand((s1, B), device=device)
-            b = torch.rand((s2, B), device=device)
-            bufs.append((a, b, torch.empty((kp.n_out, B), device=device), torch.rand((kp.n_out, B), device=device),
-                         torch.empty_like(a), torch.empty_like(b)))
-        sets.append(bufs)
-    fwd_bytes = sum(4 * B * (kp.sizes[0] + kp.sizes[1] + kp.n_out) for kp, _ in steps)
-    bwd_bytes = sum(4 * B * (kp.n_out + 2 * (kp.sizes[0] + kp.sizes[1])) for kp, _ in steps)
+    for _ in range(nsets):
+        base = torch.rand((B, n0), device=device).t()  # (B, 10) softmax blocks read in place
+        filt = [torch.rand((B, kf), device=device).t() for _ in range(m)]
+        states = torch.empty((rows, B), device=device)
+        out = torch.empty((n_out, B), device=device)
+        g = torch.rand((n_out, B), device=device)
+        gbase = torch.empty_like(base)
+        gfilt = [torch.empty_like(f) for f in filt]
+        c = ops._chain_struct(n0, kf, B, base, filt, states)
+        garr = (N.SgRows * N.CHAIN_MAX_STEPS)()
+        for i, t in enumerate(gfilt):
+            garr[i] = N.rows(t)
+        sets.append((c, out, g, gbase, garr, (base, filt, states, gfilt)))
 
     def run(kind, j):
         st = torch.cuda.current_stream(device).cuda_stream
-        for (kp, s), (a, b, out, g, ga, gb) in zip(steps, sets[j % 2]):
-            if kind == "fwd":
-                rc = lib.sg_damp_apply_fwd(ctypes.byref(s), N.rows_array([a, b]), B, out.data_ptr(), None, st)
-            else:
-                rc = lib.sg_damp_apply_bwd(ctypes.byref(s), N.rows_array([a, b]), g.data_ptr(), B,
-                                           N.rows_array([ga, gb]), None, st)
-            N.check(rc, kind)
+        c, out, g, gbase, garr, _ = sets[j % nsets]
+        if kind == "fwd":
+            rc = lib.sg_chain_fwd(ctypes.byref(c), out.data_ptr(), st)
+        else:
+            rc = lib.sg_chain_bwd(ctypes.byref(c), g.data_ptr(), N.rows(gbase), garr, st)
+        N.check(rc, kind)
 
     res = {}
     for kind, nbytes in (("fwd", fwd_bytes), ("bwd", bwd_bytes)):
         side = torch.cuda.Stream(device)
         side.wait_stream(torch.cuda.current_stream(device))
         with torch.cuda.stream(side):
-            run(kind, 0)
-            run(kind, 1)
+            for j in range(nsets):
+                run(kind, j)
         torch.cuda.current_stream(device).wait_stream(side)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
             for j in range(reps):
                 run(kind, j)
-        g.replay()
+        graph.replay()
         torch.cuda.synchronize(device)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        g.replay()
-        e1.record()
-        torch.cuda.synchronize(device)
-        launches = reps * len(steps)
-        avg_us = e0.elapsed_time(e1) * 1e3 / launches
-        avg_bytes = nbytes / len(steps)
-        gbs = avg_bytes / (avg_us * 1e-6) / 1e9
-        res[f"damp_apply_{kind}"] = {"kernel": "k_conv_fwd<10,16>" if kind == "fwd" else "k_conv_bwd<10,R=8|16|32>",
-                                     "launches": launches, "avg_us": avg_us, "avg_bytes": avg_bytes,
-                                     "achieved_gbs": gbs, "frac": gbs / hbm_gbs}
+        best = None
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            graph.replay()
+            e1.record()
+            torch.cuda.synchronize(device)
+            us = e0.elapsed_time(e1) * 1e3 / reps
+            best = us if best is None else min(best, us)
+        gbs = nbytes / (best * 1e-6) / 1e9
+        res[f"chain_{kind}"] = {"kernel": f"k_chain_{kind}<10,8>", "launches": reps, "avg_us": best,
+                                "avg_bytes": nbytes, "achieved_gbs": gbs, "frac": gbs / hbm_gbs}
     del sets
     torch.cuda.empty_cache()
     return res
+
+
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the
+    committed `ncu --set full` capture summary (profiles/traffic.json), or None."""
+    try:
+        t = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+        return t.get(kernel)
+    except (OSError, ValueError):
+        return None
 
 
 def run_gpu_arm(args):
@@ -383,11 +406,14 @@ def run_gpu_arm(args):
     roof = None
     cpu = None
     if rank == 0:
-        kr = kernel_roofline(torch, sg, device, B, hbm)
-        dom_name = max(kr, key=lambda k: kr[k]["avg_us"] * kr[k]["launches"])
+        kr = kernel_roofline(torch, device, B, hbm)
+        dom_name = max(kr, key=lambda k: kr[k]["avg_us"])
         dom = kr[dom_name]
+        tr = ncu_traffic(dom["kernel"])
         roof = {"bound": "hbm", "kernel": dom_name, "achieved": dom["achieved_gbs"], "peak": hbm, "unit": "GB/s",
-                "frac": dom["achieved_gbs"] / hbm, "traffic": None, "peak_source": pk_src,
+                "frac": dom["achieved_gbs"] / hbm,
+                "traffic": tr["bytes_per_launch"] if tr and tr.get("batch") == B else None,
+                "traffic_source": tr.get("source") if tr else None, "peak_source": pk_src,
                 "bytes_per_launch": dom["avg_bytes"], "avg_launch_us": dom["avg_us"], "kernels": kr}
         if world == 1 and not args.no_cpu_baseline:
             try:
@@ -426,9 +452,10 @@ def run_gpu_arm(args):
             "gpu_launches": launches * args.steps,
             "gpu_launches_per_step": launches,
             "roofline": roof,
-            "roofline_method": "algorithmic bytes (SURVEY 8d: fwd 4B(S1+S2+Nout), bwd 4B(Nout+2(S1+S2))) / "
-                               "CUDA-event time per launch over graph-replayed back-to-back launches, "
-                               "HBM-streamed (rotating buffer sets > L2)",
+            "roofline_method": "algorithmic bytes of the fused chain launch (DESIGN.md 4: fwd 4B(n0+m*kf+"
+                               "states+n_out), bwd 4B(n_out+2*m*kf+states+2*n0)) / CUDA-event time per "
+                               "launch over graph-replayed back-to-back launches, HBM-streamed (rotating "
+                               "buffer sets > 2x L2)",
             "cpu_baseline": cpu,
             "clocks": clk,
         }

@@ -141,7 +141,7 @@ class _ConvChain:
 
     __slots__ = ("base", "filters", "kf", "B", "n_out", "first_plan")
     MAX_STEPS = 32
-    MAX_ROWS = 768  # two [rows][32] fp32 state buffers per 32-sample CTA in shared memory
+    MAX_ROWS = 720  # two [rows][32] fp32 state buffers per 32-sample CTA fit in 227 KB of smem
 
     def __init__(self, base, filters, kf, B, n_out, first_plan):
         self.base, self.filters, self.kf, self.B, self.n_out = base, filters, kf, B, n_out
