@@ -200,7 +200,7 @@ def kernel_roofline(torch, device, B, hbm_gbs, reps=12):
 
     lib = N.load()
     n0, kf, m = 10, 10, N_DIGITS - 1
-    rows = int(lib.sg_chain_states_rows(n0, kf, m))
+    rows = sum(n0 + i * (kf - 1) for i in range(1, m))
     n_out = n0 + m * (kf - 1)
     fwd_bytes, bwd_bytes = chain_bytes(B, n0, kf, m)
     per_set = 4 * B * (n0 + 2 * m * kf + rows + 2 * n_out + n0)
@@ -209,7 +209,7 @@ def kernel_roofline(torch, device, B, hbm_gbs, reps=12):
     for _ in range(nsets):
         base = torch.rand((B, n0), device=device).t()  # (B, 10) softmax blocks read in place
         filt = [torch.rand((B, kf), device=device).t() for _ in range(m)]
-        states = torch.empty((rows, B), device=device)
+        states = torch.empty((int(lib.sg_chain_states_elems(n0, kf, m, B)),), device=device)
         out = torch.empty((n_out, B), device=device)
         g = torch.rand((n_out, B), device=device)
         gbase = torch.empty_like(base)

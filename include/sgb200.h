@@ -115,7 +115,9 @@ int sg_damp_rows_add(const sg_rows A, const int32_t* ia, const sg_rows Bm, const
  * v_i = clamp01(v_{i-1} (*) S_i), i = 1..m — a left fold of Toeplitz applies (every Sum-N
  * fold step) as ONE forward and ONE backward launch; per-step arithmetic is the one of
  * sg_damp_apply_fwd/bwd.  All filters have kf rows; v_i has n0 + i (kf - 1) rows.
- * states: [sg_chain_states_rows(n0, kf, m)][B] floats, written by fwd, read by bwd. */
+ * states: sg_chain_states_elems(n0, kf, m, B) floats (a CTA-blocked layout private to the
+ * two kernels), written by fwd, read by bwd.  Chains whose longest state exceeds
+ * sg_chain_max_rows(kf) rows do not fit in shared memory (cudaErrorNotSupported). */
 #define SG_CHAIN_MAX_STEPS 32
 typedef struct sg_chain {
   sg_rows base;
@@ -128,7 +130,8 @@ typedef struct sg_chain {
   float* states;
 } sg_chain;
 
-int64_t sg_chain_states_rows(int32_t n0, int32_t kf, int32_t m);
+int64_t sg_chain_states_elems(int32_t n0, int32_t kf, int32_t m, int64_t B);
+int32_t sg_chain_max_rows(int32_t kf);
 int sg_chain_fwd(const sg_chain* chain, float* out, sg_stream_t stream);
 int sg_chain_bwd(const sg_chain* chain, const float* grad_out, sg_rows grad_base,
                  const sg_rows* grad_filters, sg_stream_t stream);

@@ -64,7 +64,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     for obj, src, extra in _units():
         out = BUILD / obj
         if force or _stale(out, deps):
-            cmd = [nvcc, *ARCH, *NVCC_FLAGS, f"-I{INCLUDE}", *extra, "-c", str(src), "-o", str(out)]
+            cmd = [nvcc, *ARCH, *NVCC_FLAGS, *os.environ.get("SG_NVCC_EXTRA", "").split(), f"-I{INCLUDE}", *extra,
+                   "-c", str(src), "-o", str(out)]
             jobs.append((obj, cmd))
 
     def run(job):

@@ -17,6 +17,7 @@ Gradient conventions follow the reference tape (tensor.py):
 from __future__ import annotations
 
 import ctypes
+import functools
 
 import numpy as np
 import torch
@@ -147,6 +148,11 @@ def damp_apply(kplan: KernelPlan, inputs, B: int) -> torch.Tensor:
     return DampApply.apply(kplan, B, *inputs)
 
 
+@functools.lru_cache(maxsize=None)
+def chain_max_rows(kf: int) -> int:
+    return int(_lib().sg_chain_max_rows(kf))
+
+
 class ConvChainFn(torch.autograd.Function):
     """A left fold of Toeplitz applies v_i = clamp01(v_{i-1} (*) S_i) as one fused forward
     and one fused backward launch (csrc/chain.cu); identical per-step arithmetic to
@@ -159,8 +165,8 @@ class ConvChainFn(torch.autograd.Function):
         _check_operand(base, "chain base")
         for f in filters:
             _check_operand(f, "chain filter")
-        rows = int(_lib().sg_chain_states_rows(n0, kf, m))
-        states = torch.empty((max(rows, 1), B), device=dev, dtype=F32)
+        elems = int(_lib().sg_chain_states_elems(n0, kf, m, B))
+        states = torch.empty((max(elems, 1),), device=dev, dtype=F32)
         out = torch.empty((n0 + m * (kf - 1), B), device=dev, dtype=F32)
         c = _chain_struct(n0, kf, B, base, filters, states)
         rc = _lib().sg_chain_fwd(ctypes.byref(c), out.data_ptr(), N.stream_ptr(dev))

@@ -141,7 +141,11 @@ class _ConvChain:
 
     __slots__ = ("base", "filters", "kf", "B", "n_out", "first_plan")
     MAX_STEPS = 32
-    MAX_ROWS = 720  # two [rows][32] fp32 state buffers per 32-sample CTA fit in 227 KB of smem
+
+    @staticmethod
+    def max_rows(kf: int) -> int:
+        """Longest state (rows) whose fwd/bwd shared-memory working set fits one CTA."""
+        return ops.chain_max_rows(kf)
 
     def __init__(self, base, filters, kf, B, n_out, first_plan):
         self.base, self.filters, self.kf, self.B, self.n_out = base, filters, kf, B, n_out
@@ -149,7 +153,7 @@ class _ConvChain:
 
     def can_extend(self, kf: int, B: int, n_out: int) -> bool:
         return (kf == self.kf and B == self.B and len(self.filters) < self.MAX_STEPS
-                and n_out <= self.MAX_ROWS and n_out == self.n_out + kf - 1)
+                and n_out <= self.max_rows(kf) and n_out == self.n_out + kf - 1)
 
     def extend(self, short_sm: torch.Tensor, n_out: int) -> "_ConvChain":
         return _ConvChain(self.base, self.filters + [short_sm], self.kf, self.B, n_out, self.first_plan)
@@ -292,7 +296,7 @@ class Damp:
         if self.fuse_chains and kp.conv and len(tags_list) == 2:
             long_t, short_t = tags_list[1 - kp.conv_short], tags_list[kp.conv_short]
             kf = kp.sizes[kp.conv_short]
-            if short_t.batch in (1, batch) and long_t.batch in (1, batch) and kp.n_out <= _ConvChain.MAX_ROWS:
+            if short_t.batch in (1, batch) and long_t.batch in (1, batch) and kp.n_out <= _ConvChain.max_rows(kf):
                 ch = long_t._chain
                 if ch is not None and ch.can_extend(kf, batch, kp.n_out):
                     return DampTags(chain=ch.extend(short_t.sm, kp.n_out))

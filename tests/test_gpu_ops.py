@@ -351,7 +351,7 @@ def test_sum15_full_batch_properties(cuda):
 
 
 # ------------------------------------------------------------------ fused Toeplitz chains
-@pytest.mark.parametrize("n_digits,B", [(3, 100), (15, 4096), (33, 64)])
+@pytest.mark.parametrize("n_digits,B", [(3, 100), (15, 4096), (33, 64), (5, 77), (40, 33), (15, 1)])
 def test_fused_chain_equals_per_apply_kernels(cuda, n_digits, B):
     """sum_n through the fused chain kernels vs the per-apply Toeplitz kernels: forward
     bit-identical, gradients within fp32 rounding; intermediates can still be read."""
