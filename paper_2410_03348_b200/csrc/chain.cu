@@ -13,29 +13,28 @@
 // Reference semantics per step: provenance.py:233-253 (gather, conj, group_disj + clamp);
 // backward tensor.py:287 (clamp pass-through), :415, :240, :386-391.
 //
-// Mapping (B200): a CTA owns 64 samples for the whole chain; lane l holds the sample PAIR
-// (b0 + 2l, b0 + 2l + 1) so every multiply-add is one packed FFMA2 (fma.rn.f32x2, two
-// IEEE fp32 FMAs — identical rounding to two FFMAs) and every shared-memory access is one
-// conflict-free 8-byte LDS.64/STS.64 per lane.  The warps of the CTA split each step's
-// output tiles (R rows each) and share the state through a ping-pong pair of
-// [rows][32 lanes] float2 shared-memory buffers.  Intermediate states go to HBM in a
-// CTA-blocked layout ([cta][row][64 samples]) so a tile's rows are 256-byte lines at
-// immediate offsets from one base pointer.
+// Mapping (B200).  A warp owns 16 samples for the whole chain and is self-contained: its
+// state lives in its own slice of shared memory, so the 14 sequential steps of a Sum-15
+// chain need only __syncwarp, never a block barrier.  Lane = (row group g = lane / 8,
+// sample pair c = lane % 8): the four row groups work on four output tiles of R rows at
+// once, and each lane holds the sample PAIR (2c, 2c+1), so every multiply-add is one
+// packed FFMA2 (fma.rn.f32x2: two IEEE fp32 FMAs, identical rounding to two FFMAs) and
+// every shared-memory access is one 8-byte LDS.64/STS.64.  Shared rows are 8 pairs + 1 pad
+// (72 B), which puts the four groups' tiles (R = 8 rows apart) on alternating bank halves:
+// a warp-wide LDS.64 costs the minimum two wavefronts.  Intermediate states go to HBM in a
+// warp-blocked layout ([warp][row][16 samples]: one 64-byte segment per group-row).
 #include "common.cuh"
 
 namespace sg {
 
 constexpr int kChainMaxSteps = 32;
-constexpr int kChainR = 8;      // output rows per tile
-constexpr int kChainNW = 8;     // warps per CTA
-constexpr int kChainS = 64;     // samples per CTA (32 lanes x 2)
-constexpr int kRing = 4;        // cp.async filter ring depth
-#ifndef SG_CHAIN_TCH
-#define SG_CHAIN_TCH 2
-#endif
-constexpr int kChainTch = SG_CHAIN_TCH;  // backward: tiles whose v_{i-1} loads are in flight together
+constexpr int kCR = 8;       // rows per group tile
+constexpr int kCG = 4;       // row groups per warp
+constexpr int kCWS = 16;     // samples per warp (8 pairs)
+constexpr int kCP = 9;       // float2 per shared row (8 pairs + 1 pad = 72 bytes)
+constexpr int kRing = 4;     // cp.async filter ring depth (when not all filters are staged)
 constexpr size_t kChainSmemMax = 227 * 1024;
-constexpr size_t kChainSmemTwo = 227 * 1024 / 2 - 1024;  // two CTAs per SM
+constexpr size_t kSmSmem = 228 * 1024;  // per-SM shared memory (CTA reservation included)
 
 struct CRows {
   const float* p;
@@ -48,13 +47,13 @@ struct ChainArgs {
   float* dfilt_p[kChainMaxSteps];  // grad of S_i (strided like filt, writable), backward only
   int64_t dfilt_sr[kChainMaxSteps], dfilt_sb[kChainMaxSteps];
   int n[kChainMaxSteps + 1];       // n[i] = rows of v_i
-  int state_off[kChainMaxSteps + 1];  // row offset of v_i inside a CTA's state block (i = 1..m-1)
-  int state_rows;                  // rows of one CTA's state block
-  int allf;                        // forward: all m filters fit in shared memory
+  int state_off[kChainMaxSteps + 1];  // row offset of v_i inside a warp's state block (i = 1..m-1)
+  int state_rows;                  // rows of one warp's state block
+  int allf;                        // all m filters staged in shared memory up front
   int m;
   int n_max;
   int64_t B;
-  float* states;       // [ceil(B/64)][state_rows][64] clamped intermediate states
+  float* states;       // [ceil(B/16)][state_rows][16] clamped intermediate states
   float* out;          // [n[m]][B]
   const float* g_out;  // backward: [n[m]][B]
   float* dbase_p;      // backward: grad of v_0 (strided like base)
@@ -67,310 +66,381 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(src) : "memory");
 }
+// 8-byte cp.async with zero fill: src_bytes = 0 writes zeros without reading
+__device__ __forceinline__ void cp_async8z(float2* dst, const void* src, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async4z(float* dst, const float* src, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(src), "r"(src_bytes) : "memory");
+}
+// bulk prefetch of a contiguous global range into L2 (no registers, no shared memory)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_ring() { asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 2) : "memory"); }
 
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 clamp01x2(float2 v) { return make_float2(clamp01(v.x), clamp01(v.y)); }
+__device__ __forceinline__ float2 zero2() { return make_float2(0.f, 0.f); }
 
-// The pair of samples a lane owns: (b0, b0 + 1); loads use clamped indices, stores are
-// predicated by nv (number of valid samples of the pair: 0, 1 or 2).
-struct Pair {
-  int64_t b0, ba, bb;
+// What a lane owns: row group g, pair c = samples (b0, b0 + 1) of warp `wid`.  Loads use
+// clamped sample indices, stores are predicated by nv (valid samples of the pair).
+struct Lane {
+  int g, c;
+  int64_t wid, b0, ba, bb;
   int nv;
 };
 
-__device__ __forceinline__ Pair lane_pair(int64_t B, int lane) {
-  Pair p;
-  p.b0 = (int64_t)blockIdx.x * kChainS + 2 * lane;
-  const int64_t left = B - p.b0;
-  p.nv = left <= 0 ? 0 : (left >= 2 ? 2 : 1);
-  p.ba = p.b0 < B ? p.b0 : B - 1;
-  p.bb = p.b0 + 1 < B ? p.b0 + 1 : B - 1;
-  return p;
+__device__ __forceinline__ Lane lane_of(int64_t B) {
+  Lane L;
+  const int lane = threadIdx.x & 31;
+  L.g = lane >> 3;
+  L.c = lane & 7;
+  L.wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  L.b0 = L.wid * kCWS + 2 * L.c;
+  const int64_t left = B - L.b0;
+  L.nv = left <= 0 ? 0 : (left >= 2 ? 2 : 1);
+  L.ba = L.b0 < B ? L.b0 : B - 1;
+  L.bb = L.b0 + 1 < B ? L.b0 + 1 : B - 1;
+  return L;
 }
 
-// Row `row` of a strided operand for the lane's two samples.
-__device__ __forceinline__ float2 ld_strided(const CRows& S, const Pair& p, int64_t row) {
-  return make_float2(__ldg(S.p + p.ba * S.sb + row * S.sr), __ldg(S.p + p.bb * S.sb + row * S.sr));
+__device__ __forceinline__ float2 ld_strided(const CRows& S, const Lane& L, int64_t row) {
+  return make_float2(__ldg(S.p + L.ba * S.sb + row * S.sr), __ldg(S.p + L.bb * S.sb + row * S.sr));
 }
 
-__device__ __forceinline__ void st_strided(float* base, int64_t sr, int64_t sb, const Pair& p, int64_t row, float2 v) {
-  if (p.nv > 0) base[p.b0 * sb + row * sr] = v.x;
-  if (p.nv > 1) base[(p.b0 + 1) * sb + row * sr] = v.y;
+__device__ __forceinline__ void st_strided(float* base, int64_t sr, int64_t sb, const Lane& L, int64_t row, float2 v) {
+  if (L.nv > 0) base[L.b0 * sb + row * sr] = v.x;
+  if (L.nv > 1) base[(L.b0 + 1) * sb + row * sr] = v.y;
 }
 
-// [rows][B] contiguous row-major (out, g_out): 8-byte vector access when B is even
-// (then a pair is either fully valid or fully past the end).
+// [rows][B] row-major (out, g_out): 8-byte vector access when B is even (then a pair is
+// either fully valid or fully past the end).
 template <bool VEC>
-__device__ __forceinline__ float2 ld_rowmajor(const float* q, const Pair& p) {  // q = row start
+__device__ __forceinline__ float2 ld_rowmajor(const float* q, const Lane& L) {  // q = row start
   if constexpr (VEC) {
-    return p.nv == 2 ? __ldg(reinterpret_cast<const float2*>(q + p.b0)) : make_float2(0.f, 0.f);
+    return L.nv == 2 ? __ldg(reinterpret_cast<const float2*>(q + L.b0)) : zero2();
   } else {
-    return make_float2(__ldg(q + p.ba), __ldg(q + p.bb));
+    return make_float2(__ldg(q + L.ba), __ldg(q + L.bb));
   }
 }
 
 template <bool VEC>
-__device__ __forceinline__ void st_rowmajor(float* q, const Pair& p, float2 v) {
+__device__ __forceinline__ void st_rowmajor(float* q, const Lane& L, float2 v) {
   if constexpr (VEC) {
-    if (p.nv == 2) *reinterpret_cast<float2*>(q + p.b0) = v;
+    if (L.nv == 2) *reinterpret_cast<float2*>(q + L.b0) = v;
   } else {
-    if (p.nv > 0) q[p.b0] = v.x;
-    if (p.nv > 1) q[p.b0 + 1] = v.y;
+    if (L.nv > 0) q[L.b0] = v.x;
+    if (L.nv > 1) q[L.b0 + 1] = v.y;
   }
 }
 
-// Filter S (KF rows of this CTA's 64 samples) -> ring slot, as float2 [KF][32].
+// Filter S (KF rows of the warp's 16 samples) -> shared slot `slot` ([KF][kCP] float2).
+// Element e = lane + 32k: row e / 16, sample e % 16 (pair, half).
 template <int KF>
-__device__ __forceinline__ void stage_filter(float2* ring, int slot, const CRows& S, const Pair& p, int lane,
-                                             int warp) {
-  float* d = reinterpret_cast<float*>(ring + (size_t)slot * KF * kWarp + lane);
-  const float* qa = S.p + p.ba * S.sb;
-  const float* qb = S.p + p.bb * S.sb;
-  for (int j = warp; j < KF; j += kChainNW) {
-    cp_async4(d + 2 * j * kWarp, qa + (int64_t)j * S.sr);
-    cp_async4(d + 2 * j * kWarp + 1, qb + (int64_t)j * S.sr);
+__device__ __forceinline__ void stage_filter(float2* F, int slot, const CRows& S, const Lane& L, int64_t B) {
+  const int lane = threadIdx.x & 31;
+  float* d = reinterpret_cast<float*>(F + (size_t)slot * KF * kCP);
+  const int64_t wb = L.wid * kCWS;
+#pragma unroll
+  for (int e0 = 0; e0 < KF * kCWS; e0 += 32) {
+    const int e = e0 + lane;
+    if (KF * kCWS % 32 == 0 || e < KF * kCWS) {
+      const int j = e >> 4, t = e & 15;
+      int64_t b = wb + t;
+      b = b < B ? b : B - 1;
+      cp_async4(d + (j * kCP + (t >> 1)) * 2 + (t & 1), S.p + b * S.sb + (int64_t)j * S.sr);
+    }
   }
+}
+
+// acc[r] = sum_{j ascending} w[r + KF-1-j] * f[j] (the k_conv_fwd order), computed j
+// outer / r inner so the R accumulators are independent back-to-back FFMA2s.
+template <int KF, int R>
+__device__ __forceinline__ void conv_tile(float2 (&acc)[R], const float2 (&w)[R + KF - 1], const float2 (&f)[KF]) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = zero2();
+#pragma unroll
+  for (int j = 0; j < KF; ++j)
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = ffma2(w[r + KF - 1 - j], f[j], acc[r]);
 }
 
 __host__ __device__ constexpr int round_up(int a, int r) { return (a + r - 1) / r * r; }
 
-// Shared-memory rows ([rows][32] float2 = 256 B each) of the forward / backward kernels.
-__host__ __device__ inline int fwd_vrows(int kf, int n_max) { return (kf - 1) + round_up(n_max, kChainR); }
-__host__ __device__ inline int bwd_grows(int kf, int n_max) { return round_up(n_max, kChainR) + kChainR + kf; }
-inline size_t fwd_smem_bytes(int kf, int n_max, int fslots = kRing) {
-  return (size_t)(fslots * kf + 2 * fwd_vrows(kf, n_max)) * kWarp * sizeof(float2);
+// Shared rows of one warp's slice (kCP float2 = 72 B each).  The state is updated IN
+// PLACE (one buffer): rounds of kCG tiles are warp-uniform and every round loads all its
+// windows before it stores (with a __syncwarp between), so no tile overwrites a row that
+// another group of the same round still has to read.
+constexpr int kRound = kCG * kCR;  // rows per warp round
+__host__ __device__ inline int fwd_vrows(int kf, int n_max) { return (kf - 1) + round_up(n_max, kRound); }
+__host__ __device__ inline int bwd_grows(int kf, int n_max) { return round_up(n_max, kRound) + kf + kCR; }
+inline size_t fwd_warp_bytes(int kf, int n_max, int fslots) {
+  return (size_t)(fslots * kf + fwd_vrows(kf, n_max)) * kCP * sizeof(float2);
 }
-inline size_t bwd_smem_bytes(int kf, int n_max) {
-  return (size_t)(kRing * kf + 2 * bwd_grows(kf, n_max) + kChainNW * kf) * kWarp * sizeof(float2);
+inline size_t bwd_warp_bytes(int kf, int n_max) {
+  return (size_t)(kRing * kf + bwd_grows(kf, n_max) + kCG * kf) * kCP * sizeof(float2);
+}
+// resident warps per SM for a per-warp slice (one warp per CTA; 1 KB reserved per CTA)
+inline int warps_per_sm(size_t wbytes) {
+  const int w = (int)(kSmSmem / (wbytes + 1024));
+  return w > 32 ? 32 : w;
 }
 
-// Forward.  Source buffer rows >= n_{i-1} are always exactly 0 (never written, or
+// Forward.  Rows >= n_{i-1} of the source buffer are always exactly 0 (never written, or
 // clamp01(0) from a padded tile of an earlier, shorter step), and kf-1 zero rows sit in
-// front, so every window load is unconditional.  Filters arrive through the cp.async ring
-// kRing-1 steps ahead; inside a step the only global traffic is the (streaming) stores.
+// front, so every window load is unconditional.
 template <int KF, bool VEC>
-__global__ void __launch_bounds__(kChainNW * 32, 2) k_chain_fwd(const ChainArgs a) {
+__global__ void __launch_bounds__(32) k_chain_fwd(const ChainArgs a) {
   extern __shared__ float2 smem2[];
-  constexpr int R = kChainR, PAD = KF - 1;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const Pair pr = lane_pair(a.B, lane);
+  constexpr int R = kCR, PAD = KF - 1;
+  const Lane L = lane_of(a.B);
   const int vrows = fwd_vrows(KF, a.n_max);
-  // all m filters staged up front when they fit (one exposed latency for the whole
-  // chain), else a ring of kRing slots refilled kRing-1 steps ahead
   const int fslots = a.allf ? a.m : kRing;
-  float2* ring = smem2;
-  float2* VA = ring + (size_t)fslots * KF * kWarp;
-  float2* VB = VA + (size_t)vrows * kWarp;
+  float2* F = smem2;
+  float2* V = F + (size_t)fslots * KF * kCP;
   pdl_wait_c();
   if (a.allf) {
-    for (int s = 1; s <= a.m; ++s) stage_filter<KF>(ring, s - 1, a.filt[s - 1], pr, lane, warp);
+    for (int s = 1; s <= a.m; ++s) stage_filter<KF>(F, s - 1, a.filt[s - 1], L, a.B);
     cp_commit();
   } else {
     for (int s = 1; s < kRing; ++s) {
-      if (s <= a.m) stage_filter<KF>(ring, s % kRing, a.filt[s - 1], pr, lane, warp);
+      if (s <= a.m) stage_filter<KF>(F, s % kRing, a.filt[s - 1], L, a.B);
       cp_commit();
     }
   }
-  for (int r = warp; r < vrows; r += kChainNW) {
+  for (int r = L.g; r < vrows; r += kCG) {
     const int s = r - PAD;
-    VA[r * kWarp + lane] = (s >= 0 && s < a.n[0]) ? ld_strided(a.base, pr, s) : make_float2(0.f, 0.f);
-    VB[r * kWarp + lane] = make_float2(0.f, 0.f);
+    const bool in = s >= 0 && s < a.n[0];
+    float* d = reinterpret_cast<float*>(V + r * kCP + L.c);
+    const float* q = a.base.p + (int64_t)(in ? s : 0) * a.base.sr;
+    cp_async4z(d, q + L.ba * a.base.sb, in ? 4 : 0);
+    cp_async4z(d + 1, q + L.bb * a.base.sb, in ? 4 : 0);
   }
-  if (a.allf)
-    cp_wait_all();
-  else
-    cp_wait_ring();
-  __syncthreads();
-  const float2* src = VA + PAD * kWarp + lane;
-  float2* dst = VB + PAD * kWarp + lane;
-  float2* sblk = reinterpret_cast<float2*>(a.states) + (size_t)blockIdx.x * a.state_rows * kWarp + lane;
+  cp_commit();
+  cp_wait_all();
+  __syncwarp();
+  float2* v0 = V + PAD * kCP + L.c;  // state row 0 of this lane's pair
+  float2* sblk = reinterpret_cast<float2*>(a.states) + (size_t)L.wid * a.state_rows * (kCWS / 2) + L.c;
   for (int i = 1; i <= a.m; ++i) {
     if (!a.allf) {
       const int s = i + kRing - 1;
-      if (s <= a.m) stage_filter<KF>(ring, s % kRing, a.filt[s - 1], pr, lane, warp);
+      if (s <= a.m) stage_filter<KF>(F, s % kRing, a.filt[s - 1], L, a.B);
       cp_commit();
     }
     float2 f[KF];
     {
-      const float2* F = ring + (size_t)(a.allf ? i - 1 : i % kRing) * KF * kWarp + lane;
+      const float2* Fi = F + (size_t)(a.allf ? i - 1 : i % kRing) * KF * kCP + L.c;
 #pragma unroll
-      for (int j = 0; j < KF; ++j) f[j] = F[j * kWarp];
+      for (int j = 0; j < KF; ++j) f[j] = Fi[j * kCP];
     }
     const int nout = a.n[i];
-    if (i < a.m) {
-      float2* gst = sblk + (size_t)a.state_off[i] * kWarp;
-      for (int o0 = warp * R; o0 < nout; o0 += kChainNW * R) {
-        float2 w[R + KF - 1];
-        const float2* p = src + (o0 - PAD) * kWarp;
+    const bool last = i == a.m;
+    float2* gst = sblk + (size_t)a.state_off[i] * (kCWS / 2);
+    // rounds in DESCENDING row order: out[o] reads v[o-KF+1 .. o], so a round only reads
+    // rows that no later (lower) round has overwritten yet
+    for (int k = round_up(nout, kRound) / kRound - 1; k >= 0; --k) {
+      const int o0 = k * kRound + L.g * R;
+      float2 w[R + KF - 1];
+      const float2* p = v0 + (o0 - PAD) * kCP;
 #pragma unroll
-        for (int u = 0; u < R + KF - 1; ++u) w[u] = p[u * kWarp];
+      for (int u = 0; u < R + KF - 1; ++u) w[u] = p[u * kCP];
+      float2 acc[R];
+      conv_tile<KF, R>(acc, w, f);
+      __syncwarp();  // every group's window is loaded before any group stores
+      if (!last) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int j = 0; j < KF; ++j) acc = ffma2(w[r + KF - 1 - j], f[j], acc);
-          const float2 v = clamp01x2(acc);
-          dst[(o0 + r) * kWarp] = v;  // padded tile rows >= nout get clamp01(0) = 0
-          if (o0 + r < nout) gst[(o0 + r) * kWarp] = v;
+          const float2 v = clamp01x2(acc[r]);
+          v0[(o0 + r) * kCP] = v;  // padded rows >= nout get clamp01(0) = 0
+          if (o0 + r < nout) gst[(o0 + r) * (kCWS / 2)] = v;
         }
-      }
-    } else {
-      for (int o0 = warp * R; o0 < nout; o0 += kChainNW * R) {
-        float2 w[R + KF - 1];
-        const float2* p = src + (o0 - PAD) * kWarp;
-#pragma unroll
-        for (int u = 0; u < R + KF - 1; ++u) w[u] = p[u * kWarp];
+      } else {
         float* q = a.out + (size_t)o0 * a.B;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int j = 0; j < KF; ++j) acc = ffma2(w[r + KF - 1 - j], f[j], acc);
-          if (o0 + r < nout) st_rowmajor<VEC>(q, pr, clamp01x2(acc));
+          if (o0 + r < nout) st_rowmajor<VEC>(q, L, clamp01x2(acc[r]));
           q += a.B;
         }
       }
     }
     if (!a.allf) cp_wait_ring();
-    __syncthreads();
-    const float2* t = src;
-    src = dst;
-    dst = const_cast<float2*>(t);
+    __syncwarp();
   }
 }
 
-// v_{ii-1} rows c0 + q*NW*R + r (the warp's chunk of tiles) of step ii for the lane's
-// pair; rows past the state's end read as 0 (they meet nonzero G rows in the dS sums).
-template <int R>
-__device__ __forceinline__ void load_prev(float2 (&pv)[kChainTch][R], const ChainArgs& a, const float2* sblk,
-                                          const Pair& pr, int ii, int c0) {
+// v_{ii-1} rows s0 .. s0+R-1 of step ii for the lane's pair (0 past the state's end: those
+// rows meet nonzero G rows in the dS sums).  FIRST: v_0 is the (strided) base operand.
+template <int R, bool FIRST>
+__device__ __forceinline__ void load_prev(float2 (&pv)[R], const ChainArgs& a, const float2* sblk, const Lane& L,
+                                          int ii, int s0) {
   const int nin = a.n[ii - 1];
-  const float2* pst = sblk + (size_t)a.state_off[ii - 1] * kWarp;
+  if constexpr (!FIRST) {
+    const float2* p = sblk + (size_t)(a.state_off[ii - 1] + s0) * (kCWS / 2);
 #pragma unroll
-  for (int q = 0; q < kChainTch; ++q)
+    for (int r = 0; r < R; ++r) pv[r] = s0 + r < nin ? p[r * (kCWS / 2)] : zero2();
+  } else {
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int s = c0 + q * kChainNW * R + r;
-      if (s >= nin)
-        pv[q][r] = make_float2(0.f, 0.f);
-      else if (ii > 1)
-        pv[q][r] = pst[s * kWarp];
-      else
-        pv[q][r] = ld_strided(a.base, pr, s);
-    }
+    for (int r = 0; r < R; ++r) pv[r] = s0 + r < nin ? ld_strided(a.base, L, s0 + r) : zero2();
+  }
 }
 
-// Backward.  The upstream gradient G of the current step lives in a ping-pong pair of
-// shared buffers (rows past each step's length zeroed, so windows are unconditional).
-// Per step every warp first issues the loads of v_{i-1} for kChainTch of its tiles at
-// once, then computes G_{i-1} = G_i (*)^T S_i and its dS_i partials.  dS partials are
-// reduced across the warps in shared memory in fixed order (deterministic, no atomics).
+// One backward step (apply i), in place on G.  Rounds ascend: G_{i-1}[s] reads G_i[s ..
+// s+KF-1], so a round only reads rows no earlier round has overwritten, and inside a round
+// every group loads its window before any group stores (__syncwarp).  Per tile: rows
+// s0..s0+R-1 of G_{i-1} = G_i (*)^T S_i (j outer / rows inner for ILP; per-row order j
+// ascending as in k_conv_bwd) and the tile's dS_i partials (rows ascending, KF chains).
+// The v_{i-1} rows of a group's next tile are in flight (second register set) while the
+// current tile computes; pvA holds the first tile on entry and the next step's first tile
+// on exit.  The four groups' dS partials are summed through shared scratch in fixed order
+// (deterministic, no atomics).
+template <int KF, int R, bool FIRST>
+__device__ __forceinline__ void bwd_round(float2* G, const float2 (&f)[KF], const float2 (&pv)[R], float2 (&d2)[KF],
+                                          int s0, int nin, const ChainArgs& a, const Lane& L) {
+  float2 gw[R + KF - 1];
+#pragma unroll
+  for (int u = 0; u < R + KF - 1; ++u) gw[u] = G[(s0 + u) * kCP];
+  float2 acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = zero2();
+#pragma unroll
+  for (int j = 0; j < KF; ++j)
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = ffma2(gw[r + j], f[j], acc[r]);
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int j = 0; j < KF; ++j) d2[j] = ffma2(gw[r + j], pv[r], d2[j]);
+  if constexpr (!FIRST) {
+    __syncwarp();  // every group's window is loaded before any group stores
+#pragma unroll
+    for (int r = 0; r < R; ++r) G[(s0 + r) * kCP] = s0 + r < nin ? acc[r] : zero2();
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (s0 + r < nin) st_strided(a.dbase_p, a.dbase_sr, a.dbase_sb, L, s0 + r, acc[r]);
+  }
+}
+
+template <int KF, int R, bool FIRST>
+__device__ __forceinline__ void bwd_step(float2* G, float2* scratch, const float2 (&f)[KF], float2 (&pvA)[R], int i,
+                                         const ChainArgs& a, const float2* sblk, const Lane& L) {
+  constexpr int STEP = kRound;
+  const int nin = a.n[i - 1];
+  const int kr = round_up(nin, STEP) / STEP;  // warp-uniform round count
+  float2 d2[KF];
+#pragma unroll
+  for (int j = 0; j < KF; ++j) d2[j] = zero2();
+  float2 pvB[R];
+  const int s0g = L.g * R;
+  for (int k = 0; k < kr; k += 2) {
+    const int s0 = k * STEP + s0g;
+    if (k + 1 < kr) load_prev<R, FIRST>(pvB, a, sblk, L, i, s0 + STEP);
+    bwd_round<KF, R, FIRST>(G, f, pvA, d2, s0, nin, a, L);
+    if (k + 1 >= kr) break;
+    if (k + 2 < kr) load_prev<R, FIRST>(pvA, a, sblk, L, i, s0 + 2 * STEP);
+    bwd_round<KF, R, FIRST>(G, f, pvB, d2, s0 + STEP, nin, a, L);
+  }
+  if constexpr (!FIRST) {
+    // rows [kr*STEP, kr*STEP + KF - 1) may still hold G_i; the next step's windows reach them
+    for (int r = kr * STEP + L.g; r < kr * STEP + KF - 1; r += kCG) G[r * kCP] = zero2();
+    const int nn = a.n[i - 2];
+    if (i - 1 > 1) {
+      load_prev<R, false>(pvA, a, sblk, L, i - 1, s0g);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) pvA[r] = s0g + r < nn ? ld_strided(a.base, L, s0g + r) : zero2();
+    }
+  }
+  // dS_i: group partials -> scratch rows g * KF + j, summed in fixed group order
+#pragma unroll
+  for (int j = 0; j < KF; ++j) scratch[(L.g * KF + j) * kCP] = d2[j];
+  __syncwarp();
+  float* da = a.dfilt_p[i - 1] + L.b0 * a.dfilt_sb[i - 1];
+  const int64_t dsr = a.dfilt_sr[i - 1], dsb = a.dfilt_sb[i - 1];
+#pragma unroll
+  for (int j0 = 0; j0 < KF; j0 += kCG) {
+    const int j = j0 + L.g;
+    if (j < KF) {
+      float2 v = scratch[j * kCP];
+#pragma unroll
+      for (int g = 1; g < kCG; ++g) v = __fadd2_rn(v, scratch[(g * KF + j) * kCP]);
+      if (L.nv > 0) da[j * dsr] = v.x;
+      if (L.nv > 1) da[j * dsr + dsb] = v.y;
+    }
+  }
+}
+
+// Backward.  The upstream gradient G of the current step lives in one shared buffer,
+// updated in place step by step (rows past each step's length zeroed, so windows are
+// unconditional).
 template <int KF, bool VEC>
-__global__ void __launch_bounds__(kChainNW * 32, 2) k_chain_bwd(const ChainArgs a) {
+__global__ void __launch_bounds__(32) k_chain_bwd(const ChainArgs a) {
   extern __shared__ float2 smem2[];
-  constexpr int R = kChainR;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const Pair pr = lane_pair(a.B, lane);
+  constexpr int R = kCR;
+  const Lane L = lane_of(a.B);
   const int grows = bwd_grows(KF, a.n_max);
-  float2* ring = smem2;
-  float2* GA = ring + kRing * KF * kWarp;
-  float2* GB = GA + (size_t)grows * kWarp;
-  float2* red = GB + (size_t)grows * kWarp;  // [kChainNW][KF][32]
+  float2* F = smem2;
+  float2* G = F + kRing * KF * kCP;
+  float2* scratch = G + (size_t)grows * kCP;  // [kCG * KF] rows
   pdl_wait_c();
   // backward step t handles apply i = m - t; its filter sits in ring slot t % kRing
   for (int t = 0; t < kRing - 1; ++t) {
-    if (t < a.m) stage_filter<KF>(ring, t % kRing, a.filt[a.m - 1 - t], pr, lane, warp);
+    if (t < a.m) stage_filter<KF>(F, t % kRing, a.filt[a.m - 1 - t], L, a.B);
     cp_commit();
   }
   {
+    // g_out rows -> G through cp.async (all rows in flight at once), zero-filled past the
+    // last row and for samples past B; joins the first ring group
     const int nm = a.n[a.m];
-    for (int r = warp; r < grows; r += kChainNW) {
-      GA[r * kWarp + lane] = r < nm ? ld_rowmajor<VEC>(a.g_out + (size_t)r * a.B, pr) : make_float2(0.f, 0.f);
-      GB[r * kWarp + lane] = make_float2(0.f, 0.f);
+    for (int r = L.g; r < grows; r += kCG) {
+      const float* q = a.g_out + (size_t)(r < nm ? r : 0) * a.B;
+      if (VEC) {
+        cp_async8z(G + r * kCP + L.c, q + L.ba, (r < nm && L.nv == 2) ? 8 : 0);
+      } else {
+        float* d = reinterpret_cast<float*>(G + r * kCP + L.c);
+        cp_async4z(d, q + L.ba, (r < nm && L.nv > 0) ? 4 : 0);
+        cp_async4z(d + 1, q + L.bb, (r < nm && L.nv > 1) ? 4 : 0);
+      }
     }
+    cp_commit();
   }
-  cp_wait_ring();
-  __syncthreads();
-  const float2* G = GA + lane;
-  float2* Gn = GB + lane;
   const float2* sblk =
-      reinterpret_cast<const float2*>(a.states) + (size_t)blockIdx.x * a.state_rows * kWarp + lane;
-  // v_{i-1} rows of the warp's first chunk of tiles are loaded into registers one step
-  // ahead (at the end of step i+1), so their latency overlaps the barrier, the dS
-  // reduction and the G part of the next step.
-  float2 pv[kChainTch][R];
-  load_prev<R>(pv, a, sblk, pr, a.m, warp * R);
+      reinterpret_cast<const float2*>(a.states) + (size_t)L.wid * a.state_rows * (kCWS / 2) + L.c;
+  float2 pv[R];
+  if (a.m > 1)
+    load_prev<R, false>(pv, a, sblk, L, a.m, L.g * R);
+  else
+    load_prev<R, true>(pv, a, sblk, L, a.m, L.g * R);
+  if (a.m > 2 && (threadIdx.x & 31) == 0)
+    prefetch_l2_bulk(sblk - L.c + (size_t)a.state_off[a.m - 2] * (kCWS / 2), a.n[a.m - 2] * kCWS * 4);
+  cp_wait_all();
+  __syncwarp();
   for (int t = 0; t < a.m; ++t) {
     const int i = a.m - t;
     {
       const int tt = t + kRing - 1;
-      if (tt < a.m) stage_filter<KF>(ring, tt % kRing, a.filt[a.m - 1 - tt], pr, lane, warp);
+      if (tt < a.m) stage_filter<KF>(F, tt % kRing, a.filt[a.m - 1 - tt], L, a.B);
       cp_commit();
     }
-    float2 f[KF], d2[KF];
+    float2 f[KF];
     {
-      const float2* F = ring + (size_t)(t % kRing) * KF * kWarp + lane;
+      const float2* Fi = F + (size_t)(t % kRing) * KF * kCP + L.c;
 #pragma unroll
-      for (int j = 0; j < KF; ++j) {
-        f[j] = F[j * kWarp];
-        d2[j] = make_float2(0.f, 0.f);
-      }
+      for (int j = 0; j < KF; ++j) f[j] = Fi[j * kCP];
     }
-    const int nin = a.n[i - 1];
-    for (int c0 = warp * R; c0 < nin; c0 += kChainTch * kChainNW * R) {
-      if (c0 != warp * R) load_prev<R>(pv, a, sblk, pr, i, c0);  // chains longer than one chunk
-#pragma unroll
-      for (int q = 0; q < kChainTch; ++q) {
-        const int s0 = c0 + q * kChainNW * R;
-        if (s0 >= nin) break;
-        float2 gw[R + KF - 1];
-#pragma unroll
-        for (int u = 0; u < R + KF - 1; ++u) gw[u] = G[(s0 + u) * kWarp];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int j = 0; j < KF; ++j) acc = ffma2(gw[r + j], f[j], acc);
-          const int s = s0 + r;
-          if (i > 1)
-            Gn[s * kWarp] = s < nin ? acc : make_float2(0.f, 0.f);
-          else if (s < nin)
-            st_strided(a.dbase_p, a.dbase_sr, a.dbase_sb, pr, s, acc);
-        }
-#pragma unroll
-        for (int j = 0; j < KF; ++j) {
-          float2 acc = d2[j];
-#pragma unroll
-          for (int r = 0; r < R; ++r) acc = ffma2(gw[r + j], pv[q][r], acc);
-          d2[j] = acc;
-        }
-      }
-    }
-    if (i > 1)  // rows past the padded tiles that the next step's windows can reach
-      for (int r = round_up(nin, R) + warp; r < nin + R + KF - 1; r += kChainNW) Gn[r * kWarp] = make_float2(0.f, 0.f);
-    float2* rd = red + lane;
-#pragma unroll
-    for (int j = 0; j < KF; ++j) rd[(warp * KF + j) * kWarp] = d2[j];
-    if (i > 1) load_prev<R>(pv, a, sblk, pr, i - 1, warp * R);
+    if (i > 3 && (threadIdx.x & 31) == 0)  // v_{i-3} (read in step i-2) -> L2
+      prefetch_l2_bulk(sblk - L.c + (size_t)a.state_off[i - 3] * (kCWS / 2), a.n[i - 3] * kCWS * 4);
+    if (i > 1)
+      bwd_step<KF, R, false>(G + L.c, scratch + L.c, f, pv, i, a, sblk, L);
+    else
+      bwd_step<KF, R, true>(G + L.c, scratch + L.c, f, pv, i, a, sblk, L);
     cp_wait_ring();
-    __syncthreads();
-    for (int j = warp; j < KF; j += kChainNW) {
-      float2 acc = rd[j * kWarp];
-#pragma unroll
-      for (int w = 1; w < kChainNW; ++w) {
-        const float2 v = rd[(w * KF + j) * kWarp];
-        acc.x += v.x;
-        acc.y += v.y;
-      }
-      st_strided(a.dfilt_p[i - 1], a.dfilt_sr[i - 1], a.dfilt_sb[i - 1], pr, j, acc);
-    }
-    __syncthreads();  // red is rewritten by the next step
-    const float2* tmp = G;
-    G = Gn;
-    Gn = const_cast<float2*>(tmp);
+    __syncwarp();
   }
 }
 
@@ -379,8 +449,8 @@ static cudaError_t launch_chain(void (*kernel)(KArgs...), const ChainArgs& a, si
   cudaError_t e = ensure_smem((const void*)kernel, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(ceil_div(a.B, kChainS));
-  cfg.blockDim = dim3(kChainNW * kWarp);
+  cfg.gridDim = dim3(ceil_div(a.B, kCWS));
+  cfg.blockDim = dim3(32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -431,13 +501,13 @@ using namespace sg;
 extern "C" {
 
 int64_t sg_chain_states_elems(int32_t n0, int32_t kf, int32_t m, int64_t B) {
-  return (int64_t)state_rows(n0, kf, m) * (int64_t)ceil_div(B, kChainS) * kChainS;
+  return (int64_t)state_rows(n0, kf, m) * (int64_t)ceil_div(B, kCWS) * kCWS;
 }
 
 int32_t sg_chain_max_rows(int32_t kf) {
   if (kf < 1 || kf > 16) return 0;
   int n = 0;
-  while (fwd_smem_bytes(kf, n + 1) <= kChainSmemMax && bwd_smem_bytes(kf, n + 1) <= kChainSmemMax) ++n;
+  while (fwd_warp_bytes(kf, n + 1, kRing) <= kChainSmemMax && bwd_warp_bytes(kf, n + 1) <= kChainSmemMax) ++n;
   return n;
 }
 
@@ -447,12 +517,15 @@ int sg_chain_fwd(const sg_chain* c, float* out, sg_stream_t stream) {
   if (rc) return rc;
   if (c->B <= 0) return 0;
   a.out = out;
-  // all filters up front if that still leaves two CTAs per SM (or the ring would not either)
-  const size_t ring_smem = fwd_smem_bytes(c->kf, a.n_max);
-  const size_t all_smem = fwd_smem_bytes(c->kf, a.n_max, a.m);
-  SG_RETURN_IF(ring_smem > kChainSmemMax, cudaErrorNotSupported);
-  a.allf = all_smem <= kChainSmemTwo || (ring_smem > kChainSmemTwo && all_smem <= kChainSmemMax);
-  const size_t smem = a.allf ? all_smem : ring_smem;
+  // stage all filters up front unless that costs occupancy the launch could use
+  const size_t ring_bytes = fwd_warp_bytes(c->kf, a.n_max, kRing);
+  const size_t all_bytes = fwd_warp_bytes(c->kf, a.n_max, a.m);
+  SG_RETURN_IF(ring_bytes > kChainSmemMax, cudaErrorNotSupported);
+  const int need = ceil_div(ceil_div(c->B, kCWS), 148);
+  const int occ_ring = warps_per_sm(ring_bytes);
+  const int occ_all = all_bytes <= kChainSmemMax ? warps_per_sm(all_bytes) : 0;
+  a.allf = occ_all >= (need < occ_ring ? need : occ_ring);
+  const size_t smem = a.allf ? all_bytes : ring_bytes;
   cudaStream_t st = (cudaStream_t)stream;
   const bool vec = (c->B % 2 == 0) && ((uintptr_t)out % 8 == 0);
   switch (c->kf) {
@@ -481,7 +554,7 @@ int sg_chain_bwd(const sg_chain* c, const float* grad_out, sg_rows grad_base, co
     a.dfilt_sr[i] = grad_filters[i].stride_row;
     a.dfilt_sb[i] = grad_filters[i].stride_b;
   }
-  const size_t smem = bwd_smem_bytes(c->kf, a.n_max);
+  const size_t smem = bwd_warp_bytes(c->kf, a.n_max);
   SG_RETURN_IF(smem > kChainSmemMax, cudaErrorNotSupported);
   cudaStream_t st = (cudaStream_t)stream;
   const bool vec = (c->B % 2 == 0) && ((uintptr_t)grad_out % 8 == 0);
