@@ -140,13 +140,14 @@ int sg_chain_bwd(const sg_chain* chain, const float* grad_out, sg_rows grad_base
  * loss = -(1/B) sum_b log(max(max(p[t_b][b] / (sum_n p[n][b] + 1e-8), 1e-12), 1e-12)),
  * t_b = -1 marks "no mass" (the floor's penalty, no gradient).  fp64 inside.
  * scratch: >= sg_nll_scratch_bytes(n, B) bytes; its first 8 bytes must be zero before the
- * first sg_nll_fwd on it (a self-resetting ticket); the backward only uses the tail. */
+ * first sg_nll_fwd on it (a self-resetting ticket).  rowsum: [B] doubles, the per-sample
+ * sum_n p[n][b] written by the forward for the backward (saved by the caller). */
 int64_t sg_nll_scratch_bytes(int64_t n, int64_t B);
 int sg_nll_fwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, double* loss,
-               void* scratch, sg_stream_t stream);
+               void* scratch, double* rowsum, sg_stream_t stream);
 /* grad[n][b] = -(g/B) / c_b * (delta(n, t_b) / (s_b + 1e-8) - p[t_b][b] / (s_b + 1e-8)^2) */
 int sg_nll_bwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets,
-               const double* grad_loss, sg_rows grad, void* scratch, sg_stream_t stream);
+               const double* grad_loss, const double* rowsum, sg_rows grad, sg_stream_t stream);
 
 /* ---- row gather (filter / placement / inverse scatter), any tag kind -----------------
  * dst row r = src row idx[r] (idx -1 -> zero row); rows are row_bytes contiguous bytes. */

@@ -28,10 +28,14 @@
 namespace sg {
 
 constexpr int kChainMaxSteps = 32;
-constexpr int kCR = 8;       // rows per group tile
-constexpr int kCG = 4;       // row groups per warp
-constexpr int kCWS = 16;     // samples per warp (8 pairs)
-constexpr int kCP = 9;       // float2 per shared row (8 pairs + 1 pad = 72 bytes)
+#ifndef SG_CHAIN_GROUPS
+#define SG_CHAIN_GROUPS 4
+#endif
+constexpr int kCG = SG_CHAIN_GROUPS;  // row groups per warp
+constexpr int kCR = 32 / kCG;         // rows per group tile
+constexpr int kPairs = 32 / kCG;      // sample pairs per group (lanes per group)
+constexpr int kCWS = 2 * kPairs;      // samples per warp
+constexpr int kCP = kPairs + 1;       // float2 per shared row (+1 pad: groups land on distinct bank sets)
 constexpr int kRing = 4;     // cp.async filter ring depth (when not all filters are staged)
 constexpr size_t kChainSmemMax = 227 * 1024;
 constexpr size_t kSmSmem = 228 * 1024;  // per-SM shared memory (CTA reservation included)
@@ -98,8 +102,8 @@ struct Lane {
 __device__ __forceinline__ Lane lane_of(int64_t B) {
   Lane L;
   const int lane = threadIdx.x & 31;
-  L.g = lane >> 3;
-  L.c = lane & 7;
+  L.g = lane / kPairs;
+  L.c = lane % kPairs;
   L.wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   L.b0 = L.wid * kCWS + 2 * L.c;
   const int64_t left = B - L.b0;
@@ -150,7 +154,7 @@ __device__ __forceinline__ void stage_filter(float2* F, int slot, const CRows& S
   for (int e0 = 0; e0 < KF * kCWS; e0 += 32) {
     const int e = e0 + lane;
     if (KF * kCWS % 32 == 0 || e < KF * kCWS) {
-      const int j = e >> 4, t = e & 15;
+      const int j = e / kCWS, t = e % kCWS;
       int64_t b = wb + t;
       b = b < B ? b : B - 1;
       cp_async4(d + (j * kCP + (t >> 1)) * 2 + (t & 1), S.p + b * S.sb + (int64_t)j * S.sr);
@@ -189,6 +193,40 @@ inline size_t bwd_warp_bytes(int kf, int n_max) {
 inline int warps_per_sm(size_t wbytes) {
   const int w = (int)(kSmSmem / (wbytes + 1024));
   return w > 32 ? 32 : w;
+}
+
+template <int KF, int R>
+__device__ __forceinline__ void fwd_window(float2 (&w)[R + KF - 1], const float2* v0, int o0) {
+  const float2* p = v0 + (o0 - (KF - 1)) * kCP;
+#pragma unroll
+  for (int u = 0; u < R + KF - 1; ++u) w[u] = p[u * kCP];
+}
+
+// One forward round for the lane's group: rows o0..o0+R-1 of v_i from its window.
+template <int KF, int R, bool VEC>
+__device__ __forceinline__ void fwd_round(const float2 (&w)[R + KF - 1], const float2 (&f)[KF], float2* v0,
+                                          float2* gst, int o0, int nout, bool last, const ChainArgs& a,
+                                          const Lane& L) {
+  float2 acc[R];
+  conv_tile<KF, R>(acc, w, f);
+  __syncwarp();  // every group's window (this round's and the next's) is loaded before any store
+  if (!last) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const float2 v = clamp01x2(acc[r]);
+      v0[(o0 + r) * kCP] = v;  // padded rows >= nout get clamp01(0) = 0
+#ifndef SG_CHAIN_NOSTORE
+      if (o0 + r < nout) gst[(o0 + r) * (kCWS / 2)] = v;
+#endif
+    }
+  } else {
+    float* q = a.out + (size_t)o0 * a.B;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (o0 + r < nout) st_rowmajor<VEC>(q, L, clamp01x2(acc[r]));
+      q += a.B;
+    }
+  }
 }
 
 // Forward.  Rows >= n_{i-1} of the source buffer are always exactly 0 (never written, or
@@ -242,31 +280,17 @@ __global__ void __launch_bounds__(32) k_chain_fwd(const ChainArgs a) {
     const bool last = i == a.m;
     float2* gst = sblk + (size_t)a.state_off[i] * (kCWS / 2);
     // rounds in DESCENDING row order: out[o] reads v[o-KF+1 .. o], so a round only reads
-    // rows that no later (lower) round has overwritten yet
-    for (int k = round_up(nout, kRound) / kRound - 1; k >= 0; --k) {
-      const int o0 = k * kRound + L.g * R;
-      float2 w[R + KF - 1];
-      const float2* p = v0 + (o0 - PAD) * kCP;
-#pragma unroll
-      for (int u = 0; u < R + KF - 1; ++u) w[u] = p[u * kCP];
-      float2 acc[R];
-      conv_tile<KF, R>(acc, w, f);
-      __syncwarp();  // every group's window is loaded before any group stores
-      if (!last) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const float2 v = clamp01x2(acc[r]);
-          v0[(o0 + r) * kCP] = v;  // padded rows >= nout get clamp01(0) = 0
-          if (o0 + r < nout) gst[(o0 + r) * (kCWS / 2)] = v;
-        }
-      } else {
-        float* q = a.out + (size_t)o0 * a.B;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if (o0 + r < nout) st_rowmajor<VEC>(q, L, clamp01x2(acc[r]));
-          q += a.B;
-        }
-      }
+    // rows that no later (lower) round has overwritten yet -- which also lets the next
+    // round's windows be loaded while this round computes (two register sets)
+    const int kr = round_up(nout, kRound) / kRound;
+    float2 wA[R + KF - 1], wB[R + KF - 1];
+    fwd_window<KF, R>(wA, v0, (kr - 1) * kRound + L.g * R);
+    for (int k = kr - 1; k >= 0; k -= 2) {
+      if (k >= 1) fwd_window<KF, R>(wB, v0, (k - 1) * kRound + L.g * R);
+      fwd_round<KF, R, VEC>(wA, f, v0, gst, k * kRound + L.g * R, nout, last, a, L);
+      if (k < 1) break;
+      if (k >= 2) fwd_window<KF, R>(wA, v0, (k - 2) * kRound + L.g * R);
+      fwd_round<KF, R, VEC>(wB, f, v0, gst, (k - 1) * kRound + L.g * R, nout, last, a, L);
     }
     if (!a.allf) cp_wait_ring();
     __syncwarp();

@@ -487,51 +487,115 @@ __device__ __forceinline__ double nll_picked(double s, double pt, int64_t t) {
   return fmax(t >= 0 ? fl : 0.0, 1e-12);
 }
 
+// Sum of the CTA's log terms (v: this thread's term); the last CTA to finish
+// (self-resetting ticket) adds the per-CTA partials in CTA order -> *loss.
+__device__ __forceinline__ void nll_finish(double v, double* __restrict__ loss, double* __restrict__ blocks,
+                                           unsigned* __restrict__ counter, int64_t B) {
+  __shared__ double red[32];
+  __shared__ bool last;
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  const int nthreads = blockDim.x * blockDim.y;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((tid & 31) == 0) red[tid >> 5] = v;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (nthreads >> 5); ++w) t += red[w];
+    blocks[blockIdx.x] = t;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  // the whole last CTA adds the partials: thread i sums i, i + T, ... (fixed order), then a
+  // fixed shuffle tree and warp order -> deterministic
+  __threadfence();
+  double t = 0.0;
+  for (unsigned i = tid; i < gridDim.x; i += nthreads) t += __ldcg(blocks + i);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+  __syncthreads();
+  if ((tid & 31) == 0) red[tid >> 5] = t;
+  __syncthreads();
+  if (tid == 0) {
+    double u = 0.0;
+    for (int w = 0; w < (nthreads >> 5); ++w) u += red[w];
+    *loss = -u / (double)B;
+    *counter = 0u;  // self-reset for the next launch / graph replay
+  }
+}
+
+// Two-pass finish (chunks > 1): per-sample sums from the chunk partials.
 __global__ void __launch_bounds__(256) k_nll_fwd(const Rows p, int64_t B, const int64_t* __restrict__ targets,
                                                  const double* __restrict__ part, int chunks,
-                                                 double* __restrict__ loss, double* __restrict__ blocks,
-                                                 unsigned* __restrict__ counter) {
-  __shared__ double red[8];
-  __shared__ bool last;
+                                                 double* __restrict__ rowsum, double* __restrict__ loss,
+                                                 double* __restrict__ blocks, unsigned* __restrict__ counter) {
   const int64_t b0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   pdl_wait();
   double v = 0.0;
   if (b0 < B) {
     const int64_t t = __ldg(targets + b0);
     const double s = nll_rowsum(part, chunks, B, b0);
+    rowsum[b0] = s;
     const double pt = t >= 0 ? (double)p.ld(t, b0) : 0.0;
     v = log(nll_picked(s, pt, t));
   }
+  nll_finish(v, loss, blocks, counter, B);
+}
+
+// One-pass forward (chunks == 1): a CTA sums all rows of its 32 samples (warps split the
+// rows, same order as k_nll_partial), then finishes their log terms.
+__global__ void __launch_bounds__(256) k_nll_fwd1(const Rows p, int n, int64_t B, const int64_t* __restrict__ targets,
+                                                  double* __restrict__ rowsum, double* __restrict__ loss,
+                                                  double* __restrict__ blocks, unsigned* __restrict__ counter) {
+  __shared__ double red[kNllWarps][kWarp];
+  const int lane = threadIdx.x, warp = threadIdx.y;
+  const int64_t b0 = (int64_t)blockIdx.x * kWarp + lane;
+  const int64_t b = b0 < B ? b0 : B - 1;
+  pdl_wait();
+  // rows warp, warp + W, ...: 8 loads in flight per thread, added in row order
+  double acc0 = 0.0, acc1 = 0.0;
+  int r = warp;
+  for (; r + 7 * kNllWarps < n; r += 8 * kNllWarps) {
+    float x[8];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    blocks[blockIdx.x] = t;
-    __threadfence();
-    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    for (int k = 0; k < 8; ++k) x[k] = p.ld(r + k * kNllWarps, b);
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+      acc0 += (double)x[k];
+      acc1 += (double)x[k + 1];
+    }
   }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    double t = 0.0;
-    for (unsigned i = 0; i < gridDim.x; ++i) t += ((volatile double*)blocks)[i];
-    *loss = -t / (double)B;
-    *counter = 0u;  // self-reset for the next launch / graph replay
+  for (; r + kNllWarps < n; r += 2 * kNllWarps) {
+    acc0 += (double)p.ld(r, b);
+    acc1 += (double)p.ld(r + kNllWarps, b);
   }
+  if (r < n) acc0 += (double)p.ld(r, b);
+  red[warp][lane] = acc0 + acc1;
+  __syncthreads();
+  double v = 0.0;
+  if (warp == 0 && b0 < B) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kNllWarps; ++w) s += red[w][lane];
+    rowsum[b0] = s;
+    const int64_t t = __ldg(targets + b0);
+    const double pt = t >= 0 ? (double)p.ld(t, b0) : 0.0;
+    v = log(nll_picked(s, pt, t));
+  }
+  nll_finish(v, loss, blocks, counter, B);
 }
 
 __global__ void __launch_bounds__(256) k_nll_bwd(const Rows p, int n, int64_t B, const int64_t* __restrict__ targets,
-                                                 const double* __restrict__ gloss, const double* __restrict__ part,
-                                                 int chunks, int rows_per, WRows grad) {
+                                                 const double* __restrict__ gloss, const double* __restrict__ rowsum,
+                                                 int rows_per, WRows grad) {
   const int lane = threadIdx.x, warp = threadIdx.y;
   const int64_t b = (int64_t)blockIdx.x * kWarp + lane;
   pdl_wait();
   if (b >= B) return;
   const int64_t t = __ldg(targets + b);
-  const double s = nll_rowsum(part, chunks, B, b);
+  const double s = rowsum[b];
   const double pt = t >= 0 ? (double)p.ld(t, b) : 0.0;
   const double c = nll_picked(s, pt, t);
   const double den = s + 1e-8;
@@ -687,43 +751,41 @@ int sg_damp_rows_add(const sg_rows A, const int32_t* ia, const sg_rows Bm, const
 
 int64_t sg_nll_scratch_bytes(int64_t n, int64_t B) {
   const int chunks = nll_chunks(n, B);
-  const int blocks = ceil_div(B, 256);
-  return (int64_t)(2 + blocks + (int64_t)chunks * B) * (int64_t)sizeof(double);
+  const int blocks = ceil_div(B, kWarp);
+  return (int64_t)(2 + blocks + (chunks > 1 ? (int64_t)chunks * B : 0)) * (int64_t)sizeof(double);
 }
 
 // scratch layout (doubles): [0] ticket counter (zero-initialised once, self-resetting),
-// [2, 2 + blocks) per-CTA log-term partials, then [chunks][B] row-sum partials.
+// [2, 2 + blocks) per-CTA log-term partials, then [chunks][B] row-sum partials (chunks > 1).
 int sg_nll_fwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, double* loss, void* scratch,
-               sg_stream_t stream) {
+               double* rowsum, sg_stream_t stream) {
   if (B <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   const int chunks = nll_chunks(n, B);
-  const int rows_per = ceil_div(n, chunks);
-  const int blocks = ceil_div(B, 256);
   double* base = (double*)scratch;
   unsigned* counter = (unsigned*)base;
   double* blk = base + 2;
-  double* part = base + 2 + blocks;
+  if (chunks == 1)
+    return (int)launch(k_nll_fwd1, dim3(ceil_div(B, kWarp)), dim3(kWarp, kNllWarps), 0, st, rows_of(probs), (int)n,
+                       B, targets, rowsum, loss, blk, counter);
+  const int rows_per = ceil_div(n, chunks);
+  const int blocks = ceil_div(B, 256);
+  double* part = base + 2 + ceil_div(B, kWarp);
   cudaError_t e = launch(k_nll_partial, dim3(ceil_div(B, kWarp), chunks), dim3(kWarp, kNllWarps), 0, st,
                          rows_of(probs), (int)n, B, rows_per, part);
   if (e != cudaSuccess) return (int)e;
   return (int)launch(k_nll_fwd, dim3(blocks), dim3(256), 0, st, rows_of(probs), B, targets, (const double*)part, chunks,
-                     loss, blk, counter);
+                     rowsum, loss, blk, counter);
 }
 
-int sg_nll_bwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, const double* grad_loss, sg_rows grad,
-               void* scratch, sg_stream_t stream) {
+int sg_nll_bwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, const double* grad_loss,
+               const double* rowsum, sg_rows grad, sg_stream_t stream) {
   if (B <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   const int chunks = nll_chunks(n, B);
   const int rows_per = ceil_div(n, chunks);
-  const int blocks = ceil_div(B, 256);
-  double* part = (double*)scratch + 2 + blocks;
-  cudaError_t e = launch(k_nll_partial, dim3(ceil_div(B, kWarp), chunks), dim3(kWarp, kNllWarps), 0, st,
-                         rows_of(probs), (int)n, B, rows_per, part);
-  if (e != cudaSuccess) return (int)e;
   return (int)launch(k_nll_bwd, dim3(ceil_div(B, kWarp), chunks), dim3(kWarp, kNllWarps), 0, st, rows_of(probs),
-                     (int)n, B, targets, grad_loss, (const double*)part, chunks, rows_per, wrows_of(grad));
+                     (int)n, B, targets, grad_loss, rowsum, rows_per, wrows_of(grad));
 }
 
 int sg_rows_gather(const void* src, const int32_t* idx, int64_t n_rows, int64_t row_bytes, void* dst,

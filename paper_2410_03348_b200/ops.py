@@ -303,21 +303,21 @@ class NllLoss(torch.autograd.Function):
         dev = probs_nb.device
         loss = torch.empty((), device=dev, dtype=torch.float64)
         scratch = _nll_scratch(dev, n, B)
+        rowsum = torch.empty((B,), device=dev, dtype=torch.float64)
         rc = _lib().sg_nll_fwd(N.rows(probs_nb), n, B, targets.data_ptr(), loss.data_ptr(), scratch.data_ptr(),
-                               N.stream_ptr(dev))
+                               rowsum.data_ptr(), N.stream_ptr(dev))
         N.check(rc, "sg_nll_fwd")
-        ctx.save_for_backward(probs_nb, targets)
+        ctx.save_for_backward(probs_nb, targets, rowsum)
         return loss
 
     @staticmethod
     def backward(ctx, gloss):
-        probs_nb, targets = ctx.saved_tensors
+        probs_nb, targets, rowsum = ctx.saved_tensors
         n, B = probs_nb.shape
         g = gloss.detach().to(torch.float64).reshape(()).contiguous()
         grad = torch.empty_like(probs_nb)
-        scratch = torch.empty(int(_lib().sg_nll_scratch_bytes(n, B)), device=probs_nb.device, dtype=torch.uint8)
-        rc = _lib().sg_nll_bwd(N.rows(probs_nb), n, B, targets.data_ptr(), g.data_ptr(), N.rows(grad),
-                               scratch.data_ptr(), N.stream_ptr(probs_nb.device))
+        rc = _lib().sg_nll_bwd(N.rows(probs_nb), n, B, targets.data_ptr(), g.data_ptr(), rowsum.data_ptr(),
+                               N.rows(grad), N.stream_ptr(probs_nb.device))
         N.check(rc, "sg_nll_bwd")
         return grad, None
 
