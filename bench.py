@@ -362,9 +362,13 @@ def run_gpu_arm(args):
 
     x_pin = x_h.pin_memory()
     t_pin = t_h.pin_memory()
-    host_inputs = [x_pin[i] for i in range(N_DIGITS)] + [t_pin]
     e2e_steps = max(3, min(args.steps, 50))
     gstep = GraphedStep(lambda *a: step(list(a[:N_DIGITS]), a[N_DIGITS]), x + [targets])
+    # the step's host inputs staged in GraphedStep's pinned arena: one H2D copy per step
+    host_inputs = gstep.pinned_inputs()
+    for i in range(N_DIGITS):
+        host_inputs[i].copy_(x_h[i])
+    host_inputs[N_DIGITS].copy_(t_h)
 
     def e2e_graph():
         loss, _ = gstep(*host_inputs)

@@ -413,3 +413,44 @@ def test_fused_chain_intermediate_and_reuse(cuda):
     gb = OP.grad_inputs(obr, wb)
     for i, lf in enumerate(leaves):
         assert_close_rel(lf.grad.cpu().numpy(), ge[i] + gm[i] + gb[i], 1e-5, 1e-6, what=f"leaf {i}")
+
+
+# ------------------------------------------------------------------ whole-step CUDA graph
+def test_graphed_step_matches_eager(cuda):
+    """GraphedStep (public API) replays Sum-4 + loss + backward on new inputs, both through
+    per-input copies and through its pinned arena (one H2D copy); results equal eager."""
+    S = sg()
+    from paper_2410_03348_b200 import programs as P
+    from paper_2410_03348_b200.graph import GraphedStep
+    from paper_2410_03348_b200.learn import loss_nll
+
+    B, nd = 96, 4
+
+    def step(*a):
+        xs, t = list(a[:nd]), a[nd]
+        ctx = S.ProgramContext(S.Damp(), device=cuda)
+        out = P.sum_n(ctx, [S.make_distribution(ctx, x, range(10)) for x in xs])
+        loss = loss_nll(S.get_probs(out), t)
+        return (loss, *torch.autograd.grad(loss, xs))
+
+    rng = np.random.default_rng(5)
+
+    def batch():
+        xs = [torch.tensor(G.rows(rng, B, 10), dtype=torch.float32) for _ in range(nd)]
+        return xs, torch.tensor(rng.integers(0, 9 * nd + 1, size=B), dtype=torch.int64)
+
+    xs0, t0 = batch()
+    g = GraphedStep(step, [x.to(cuda).requires_grad_(True) for x in xs0] + [t0.to(cuda)])
+    for use_arena in (False, True):
+        xs, t = batch()
+        if use_arena:
+            host = g.pinned_inputs()
+            for h, x in zip(host, xs + [t]):
+                h.copy_(x)
+            got = g(*host)
+        else:
+            got = g(*[x.pin_memory() for x in xs], t.pin_memory())
+        got = [o.detach().cpu().clone() for o in got]
+        want = step(*[x.to(cuda).requires_grad_(True) for x in xs], t.to(cuda))
+        for a, b in zip(got, want):
+            np.testing.assert_array_equal(a.numpy(), b.detach().cpu().numpy())
