@@ -454,3 +454,38 @@ def test_graphed_step_matches_eager(cuda):
         want = step(*[x.to(cuda).requires_grad_(True) for x in xs], t.to(cuda))
         for a, b in zip(got, want):
             np.testing.assert_array_equal(a.numpy(), b.detach().cpu().numpy())
+
+
+def test_graphed_step_pipelined_slots(cuda):
+    """GraphedStep(slots=2).submit: alternating captures with the next step's upload on a
+    copy stream give the same losses as eager calls on the same inputs."""
+    S = sg()
+    from paper_2410_03348_b200 import programs as P
+    from paper_2410_03348_b200.graph import GraphedStep
+    from paper_2410_03348_b200.learn import loss_nll
+
+    B, nd = 64, 3
+
+    def step(*a):
+        xs, t = list(a[:nd]), a[nd]
+        ctx = S.ProgramContext(S.Damp(), device=cuda)
+        loss = loss_nll(S.get_probs(P.sum_n(ctx, [S.make_distribution(ctx, x, range(10)) for x in xs])), t)
+        return (loss, *torch.autograd.grad(loss, xs))
+
+    rng = np.random.default_rng(9)
+    batches = []
+    for _ in range(5):
+        xs = [torch.tensor(G.rows(rng, B, 10), dtype=torch.float32) for _ in range(nd)]
+        batches.append(xs + [torch.tensor(rng.integers(0, 9 * nd + 1, size=B), dtype=torch.int64)])
+    g = GraphedStep(step, [x.to(cuda).requires_grad_(x.dtype == torch.float32) for x in batches[0]], slots=2)
+    got = []
+    for bt in batches:
+        slot = g.next_slot()
+        for h, x in zip(g.pinned_inputs(slot), bt):
+            h.copy_(x)
+        out = g.submit()
+        got.append(out[0].detach().clone())
+    torch.cuda.synchronize()
+    for bt, loss in zip(batches, got):
+        want = step(*[x.to(cuda).requires_grad_(x.dtype == torch.float32) for x in bt])[0]
+        assert float(loss) == float(want)
