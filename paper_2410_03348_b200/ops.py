@@ -281,9 +281,11 @@ _NLL_SCRATCH: "dict[tuple, torch.Tensor]" = {}
 
 
 def _nll_scratch(dev, n: int, B: int) -> torch.Tensor:
-    """Per (device, stream) zero-initialised scratch; the kernel resets its counter itself,
-    so the buffer is reused across calls and CUDA-graph replays without a memset."""
-    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    """Per-device zero-initialised scratch; the kernel resets its counter itself, so the
+    buffer is reused across calls, streams and CUDA-graph replays without a memset (a
+    buffer first created during a capture would put its memset into the graph).  Losses
+    on one device must not run concurrently on two streams."""
+    key = dev
     nbytes = int(_lib().sg_nll_scratch_bytes(n, B))
     buf = _NLL_SCRATCH.get(key)
     if buf is None or buf.numel() < nbytes:

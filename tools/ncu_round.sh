@@ -7,9 +7,9 @@ TAG=${TAG:-r01}
 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   --cache-control none --csv --log-file gpurun_out/${TAG}_step_launches.csv \
   python bench.py --quick --steps 2 --warmup 1 > gpurun_out/${TAG}_ncu_quick.out 2>&1; echo "launches rc=$?"
-# skip counts land on the largest launch of a step: the first backward conv (step 14)
-# and the last forward conv (step 14) of the 4th captured/eager step
-for KS in k_conv_bwd:42 k_conv_fwd:55 k_nll_fwd:3; do
+# --set full of one launch of each hot kernel inside the captured Sum-15 step (B=16384);
+# default cache control (flushed before the launch): the cold per-launch roofline case
+for KS in k_chain_bwd:4 k_chain_fwd:4 k_nll_fwd1:4 k_nll_bwd:4; do
   K=${KS%%:*}; S=${KS##*:}
   timeout 300 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 \
     -o gpurun_out/${TAG}_full_$K -f python bench.py --quick --steps 2 --warmup 1 > gpurun_out/${TAG}_ncu_$K.out 2>&1

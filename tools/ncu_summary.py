@@ -143,6 +143,20 @@ def main():
                 lines.append(f"| traffic / duration | {(br + bw) / t / 1e9:.0f} GB/s "
                              f"({100 * (br + bw) / t / 1e9 / PEAK:.1f}% of measured peak) |")
             lines.append("")
+    # per-launch DRAM traffic of the captured kernels -> profiles/traffic.json (bench.py's
+    # roofline.traffic for the dominant kernel)
+    traffic = {}
+    for rep in sorted(OUT.glob(f"{args.tag}_full_*.ncu-rep")):
+        kern = rep.stem.replace(f"{args.tag}_full_", "")
+        for d, u in raw_metrics(rep)[:1]:
+            br = to_si(d.get("dram__bytes_read.sum", ""), u.get("dram__bytes_read.sum", ""))
+            bw = to_si(d.get("dram__bytes_write.sum", ""), u.get("dram__bytes_write.sum", ""))
+            if br is not None and bw is not None:
+                traffic[kern] = {"bytes_per_launch": br + bw, "read": br, "write": bw,
+                                 "batch": 16384 if kern.startswith(("k_chain", "k_nll")) else None,
+                                 "source": f"profiles/{args.tag}_ncu_summary.md (ncu --set full, {rep.name})"}
+    if traffic:
+        (ROOT / "profiles" / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
     dst = ROOT / "profiles" / f"{args.tag}_ncu_summary.md"
     dst.parent.mkdir(exist_ok=True)
     dst.write_text("\n".join(lines) + "\n")
