@@ -185,8 +185,8 @@ def sweep(iters):
                 c = sg.ProgramContext(sg.Damp(), device=DEV)
                 return sg.get_probs(sg.apply(f, *[sg.make_distribution(c, x, syms) for x in xs]))
 
-            def step():
-                return torch.autograd.grad((fwd() * w).sum(), xs)
+            def step():  # d(sum probs * w)/dx: the upstream gradient w goes straight in
+                return torch.autograd.grad(fwd(), xs, grad_outputs=w)
 
             ms_f, mode = timed(lambda: fwd(), iters)
             ms, _ = timed(step, iters)
