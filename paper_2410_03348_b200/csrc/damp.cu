@@ -396,6 +396,75 @@ static int conv_bwd_t(const float* g, int n_out, const Rows& L, int nL, const Ro
 
 #define SG_CONV_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
 
+// ------------------------------- long Toeplitz (both operands long) ------------------
+// f = sum over two long symbol lists (sweep |S| = 100, 1000): every output is a full 1-D
+// convolution per sample, O(|S|) multiply-adds per output, so this is FMA-bound, not
+// HBM-bound.  y[t] = sum_{u < nh} X[t + t0 - u] H[u], X rows outside [0, nx) are 0;
+// forward (X = long, H = other, t0 = 0) and both gradients (X = g, H = the other input
+// reversed through a negative row stride, t0 = nh - 1) are this one kernel.  Lane =
+// sample; a warp owns R consecutive outputs of 32 samples and walks only the taps that
+// touch X, U at a time: U filter taps and the R + U - 1 row X window sit in registers, so
+// each chunk is R*U FFMA per R + 2U - 1 coalesced 128-byte row loads.  A CTA is 4 warps =
+// 4 consecutive output tiles of the same 32 samples, so H and the overlapping X windows
+// are L1 hits across the CTA.
+constexpr int kLcR = 16, kLcU = 16, kLcWarps = 4;
+
+__global__ void __launch_bounds__(kLcWarps * 32) k_lconv(const Rows X, int nx, const Rows H, int nh, int t0,
+                                                         WRows Y, int ny, int64_t B, int tblocks, int clamp) {
+  constexpr int R = kLcR, U = kLcU;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t grp = blockIdx.x / tblocks;
+  const int tile = (blockIdx.x % tblocks) * kLcWarps + warp;
+  const int64_t b0 = grp * kWarp + lane;
+  const int64_t b = b0 < B ? b0 : B - 1;
+  pdl_wait();
+  const int t = tile * R;
+  if (t >= ny) return;
+  float acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = 0.f;
+  // taps u that reach X for some output t' in [t, t + R): x = t' + t0 - u in [0, nx)
+  const int u_lo = max(0, t + t0 - nx + 1);
+  const int u_hi = min(nh, t + t0 + R);
+  for (int u0 = u_lo; u0 < u_hi; u0 += U) {
+    float h[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) h[k] = u0 + k < u_hi ? H.ld(u0 + k, b) : 0.f;
+    const int base = t + t0 - u0 - (U - 1);  // X row of w[0]
+    float w[R + U - 1];
+    if (base >= 0 && base + R + U - 2 < nx) {
+#pragma unroll
+      for (int k = 0; k < R + U - 1; ++k) w[k] = X.ld(base + k, b);
+    } else {
+#pragma unroll
+      for (int k = 0; k < R + U - 1; ++k) {
+        const int x = base + k;
+        w[k] = (x >= 0 && x < nx) ? X.ld(x, b) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = fmaf(w[r + U - 1 - k], h[k], acc[r]);
+  }
+  if (b0 >= B) return;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (t + r < ny) Y.st(t + r, b0, clamp ? clamp01(acc[r]) : acc[r]);
+}
+
+static int lconv(const Rows& X, int nx, const Rows& H, int nh, int t0, const WRows& Y, int ny, int64_t B, int clamp,
+                 cudaStream_t st) {
+  const int tiles = ceil_div(ny, kLcR);
+  const int tblocks = ceil_div(tiles, kLcWarps);
+  const int64_t blocks = (int64_t)ceil_div(B, kWarp) * tblocks;
+  SG_RETURN_IF(blocks > 0x7fffffff, cudaErrorInvalidValue);
+  return (int)launch(k_lconv, dim3((unsigned)blocks), dim3(kLcWarps * kWarp), 0, st, X, nx, H, nh, t0, Y, ny, B,
+                     tblocks, clamp);
+}
+
+static Rows reversed(const Rows& r, int n) { return Rows{r.p + (int64_t)(n - 1) * r.sr, -r.sr, r.sb}; }
+
 static int conv_fwd(int kf, const Rows& L, int nL, const Rows& S, float* out, int n_out, int64_t B, cudaStream_t st) {
   switch (kf) {
 #define X(K) \
@@ -698,6 +767,10 @@ int sg_damp_apply_fwd(const sg_damp_plan* plan, const sg_rows* inputs, int64_t B
   cudaStream_t st = (cudaStream_t)stream;
   SG_RETURN_IF(plan->arity < 1 || plan->arity > SG_MAX_ARITY, cudaErrorInvalidValue);
   if (B <= 0 || plan->n_out <= 0) return 0;
+  if (plan->conv == 2) {  // long Toeplitz: out[o] = sum_j in0[o - j] in1[j]
+    return lconv(rows_of(inputs[0]), plan->sizes[0], rows_of(inputs[1]), plan->sizes[1], 0,
+                 WRows{out, B, 1}, plan->n_out, B, 1, st);
+  }
   if (plan->conv) {
     const int sh = plan->conv_short, lo = 1 - sh;
     return conv_fwd(plan->sizes[sh], rows_of(inputs[lo]), plan->sizes[lo], rows_of(inputs[sh]), out, plan->n_out, B,
@@ -713,6 +786,17 @@ int sg_damp_apply_bwd(const sg_damp_plan* plan, const sg_rows* inputs, const flo
   const int n = plan->arity;
   SG_RETURN_IF(n < 1 || n > SG_MAX_ARITY, cudaErrorInvalidValue);
   if (B <= 0) return 0;
+  if (plan->conv == 2) {  // d in_k[s] = sum_j g[s + j] in_other[j]: correlation = conv with the other reversed
+    const Rows g{grad_out, B, 1};
+    for (int k = 0; k < 2; ++k) {
+      if (grad_in[k].ptr == nullptr) continue;
+      const int o = 1 - k;
+      int rc = lconv(g, plan->n_out, reversed(rows_of(inputs[o]), plan->sizes[o]), plan->sizes[o],
+                     plan->sizes[o] - 1, wrows_of(grad_in[k]), plan->sizes[k], B, 0, st);
+      if (rc) return rc;
+    }
+    return 0;
+  }
   if (plan->conv) {
     const int sh = plan->conv_short, lo = 1 - sh;
     SG_RETURN_IF(grad_in[0].ptr == nullptr || grad_in[1].ptr == nullptr, cudaErrorInvalidValue);

@@ -129,7 +129,7 @@ class DampApply(torch.autograd.Function):
         grads = [None] * len(inputs)
         if need:
             dplan = kplan.device(dev)
-            alloc = range(2) if kplan.conv else need  # the fused Toeplitz backward writes both
+            alloc = range(2) if kplan.conv == 1 else need  # the short-filter Toeplitz backward writes both
             for i in alloc:
                 grads[i] = torch.empty_like(inputs[i])
             s = dplan.damp_struct(B, need_bwd=() if kplan.conv else need)

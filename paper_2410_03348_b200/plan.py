@@ -411,18 +411,20 @@ class KernelPlan:
         self._dtkp_host = None
         self._dev = {}
 
-    # T[s0][s1] == s0 + s1 for every combination, no drops: a 1-D convolution per sample
+    # T[s0][s1] == s0 + s1 for every combination, no drops: a 1-D convolution per sample.
+    # conv = 1: the short operand (<= 16 symbols) in registers (k_conv_*, fused chains);
+    # conv = 2: both operands long (k_lconv, an FMA-bound direct convolution).
     def _detect_toeplitz(self):
         if self.arity != 2 or not self.clamp:
-            return False, 0
+            return 0, 0
         s0, s1 = self.sizes
         if len(self.out_idx) != s0 * s1 or self.n_out != s0 + s1 - 1:
-            return False, 0
-        if min(s0, s1) > 16:
-            return False, 0
+            return 0, 0
         if not np.array_equal(self.out_idx, self.records[:, 0] + self.records[:, 1]):
-            return False, 0
-        return True, (1 if s1 <= s0 else 0)
+            return 0, 0
+        if min(s0, s1) > 16:
+            return 2, 0
+        return 1, (1 if s1 <= s0 else 0)
 
     @property
     def n_rec(self):
@@ -507,7 +509,7 @@ class DevicePlan:
         s.n_out = kp.n_out
         for i, n in enumerate(kp.sizes):
             s.sizes[i] = n
-        s.conv = 1 if kp.conv else 0
+        s.conv = int(kp.conv)
         s.conv_short = kp.conv_short
         if not kp.conv:
             s.fwd = self.fwd().struct(B)

@@ -293,7 +293,7 @@ class Damp:
         Toeplitz applies whose long operand is the previous apply's output are deferred
         into a fused chain (``_ConvChain``) and run as one launch each way."""
         kp = plan.kernel_plan()
-        if self.fuse_chains and kp.conv and len(tags_list) == 2:
+        if self.fuse_chains and kp.conv == 1 and len(tags_list) == 2:
             long_t, short_t = tags_list[1 - kp.conv_short], tags_list[kp.conv_short]
             kf = kp.sizes[kp.conv_short]
             if short_t.batch in (1, batch) and long_t.batch in (1, batch) and kp.n_out <= _ConvChain.max_rows(kf):

@@ -320,6 +320,33 @@ def test_generic_apply_vs_oracle(cuda, arity, size, B, fn):
         assert_close_rel(lf.grad.cpu().numpy(), gr, 1e-5, 1e-6, what="grad")
 
 
+@pytest.mark.parametrize("na,nb,B", [(1000, 1000, 64), (17, 300, 33), (300, 17, 65), (40, 64, 1), (100, 100, 257)])
+def test_long_toeplitz_vs_oracle(cuda, na, nb, B):
+    """f = sum over two long lists (both > 16 symbols): the k_lconv direct-convolution path
+    (forward and both correlation backwards), against the oracle."""
+    S = sg()
+    from oracle import algebra as A
+
+    f = lambda x, y: x + y  # noqa: E731
+    rng = np.random.default_rng(na * 7 + nb)
+    xs = [G.rows(rng, B, na), G.rows(rng, B, nb)]
+    ctx = S.ProgramContext(S.Damp())
+    leaves = [torch.tensor(x, device=cuda, dtype=torch.float32, requires_grad=True) for x in xs]
+    out = S.apply(f, S.make_distribution(ctx, leaves[0], range(na)), S.make_distribution(ctx, leaves[1], range(nb)))
+    from paper_2410_03348_b200.plan import build_plan
+
+    assert build_plan(f, None, [tuple(range(na)), tuple(range(nb))]).kernel_plan().conv == 2
+    syms, combos, idx = A.map_shuffle(f, None, [list(range(na)), list(range(nb))], S.UNDEFINED)
+    assert out.symbols == syms
+    ref = A.damp_apply(xs, combos, idx, len(syms))
+    got = S.get_probs(out)
+    assert_close_rel(got.detach().cpu().numpy(), ref, 1e-5, 1e-7, what="probs")
+    w = rng.uniform(-1, 1, size=ref.shape)
+    torch.autograd.backward(got, torch.as_tensor(w, device=cuda, dtype=torch.float32))
+    for lf, gr in zip(leaves, A.damp_apply_grad(xs, combos, idx, w.astype(np.float32).astype(np.float64))):
+        assert_close_rel(lf.grad.cpu().numpy(), gr, 1e-5, 1e-6, what="grad")
+
+
 # ------------------------------------------------------------------ full-size properties
 def test_sum15_full_batch_properties(cuda):
     """BASELINE config 2 at B=16384: mass conservation on every sample, and per-sample
