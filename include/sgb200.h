@@ -69,8 +69,13 @@ typedef struct sg_damp_plan {
   int32_t arity;
   int32_t n_out;
   int32_t sizes[SG_MAX_ARITY];
-  int32_t conv;        /* 1 when arity == 2 and T[s0][s1] == s0 + s1 (Toeplitz table)  */
-  int32_t conv_short;  /* which input (0/1) is the short "filter" side                  */
+  int32_t conv;        /* Toeplitz tables (f = sum of the input positions, no drops):
+                        * 1: arity 2, one side <= 16 symbols (register-filter kernels);
+                        * 2: arity 2, both sides long (direct per-sample convolution);
+                        * 3: arity 3, run as (in0 (*) in1) (*) in2 — needs scratch of
+                        *    (sizes[0] + sizes[1] - 1) x B floats forward, twice that backward;
+                        * 0: anything else (segmented sum-of-products plans below)       */
+  int32_t conv_short;  /* conv == 1: which input (0/1) is the short "filter" side        */
   sg_segsum fwd;              /* segments = output symbols, records = input positions   */
   sg_segsum bwd[SG_MAX_ARITY];/* segments = positions of input k, records = (T[c], s_j!=k) */
 } sg_damp_plan;

@@ -407,11 +407,13 @@ static int conv_bwd_t(const float* g, int n_out, const Rows& L, int nL, const Ro
 // each chunk is R*U FFMA per R + 2U - 1 coalesced 128-byte row loads.  A CTA is 4 warps =
 // 4 consecutive output tiles of the same 32 samples, so H and the overlapping X windows
 // are L1 hits across the CTA.
-constexpr int kLcR = 16, kLcU = 16, kLcWarps = 4;
+// R = 64 outputs per warp once the taps are long (more FMAs per window load), else 32.
+constexpr int kLcU = 16, kLcWarps = 4;
 
+template <int R>
 __global__ void __launch_bounds__(kLcWarps * 32) k_lconv(const Rows X, int nx, const Rows H, int nh, int t0,
                                                          WRows Y, int ny, int64_t B, int tblocks, int clamp) {
-  constexpr int R = kLcR, U = kLcU;
+  constexpr int U = kLcU;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t grp = blockIdx.x / tblocks;
   const int tile = (blockIdx.x % tblocks) * kLcWarps + warp;
@@ -453,14 +455,21 @@ __global__ void __launch_bounds__(kLcWarps * 32) k_lconv(const Rows X, int nx, c
     if (t + r < ny) Y.st(t + r, b0, clamp ? clamp01(acc[r]) : acc[r]);
 }
 
-static int lconv(const Rows& X, int nx, const Rows& H, int nh, int t0, const WRows& Y, int ny, int64_t B, int clamp,
-                 cudaStream_t st) {
-  const int tiles = ceil_div(ny, kLcR);
+template <int R>
+static int lconv_t(const Rows& X, int nx, const Rows& H, int nh, int t0, const WRows& Y, int ny, int64_t B, int clamp,
+                   cudaStream_t st) {
+  const int tiles = ceil_div(ny, R);
   const int tblocks = ceil_div(tiles, kLcWarps);
   const int64_t blocks = (int64_t)ceil_div(B, kWarp) * tblocks;
   SG_RETURN_IF(blocks > 0x7fffffff, cudaErrorInvalidValue);
-  return (int)launch(k_lconv, dim3((unsigned)blocks), dim3(kLcWarps * kWarp), 0, st, X, nx, H, nh, t0, Y, ny, B,
+  return (int)launch(k_lconv<R>, dim3((unsigned)blocks), dim3(kLcWarps * kWarp), 0, st, X, nx, H, nh, t0, Y, ny, B,
                      tblocks, clamp);
+}
+
+static int lconv(const Rows& X, int nx, const Rows& H, int nh, int t0, const WRows& Y, int ny, int64_t B, int clamp,
+                 cudaStream_t st) {
+  return nh >= 256 ? lconv_t<64>(X, nx, H, nh, t0, Y, ny, B, clamp, st)
+                   : lconv_t<32>(X, nx, H, nh, t0, Y, ny, B, clamp, st);
 }
 
 static Rows reversed(const Rows& r, int n) { return Rows{r.p + (int64_t)(n - 1) * r.sr, -r.sr, r.sb}; }
@@ -767,6 +776,15 @@ int sg_damp_apply_fwd(const sg_damp_plan* plan, const sg_rows* inputs, int64_t B
   cudaStream_t st = (cudaStream_t)stream;
   SG_RETURN_IF(plan->arity < 1 || plan->arity > SG_MAX_ARITY, cudaErrorInvalidValue);
   if (B <= 0 || plan->n_out <= 0) return 0;
+  if (plan->conv == 3) {  // f = a + b + c: (a (*) b) (*) c, unclamped in between; scratch = a (*) b
+    SG_RETURN_IF(scratch == nullptr, cudaErrorInvalidValue);
+    const int n01 = plan->sizes[0] + plan->sizes[1] - 1;
+    int rc = lconv(rows_of(inputs[0]), plan->sizes[0], rows_of(inputs[1]), plan->sizes[1], 0,
+                   WRows{scratch, B, 1}, n01, B, 0, st);
+    if (rc) return rc;
+    return lconv(Rows{scratch, B, 1}, n01, rows_of(inputs[2]), plan->sizes[2], 0, WRows{out, B, 1}, plan->n_out, B, 1,
+                 st);
+  }
   if (plan->conv == 2) {  // long Toeplitz: out[o] = sum_j in0[o - j] in1[j]
     return lconv(rows_of(inputs[0]), plan->sizes[0], rows_of(inputs[1]), plan->sizes[1], 0,
                  WRows{out, B, 1}, plan->n_out, B, 1, st);
@@ -786,6 +804,31 @@ int sg_damp_apply_bwd(const sg_damp_plan* plan, const sg_rows* inputs, const flo
   const int n = plan->arity;
   SG_RETURN_IF(n < 1 || n > SG_MAX_ARITY, cudaErrorInvalidValue);
   if (B <= 0) return 0;
+  if (plan->conv == 3) {  // scratch = [t = a (*) b | dt = g corr c]; dc = g corr t, da = dt corr b, db = dt corr a
+    SG_RETURN_IF(scratch == nullptr, cudaErrorInvalidValue);
+    const int n0 = plan->sizes[0], n1 = plan->sizes[1], n2 = plan->sizes[2], n01 = n0 + n1 - 1;
+    float* t = scratch;
+    float* dt = scratch + (size_t)n01 * B;
+    const Rows g{grad_out, B, 1};
+    int rc = 0;
+    if (grad_in[2].ptr != nullptr) {
+      rc = lconv(rows_of(inputs[0]), n0, rows_of(inputs[1]), n1, 0, WRows{t, B, 1}, n01, B, 0, st);
+      if (rc) return rc;
+      rc = lconv(g, plan->n_out, reversed(Rows{t, B, 1}, n01), n01, n01 - 1, wrows_of(grad_in[2]), n2, B, 0, st);
+      if (rc) return rc;
+    }
+    if (grad_in[0].ptr == nullptr && grad_in[1].ptr == nullptr) return 0;
+    rc = lconv(g, plan->n_out, reversed(rows_of(inputs[2]), n2), n2, n2 - 1, WRows{dt, B, 1}, n01, B, 0, st);
+    if (rc) return rc;
+    const Rows dtr{dt, B, 1};
+    if (grad_in[0].ptr != nullptr) {
+      rc = lconv(dtr, n01, reversed(rows_of(inputs[1]), n1), n1, n1 - 1, wrows_of(grad_in[0]), n0, B, 0, st);
+      if (rc) return rc;
+    }
+    if (grad_in[1].ptr != nullptr)
+      rc = lconv(dtr, n01, reversed(rows_of(inputs[0]), n0), n0, n0 - 1, wrows_of(grad_in[1]), n1, B, 0, st);
+    return rc;
+  }
   if (plan->conv == 2) {  // d in_k[s] = sum_j g[s + j] in_other[j]: correlation = conv with the other reversed
     const Rows g{grad_out, B, 1};
     for (int k = 0; k < 2; ++k) {

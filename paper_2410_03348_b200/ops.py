@@ -103,7 +103,9 @@ class DampApply(torch.autograd.Function):
         if kplan.clamp:
             s = dplan.damp_struct(B)
             scratch = None
-            if not kplan.conv and s.fwd.n_partial:
+            if kplan.conv == 3:  # the unclamped a (*) b of a three-way sum
+                scratch = torch.empty((kplan.sizes[0] + kplan.sizes[1] - 1, B), device=dev, dtype=F32)
+            elif not kplan.conv and s.fwd.n_partial:
                 scratch = torch.empty((s.fwd.n_partial, B), device=dev, dtype=F32)
             rc = _lib().sg_damp_apply_fwd(ctypes.byref(s), ops_, B, out.data_ptr(), N.ptr(scratch), st)
             N.check(rc, "sg_damp_apply_fwd")
@@ -134,6 +136,8 @@ class DampApply(torch.autograd.Function):
                 grads[i] = torch.empty_like(inputs[i])
             s = dplan.damp_struct(B, need_bwd=() if kplan.conv else need)
             n_partial = 0 if kplan.conv else max((s.bwd[i].n_partial for i in need), default=0)
+            if kplan.conv == 3:
+                n_partial = 2 * (kplan.sizes[0] + kplan.sizes[1] - 1)
             scratch = torch.empty((n_partial, B), device=dev, dtype=F32) if n_partial else None
             rc = _lib().sg_damp_apply_bwd(ctypes.byref(s), N.rows_array(inputs), g.data_ptr(), B,
                                           N.rows_array(grads), N.ptr(scratch), N.stream_ptr(dev))

@@ -414,7 +414,14 @@ class KernelPlan:
     # T[s0][s1] == s0 + s1 for every combination, no drops: a 1-D convolution per sample.
     # conv = 1: the short operand (<= 16 symbols) in registers (k_conv_*, fused chains);
     # conv = 2: both operands long (k_lconv, an FMA-bound direct convolution).
+    # conv = 3: f = a + b + c over three lists, run as (a (*) b) (*) c (no clamp in between).
     def _detect_toeplitz(self):
+        if self.arity == 3 and self.clamp:
+            s0, s1, s2 = self.sizes
+            if (len(self.out_idx) == s0 * s1 * s2 and self.n_out == s0 + s1 + s2 - 2
+                    and np.array_equal(self.out_idx, self.records.sum(axis=1))):
+                return 3, 0
+            return 0, 0
         if self.arity != 2 or not self.clamp:
             return 0, 0
         s0, s1 = self.sizes

@@ -295,7 +295,7 @@ def test_batch_one_broadcast_and_reuse(cuda):
 @pytest.mark.parametrize("arity,size,B,fn", [
     (2, 1000, 128, "prod"),   # |S|=1000: operands exceed the shared tile (global path), long segments split
     (2, 100, 512, "mod"),
-    (3, 30, 256, "sum"),      # arity 3 (no Toeplitz path), segments of up to ~700 combos
+    (3, 30, 256, "lin3"),     # arity 3, not a plain sum: generic segments of up to ~900 combos
     (1, 5000, 96, "mod3"),    # one input, 3 outputs: segments split across items + fix-up
 ])
 def test_generic_apply_vs_oracle(cuda, arity, size, B, fn):
@@ -303,7 +303,7 @@ def test_generic_apply_vs_oracle(cuda, arity, size, B, fn):
     from oracle import algebra as A
 
     f = {"prod": lambda x, y: x * y, "mod": lambda x, y: (x * 7 + y) % 13, "sum": lambda *xs: sum(xs),
-         "mod3": lambda x: x % 3}[fn]
+         "lin3": lambda x, y, z: x + 2 * y + z, "mod3": lambda x: x % 3}[fn]
     rng = np.random.default_rng(size + arity)
     xs = [G.rows(rng, B, size) for _ in range(arity)]
     ctx = S.ProgramContext(S.Damp())
@@ -317,6 +317,33 @@ def test_generic_apply_vs_oracle(cuda, arity, size, B, fn):
     w = rng.uniform(-1, 1, size=ref.shape)
     (got.double() * torch.as_tensor(w, device=cuda)).sum().backward()
     for lf, gr in zip(leaves, A.damp_apply_grad(xs, combos, idx, w)):
+        assert_close_rel(lf.grad.cpu().numpy(), gr, 1e-5, 1e-6, what="grad")
+
+
+@pytest.mark.parametrize("sizes,B", [((12, 5, 30), 70), ((100, 100, 100), 33), ((3, 1, 2), 5), ((40, 40, 40), 1)])
+def test_three_way_sum_vs_oracle(cuda, sizes, B):
+    """f = a + b + c: the plan runs it as two chained convolutions (conv == 3); forward and
+    the four-convolution backward against the oracle's 3-way enumeration."""
+    S = sg()
+    from oracle import algebra as A
+    from paper_2410_03348_b200.plan import build_plan
+
+    f = lambda x, y, z: x + y + z  # noqa: E731
+    lists = [list(range(n)) for n in sizes]
+    assert build_plan(f, None, [tuple(x) for x in lists]).kernel_plan().conv == 3
+    rng = np.random.default_rng(sum(sizes))
+    xs = [G.rows(rng, B, n) for n in sizes]
+    ctx = S.ProgramContext(S.Damp())
+    leaves = [torch.tensor(x, device=cuda, dtype=torch.float32, requires_grad=True) for x in xs]
+    out = S.apply(f, *[S.make_distribution(ctx, lf, lst) for lf, lst in zip(leaves, lists)])
+    syms, combos, idx = A.map_shuffle(f, None, lists, S.UNDEFINED)
+    assert out.symbols == syms
+    ref = A.damp_apply(xs, combos, idx, len(syms))
+    got = S.get_probs(out)
+    assert_close_rel(got.detach().cpu().numpy(), ref, 1e-5, 1e-7, what="probs")
+    w = rng.uniform(-1, 1, size=ref.shape).astype(np.float32)
+    torch.autograd.backward(got, torch.as_tensor(w, device=cuda))
+    for lf, gr in zip(leaves, A.damp_apply_grad(xs, combos, idx, w.astype(np.float64))):
         assert_close_rel(lf.grad.cpu().numpy(), gr, 1e-5, 1e-6, what="grad")
 
 
