@@ -88,7 +88,35 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if proc.returncode != 0:
             raise RuntimeError(f"link failed:\n{proc.stdout}\n{proc.stderr}")
         os.replace(tmp, LIB)
+    build_planner(force)
     return LIB
+
+
+PLANNER_SRC = CSRC / "planner.cpp"
+
+
+def planner_path() -> Path:
+    import sysconfig
+
+    return PKG / f"_planner{sysconfig.get_config_var('EXT_SUFFIX')}"
+
+
+def build_planner(force: bool = False) -> Path:
+    """The native host planner (CPython extension, g++ -O2): apply_if's map/shuffle loop."""
+    import sysconfig
+
+    out = planner_path()
+    if not force and not _stale(out, [PLANNER_SRC]):
+        return out
+    cxx = os.environ.get("CXX") or shutil.which("g++") or "g++"
+    tmp = out.with_name(out.name + ".tmp")
+    cmd = [cxx, "-O2", "-std=c++17", "-shared", "-fPIC", "-fno-strict-aliasing", "-Wall",
+           f"-I{sysconfig.get_paths()['include']}", str(PLANNER_SRC), "-o", str(tmp)]
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        raise RuntimeError(f"planner build failed:\n{proc.stdout}\n{proc.stderr}")
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

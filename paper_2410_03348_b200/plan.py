@@ -241,7 +241,36 @@ def build_plan(f, cond, symbol_lists) -> SymbolPlan:
     return plan
 
 
+def _planner():
+    """The native map/shuffle loop (csrc/planner.cpp, built by _build.build())."""
+    global _PLANNER
+    if _PLANNER is None:
+        try:
+            from . import _planner as mod
+        except ImportError as exc:  # the product path has no interpreted fallback
+            raise N.NativeError("native host planner _planner missing: run paper_2410_03348_b200._build") from exc
+        _PLANNER = mod
+    return _PLANNER
+
+
+_PLANNER = None
+
+
 def _map_shuffle(f, cond, symbol_lists) -> SymbolPlan:
+    sizes = [len(s) for s in symbol_lists]
+    n_enum = int(np.prod(sizes, dtype=np.int64)) if sizes else 0
+    res = _planner().map_shuffle(f, cond, symbol_lists, UNDEFINED)
+    if len(res) == 3 and res[0] == "error":
+        _, syms, exc = res
+        raise SymbolFunctionError(f"symbol function failed on {syms!r}: {exc}", syms) from exc
+    out_symbols, kept_b, idx_b, calls = res
+    _stats["f_calls"] += calls
+    return _make_symbol_plan(out_symbols, sizes, np.frombuffer(kept_b, dtype=np.int64),
+                             np.frombuffer(idx_b, dtype=np.int32).copy(), n_enum)
+
+
+def _map_shuffle_py(f, cond, symbol_lists) -> SymbolPlan:
+    """Interpreted restatement of the same loop (test reference for the native planner)."""
     sizes = [len(s) for s in symbol_lists]
     n_enum = int(np.prod(sizes, dtype=np.int64)) if sizes else 0
     kept = []
@@ -264,13 +293,19 @@ def _map_shuffle(f, cond, symbol_lists) -> SymbolPlan:
         kept.append(ordinal)
         out_idx.append(idx)
     _stats["f_calls"] += calls
-    out_symbols = tuple(buckets.keys())
+    return _make_symbol_plan(tuple(buckets.keys()), sizes, np.asarray(kept, dtype=np.int64),
+                             np.asarray(out_idx, dtype=np.int32), n_enum)
+
+
+def _make_symbol_plan(out_symbols, sizes, kept, out_idx, n_enum) -> SymbolPlan:
     _INTERN.adopt(out_symbols)
-    if kept:
-        combos = np.stack(np.unravel_index(np.asarray(kept, dtype=np.int64), sizes), axis=1).astype(np.int32)
+    if len(kept) and sizes:
+        combos = np.stack(np.unravel_index(kept, sizes), axis=1).astype(np.int32)
+    elif len(kept):
+        combos = np.zeros((len(kept), 0), dtype=np.int32)
     else:
         combos = np.zeros((0, len(sizes)), dtype=np.int32)
-    return SymbolPlan(out_symbols, sizes, combos, np.asarray(out_idx, dtype=np.int32), n_enum)
+    return SymbolPlan(out_symbols, sizes, combos, out_idx, n_enum)
 
 
 # ----------------------------------------------------------------------------- device plans

@@ -142,3 +142,51 @@ def test_segsum_items_cover_every_record_once(max_item):
     for nb in (1, 2, 7, 64):
         blk = h.blocks(nb)
         assert blk[0] == 0 and blk[-1] == len(h.items) and (np.diff(blk) >= 0).all()
+
+
+# ------------------------------------------------------------------ native host planner
+def _plans_equal(a, b):
+    assert a.out_symbols == b.out_symbols
+    assert [type(s) for s in a.out_symbols] == [type(s) for s in b.out_symbols]
+    np.testing.assert_array_equal(a.combos, b.combos)
+    np.testing.assert_array_equal(a.out_idx, b.out_idx)
+    assert a.n_enumerated == b.n_enumerated
+
+
+@pytest.mark.parametrize("case", range(7))
+def test_native_planner_equals_interpreted_loop(case):
+    """csrc/planner.cpp (the product path) against the interpreted restatement of
+    distribution.py:244-260: same symbols (and their types), combos, output order."""
+    P = plan_mod()
+    f, cond, lists = [
+        (lambda x, y: x + y, None, [tuple(range(10))] * 2),
+        (lambda x, y: P.UNDEFINED if (x * y) % 5 == 3 else (x - y) % 4, lambda x, y: x != y,
+         [tuple(range(9)), tuple(range(7))]),
+        (lambda x, y, z: (x, y % 2, z > 1), None, [tuple("abc"), tuple(range(4)), tuple(range(3))]),
+        # 1 == 1.0 == True collide in the bucket dict: the first derivation's object wins
+        (lambda x: [1, 1.0, True, 2, 2.0][x], None, [tuple(range(5))]),
+        (lambda x, y: x, None, [(), (1, 2)]),            # an empty input list: nothing enumerated
+        (lambda: 7, None, []),                            # arity 0: one empty combination
+        (lambda x, y: P.UNDEFINED, lambda x, y: x < y, [tuple(range(4))] * 2),  # everything dropped
+    ][case]
+    canon = [P.canonical_symbols(tuple(s)) for s in lists]
+    _plans_equal(P._map_shuffle(f, cond, canon), P._map_shuffle_py(f, cond, canon))
+
+
+def test_native_planner_errors():
+    P = plan_mod()
+
+    def bad(x, y):
+        if (x, y) == (2, 1):
+            raise ZeroDivisionError("boom")
+        return x
+
+    with pytest.raises(P.SymbolFunctionError) as ei:
+        P._map_shuffle(bad, None, [tuple(range(3)), tuple(range(3))])
+    assert ei.value.symbols == (2, 1)
+    assert isinstance(ei.value.__cause__, ZeroDivisionError)
+    with pytest.raises(P.SymbolFunctionError) as ei:  # cond errors are wrapped the same way
+        P._map_shuffle(lambda x: x, lambda x: 1 / (x - 1), [tuple(range(3))])
+    assert ei.value.symbols == (1,)
+    with pytest.raises(TypeError):  # an unhashable result fails in the bucket dict, unwrapped
+        P._map_shuffle(lambda x: [x], None, [tuple(range(2))])
