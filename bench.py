@@ -308,10 +308,10 @@ def run_gpu_arm(args):
     torch.cuda.current_stream(device).wait_stream(side)
     torch.cuda.synchronize(device)
     graph = torch.cuda.CUDAGraph()
-    calls0 = N.CALLS["n"]
+    calls0 = N.launch_count()
     with torch.cuda.graph(graph):
         s_loss, s_gx = step(x, targets)
-    launches = N.CALLS["n"] - calls0
+    launches = N.launch_count() - calls0  # our kernels in one captured step
     for _ in range(args.warmup):
         graph.replay()
     torch.cuda.synchronize(device)

@@ -81,6 +81,8 @@ typedef struct sg_damp_plan {
 } sg_damp_plan;
 
 int sg_version(void);
+/* Kernels this library has enqueued so far (all entry points; graph capture counts once). */
+int64_t sg_launch_count(void);
 int sg_device_sm_count(int device);
 
 /* ---- layout: user (B, n) block  <->  symbol-major [n][B] fp32 ----------------------

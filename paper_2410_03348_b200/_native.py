@@ -103,6 +103,7 @@ class SgDtkpApplyDesc(Structure):
 # (name, restype, argtypes) of every exported entry point in include/sgb200.h
 EXPORTS = {
     "sg_version": (c_int32, []),
+    "sg_launch_count": (c_int64, []),
     "sg_device_sm_count": (c_int32, [c_int32]),
     "sg_to_symbol_major": (c_int32, [c_void_p, c_int32, c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p]),
     "sg_from_symbol_major": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_int32, c_int64, c_int64, c_void_p]),
@@ -145,27 +146,17 @@ EXPORTS = {
 }
 
 _lib = None
-CALLS = {"n": 0}  # ABI calls issued (each launches one or two of our kernels)
-
-
-class _Counted:
-    """Thin wrapper counting ABI calls (bench.py reports launches per step)."""
-
-    __slots__ = ("fn",)
-
-    def __init__(self, fn):
-        self.fn = fn
-
-    def __call__(self, *args):
-        CALLS["n"] += 1
-        return self.fn(*args)
-
-
 class _Lib:
     def __init__(self, cdll):
         self._cdll = cdll
         for name in EXPORTS:
-            setattr(self, name, _Counted(getattr(cdll, name)))
+            setattr(self, name, getattr(cdll, name))
+
+
+def launch_count() -> int:
+    """Kernels the library has enqueued so far (sg_launch_count; a captured graph's
+    kernels count once, at capture)."""
+    return int(load().sg_launch_count())
 
 
 def load() -> "_Lib":

@@ -482,6 +482,7 @@ static cudaError_t launch_chain(void (*kernel)(KArgs...), const ChainArgs& a, si
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  count_launch();
   return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 

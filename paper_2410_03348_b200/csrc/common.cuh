@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -53,6 +54,11 @@ __device__ __forceinline__ Rec<RW> load_rec(const int32_t* __restrict__ p) {
   }
   return r;
 }
+
+// Kernels enqueued by this library (every launch site calls count_launch once per
+// kernel), exported as sg_launch_count() so callers can report what ran natively.
+inline std::atomic<long long> g_launches{0};
+inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 

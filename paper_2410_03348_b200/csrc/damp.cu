@@ -70,6 +70,7 @@ static cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  count_launch();
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
@@ -765,6 +766,8 @@ int sg_device_sm_count(int device) {
   if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
   return v;
 }
+
+int64_t sg_launch_count(void) { return (int64_t)g_launches.load(); }
 
 int sg_segsum_run(const sg_segsum* prob, const sg_rows* ops, const int32_t* op_rows, int32_t n_ops, int64_t B,
                   int32_t clamp01_, sg_rows out, float* scratch, sg_stream_t stream) {

@@ -211,16 +211,16 @@ static int dedup_k(const uint8_t* member, const uint8_t* present, const double* 
   const int W = (I + 63) / 64;
   int grid = ceil_div(M, 128);
   if (grid > 4096) grid = 4096;
+  if (W > 8) return (int)cudaErrorNotSupported;
+  count_launch();
   if (W <= 1)
     k_dedup_topk<K, 1><<<grid, 128, 0, st>>>(member, present, p, M, R, I, k, om, op);
   else if (W <= 2)
     k_dedup_topk<K, 2><<<grid, 128, 0, st>>>(member, present, p, M, R, I, k, om, op);
   else if (W <= 4)
     k_dedup_topk<K, 4><<<grid, 128, 0, st>>>(member, present, p, M, R, I, k, om, op);
-  else if (W <= 8)
-    k_dedup_topk<K, 8><<<grid, 128, 0, st>>>(member, present, p, M, R, I, k, om, op);
   else
-    return (int)cudaErrorNotSupported;
+    k_dedup_topk<K, 8><<<grid, 128, 0, st>>>(member, present, p, M, R, I, k, om, op);
   SG_LAUNCH_CHECK();
   return 0;
 }
@@ -291,6 +291,7 @@ int sg_dtkp_probs_fwd(const uint64_t* member, const uint8_t* present, int32_t N,
 #define SG_PF(WT)                                                                                        \
   do {                                                                                                   \
     ensure_smem((const void*)k_dtkp_probs_fwd<WT>, smem);                                                \
+    count_launch();                                                                                      \
     k_dtkp_probs_fwd<WT><<<grid, nw * 32, smem, st>>>(member, present, N, K, W, p, I, B, rows_per, out);  \
   } while (0)
   if (W <= 1) SG_PF(1);
@@ -329,6 +330,7 @@ int sg_dtkp_probs_bwd(const uint64_t* member, const uint8_t* present, int32_t N,
 #define SG_PB(WT)                                                                                                  \
   do {                                                                                                             \
     ensure_smem((const void*)k_dtkp_probs_bwd<WT>, smem);                                                          \
+    count_launch();                                                                                      \
     k_dtkp_probs_bwd<WT><<<grid, nw * 32, smem, st>>>(member, present, N, K, W, p, I, B, rows_per, grad_out, scr); \
   } while (0)
   if (W <= 1) SG_PB(1);
@@ -340,6 +342,7 @@ int sg_dtkp_probs_bwd(const uint64_t* member, const uint8_t* present, int32_t N,
   const int64_t n_elem = (int64_t)I * B;
   int g2 = ceil_div(n_elem, 256);
   if (g2 > 148 * 8) g2 = 148 * 8;
+  count_launch();
   k_reduce_slabs<<<g2, 256, 0, st>>>(scr, chunks, n_elem, grad_p);
   SG_LAUNCH_CHECK();
   return 0;

@@ -336,6 +336,7 @@ static int launch_apply_kw(const DtkpK& k, int n_blocks, cudaStream_t st) {
     cudaError_t e = ensure_smem((const void*)k_dtkp_apply<K, WT>, smem);
     if (e != cudaSuccess) return (int)e;
   }
+  count_launch();
   k_dtkp_apply<K, WT><<<grid, 128, smem, st>>>(k);
   SG_LAUNCH_CHECK();
   return 0;

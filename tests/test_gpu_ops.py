@@ -543,3 +543,31 @@ def test_graphed_step_pipelined_slots(cuda):
     for bt, loss in zip(batches, got):
         want = step(*[x.to(cuda).requires_grad_(x.dtype == torch.float32) for x in bt])[0]
         assert float(loss) == float(want)
+
+
+def test_sum15_step_launches_four_native_kernels(cuda):
+    """The whole Sum-15 step (15 distributions, 14 applies, get_probs, loss_nll, backward)
+    is four kernels of libsgb200 — fused chain fwd, loss fwd, loss bwd, fused chain bwd —
+    counted by the library itself (sg_launch_count), with no torch kernels in between."""
+    S = sg()
+    from paper_2410_03348_b200 import _native as N
+    from paper_2410_03348_b200 import programs as P
+    from paper_2410_03348_b200.learn import loss_nll
+
+    rng = np.random.default_rng(3)
+    B = 4096
+    xs = [torch.tensor(G.rows(rng, B, 10), device=cuda, requires_grad=True) for _ in range(15)]
+    t = torch.tensor(rng.integers(0, 136, size=B), device=cuda)
+    one = torch.ones((), device=cuda, dtype=torch.float64)
+
+    def step():
+        ctx = S.ProgramContext(S.Damp(), device=cuda)
+        loss = loss_nll(S.get_probs(P.sum_n(ctx, [S.make_distribution(ctx, x, range(10)) for x in xs])), t)
+        return torch.autograd.grad(loss, xs, grad_outputs=one)
+
+    step()  # plans built and uploaded
+    torch.cuda.synchronize()
+    n0 = N.launch_count()
+    step()
+    torch.cuda.synchronize()
+    assert N.launch_count() - n0 == 4
