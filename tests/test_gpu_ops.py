@@ -555,7 +555,7 @@ def test_sum15_step_launches_four_native_kernels(cuda):
     from paper_2410_03348_b200.learn import loss_nll
 
     rng = np.random.default_rng(3)
-    B = 4096
+    B = 16384  # BASELINE configs[1]; the batch alone fills the GPU, so the loss is one pass
     xs = [torch.tensor(G.rows(rng, B, 10), device=cuda, requires_grad=True) for _ in range(15)]
     t = torch.tensor(rng.integers(0, 136, size=B), device=cuda)
     one = torch.ones((), device=cuda, dtype=torch.float64)
