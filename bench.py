@@ -181,11 +181,12 @@ def build_step(torch, sg, device):
 
 def chain_bytes(B, n0=10, kf=10, m=N_DIGITS - 1):
     """Algorithmic HBM bytes of one fused Sum-N chain launch (K1c/K2c):
-    fwd reads v_0 and the m filters and writes the m-1 clamped states and v_m; bwd reads
+    fwd reads v_0 and the m filters and writes the m-1 clamped states, v_m and its fp64
+    per-sample row sums; bwd reads
     g_out, the filters, the states and v_0 and writes dS_1..m and dv_0."""
     states = sum(n0 + i * (kf - 1) for i in range(1, m))
     n_out = n0 + m * (kf - 1)
-    fwd = 4 * B * (n0 + m * kf + states + n_out)
+    fwd = 4 * B * (n0 + m * kf + states + n_out) + 8 * B  # + the fp64 row sums
     bwd = 4 * B * (n_out + m * kf + states + n0 + m * kf + n0)
     return fwd, bwd
 
@@ -213,6 +214,7 @@ def kernel_roofline(torch, device, B, hbm_gbs, reps=12):
         filt = [torch.rand((B, kf), device=device).t() for _ in range(m)]
         states = torch.empty((int(lib.sg_chain_states_elems(n0, kf, m, B)),), device=device)
         out = torch.empty((n_out, B), device=device)
+        rowsum = torch.empty((B,), device=device, dtype=torch.float64)
         g = torch.rand((n_out, B), device=device)
         gbase = torch.empty_like(base)
         gfilt = [torch.empty_like(f) for f in filt]
@@ -220,13 +222,13 @@ def kernel_roofline(torch, device, B, hbm_gbs, reps=12):
         garr = (N.SgRows * N.CHAIN_MAX_STEPS)()
         for i, t in enumerate(gfilt):
             garr[i] = N.rows(t)
-        sets.append((c, out, g, gbase, garr, (base, filt, states, gfilt)))
+        sets.append((c, out, g, gbase, garr, (base, filt, states, gfilt, rowsum)))
 
     def run(kind, j):
         st = torch.cuda.current_stream(device).cuda_stream
         c, out, g, gbase, garr, _ = sets[j % nsets]
         if kind == "fwd":
-            rc = lib.sg_chain_fwd(ctypes.byref(c), out.data_ptr(), st)
+            rc = lib.sg_chain_fwd(ctypes.byref(c), out.data_ptr(), sets[j % nsets][5][4].data_ptr(), st)
         else:
             rc = lib.sg_chain_bwd(ctypes.byref(c), g.data_ptr(), N.rows(gbase), garr, st)
         N.check(rc, kind)

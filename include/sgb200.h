@@ -139,7 +139,9 @@ typedef struct sg_chain {
 
 int64_t sg_chain_states_elems(int32_t n0, int32_t kf, int32_t m, int64_t B);
 int32_t sg_chain_max_rows(int32_t kf);
-int sg_chain_fwd(const sg_chain* chain, float* out, sg_stream_t stream);
+/* rowsum (optional, may be NULL): [B] fp64 sums of each sample's output row, the
+ * normaliser loss_nll needs (sg_nll_fwd_rowsum consumes it). */
+int sg_chain_fwd(const sg_chain* chain, float* out, double* rowsum, sg_stream_t stream);
 int sg_chain_bwd(const sg_chain* chain, const float* grad_out, sg_rows grad_base,
                  const sg_rows* grad_filters, sg_stream_t stream);
 
@@ -152,6 +154,10 @@ int sg_chain_bwd(const sg_chain* chain, const float* grad_out, sg_rows grad_base
 int64_t sg_nll_scratch_bytes(int64_t n, int64_t B);
 int sg_nll_fwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, double* loss,
                void* scratch, double* rowsum, sg_stream_t stream);
+/* The same loss when the per-sample row sums are already known (rowsum: [B] fp64, e.g.
+ * from sg_chain_fwd): one launch that only gathers p[t_b][b]. */
+int sg_nll_fwd_rowsum(sg_rows probs, int64_t n, int64_t B, const int64_t* targets,
+                      const double* rowsum, double* loss, void* scratch, sg_stream_t stream);
 /* grad[n][b] = -(g/B) / c_b * (delta(n, t_b) / (s_b + 1e-8) - p[t_b][b] / (s_b + 1e-8)^2) */
 int sg_nll_bwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets,
                const double* grad_loss, const double* rowsum, sg_rows grad, sg_stream_t stream);

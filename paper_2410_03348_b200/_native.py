@@ -122,11 +122,12 @@ EXPORTS = {
     ),
     "sg_chain_states_elems": (c_int64, [c_int32, c_int32, c_int32, c_int64]),
     "sg_chain_max_rows": (c_int32, [c_int32]),
-    "sg_chain_fwd": (c_int32, [POINTER(SgChain), c_void_p, c_void_p]),
+    "sg_chain_fwd": (c_int32, [POINTER(SgChain), c_void_p, c_void_p, c_void_p]),
     "sg_chain_bwd": (c_int32, [POINTER(SgChain), c_void_p, SgRows, POINTER(SgRows), c_void_p]),
     "sg_nll_scratch_bytes": (c_int64, [c_int64, c_int64]),
     "sg_nll_fwd": (c_int32, [SgRows, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "sg_nll_bwd": (c_int32, [SgRows, c_int64, c_int64, c_void_p, c_void_p, c_void_p, SgRows, c_void_p]),
+    "sg_nll_fwd_rowsum": (c_int32, [SgRows, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "sg_rows_gather": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "sg_dtkp_apply": (c_int32, [POINTER(SgDtkpApplyDesc), c_void_p]),
     "sg_dtkp_probs_fwd": (

@@ -59,6 +59,7 @@ struct ChainArgs {
   int64_t B;
   float* states;       // [ceil(B/16)][state_rows][16] clamped intermediate states
   float* out;          // [n[m]][B]
+  double* rowsum;      // forward, optional: [B] sum over the output rows (fp64)
   const float* g_out;  // backward: [n[m]][B]
   float* dbase_p;      // backward: grad of v_0 (strided like base)
   int64_t dbase_sr, dbase_sb;
@@ -206,7 +207,7 @@ __device__ __forceinline__ void fwd_window(float2 (&w)[R + KF - 1], const float2
 template <int KF, int R, bool VEC>
 __device__ __forceinline__ void fwd_round(const float2 (&w)[R + KF - 1], const float2 (&f)[KF], float2* v0,
                                           float2* gst, int o0, int nout, bool last, const ChainArgs& a,
-                                          const Lane& L) {
+                                          const Lane& L, double2& rsum) {
   float2 acc[R];
   conv_tile<KF, R>(acc, w, f);
   __syncwarp();  // every group's window (this round's and the next's) is loaded before any store
@@ -223,7 +224,12 @@ __device__ __forceinline__ void fwd_round(const float2 (&w)[R + KF - 1], const f
     float* q = a.out + (size_t)o0 * a.B;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      if (o0 + r < nout) st_rowmajor<VEC>(q, L, clamp01x2(acc[r]));
+      if (o0 + r < nout) {
+        const float2 v = clamp01x2(acc[r]);
+        st_rowmajor<VEC>(q, L, v);
+        rsum.x += (double)v.x;  // per-sample sum of the output row (the loss' normaliser)
+        rsum.y += (double)v.y;
+      }
       q += a.B;
     }
   }
@@ -264,6 +270,7 @@ __global__ void __launch_bounds__(32) k_chain_fwd(const ChainArgs a) {
   __syncwarp();
   float2* v0 = V + PAD * kCP + L.c;  // state row 0 of this lane's pair
   float2* sblk = reinterpret_cast<float2*>(a.states) + (size_t)L.wid * a.state_rows * (kCWS / 2) + L.c;
+  double2 rsum = make_double2(0.0, 0.0);
   for (int i = 1; i <= a.m; ++i) {
     if (!a.allf) {
       const int s = i + kRing - 1;
@@ -287,13 +294,24 @@ __global__ void __launch_bounds__(32) k_chain_fwd(const ChainArgs a) {
     fwd_window<KF, R>(wA, v0, (kr - 1) * kRound + L.g * R);
     for (int k = kr - 1; k >= 0; k -= 2) {
       if (k >= 1) fwd_window<KF, R>(wB, v0, (k - 1) * kRound + L.g * R);
-      fwd_round<KF, R, VEC>(wA, f, v0, gst, k * kRound + L.g * R, nout, last, a, L);
+      fwd_round<KF, R, VEC>(wA, f, v0, gst, k * kRound + L.g * R, nout, last, a, L, rsum);
       if (k < 1) break;
       if (k >= 2) fwd_window<KF, R>(wA, v0, (k - 2) * kRound + L.g * R);
-      fwd_round<KF, R, VEC>(wB, f, v0, gst, (k - 1) * kRound + L.g * R, nout, last, a, L);
+      fwd_round<KF, R, VEC>(wB, f, v0, gst, (k - 1) * kRound + L.g * R, nout, last, a, L, rsum);
     }
     if (!a.allf) cp_wait_ring();
     __syncwarp();
+  }
+  if (a.rowsum != nullptr) {  // the groups' partial row sums, combined in fixed order
+#pragma unroll
+    for (int o = kPairs; o < 32; o <<= 1) {
+      rsum.x += __shfl_xor_sync(0xffffffffu, rsum.x, o);
+      rsum.y += __shfl_xor_sync(0xffffffffu, rsum.y, o);
+    }
+    if (L.g == 0) {
+      if (L.nv > 0) a.rowsum[L.b0] = rsum.x;
+      if (L.nv > 1) a.rowsum[L.b0 + 1] = rsum.y;
+    }
   }
 }
 
@@ -536,12 +554,13 @@ int32_t sg_chain_max_rows(int32_t kf) {
   return n;
 }
 
-int sg_chain_fwd(const sg_chain* c, float* out, sg_stream_t stream) {
+int sg_chain_fwd(const sg_chain* c, float* out, double* rowsum, sg_stream_t stream) {
   ChainArgs a{};
   int rc = fill_args(a, c);
   if (rc) return rc;
   if (c->B <= 0) return 0;
   a.out = out;
+  a.rowsum = rowsum;
   // stage all filters up front unless that costs occupancy the launch could use
   const size_t ring_bytes = fwd_warp_bytes(c->kf, a.n_max, kRing);
   const size_t all_bytes = fwd_warp_bytes(c->kf, a.n_max, a.m);

@@ -623,6 +623,22 @@ __global__ void __launch_bounds__(256) k_nll_fwd(const Rows p, int64_t B, const 
   nll_finish(v, loss, blocks, counter, B);
 }
 
+// Row sums already known (the fused Sum-N chain forward writes them as a side output):
+// only the picked probability and the log term per sample remain.
+__global__ void __launch_bounds__(256) k_nll_fwd_given(const Rows p, int64_t B, const int64_t* __restrict__ targets,
+                                                       const double* __restrict__ rowsum, double* __restrict__ loss,
+                                                       double* __restrict__ blocks, unsigned* __restrict__ counter) {
+  const int64_t b0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_wait();
+  double v = 0.0;
+  if (b0 < B) {
+    const int64_t t = __ldg(targets + b0);
+    const double pt = t >= 0 ? (double)p.ld(t, b0) : 0.0;
+    v = log(nll_picked(__ldg(rowsum + b0), pt, t));
+  }
+  nll_finish(v, loss, blocks, counter, B);
+}
+
 // One-pass forward (chunks == 1): a CTA sums all rows of its 32 samples (warps split the
 // rows, same order as k_nll_partial), then finishes their log terms.
 __global__ void __launch_bounds__(256) k_nll_fwd1(const Rows p, int n, int64_t B, const int64_t* __restrict__ targets,
@@ -906,6 +922,15 @@ int sg_nll_fwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, doub
   if (e != cudaSuccess) return (int)e;
   return (int)launch(k_nll_fwd, dim3(blocks), dim3(256), 0, st, rows_of(probs), B, targets, (const double*)part, chunks,
                      rowsum, loss, blk, counter);
+}
+
+int sg_nll_fwd_rowsum(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, const double* rowsum,
+                      double* loss, void* scratch, sg_stream_t stream) {
+  if (B <= 0) return 0;
+  (void)n;
+  double* base = (double*)scratch;
+  return (int)launch(k_nll_fwd_given, dim3(ceil_div(B, 256)), dim3(256), 0, (cudaStream_t)stream, rows_of(probs), B,
+                     targets, rowsum, loss, base + 2, (unsigned*)base);
 }
 
 int sg_nll_bwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, const double* grad_loss,

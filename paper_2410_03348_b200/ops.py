@@ -173,8 +173,10 @@ class ConvChainFn(torch.autograd.Function):
         states = torch.empty((max(elems, 1),), device=dev, dtype=F32)
         out = torch.empty((n0 + m * (kf - 1), B), device=dev, dtype=F32)
         c = _chain_struct(n0, kf, B, base, filters, states)
-        rc = _lib().sg_chain_fwd(ctypes.byref(c), out.data_ptr(), N.stream_ptr(dev))
+        rowsum = torch.empty((B,), device=dev, dtype=torch.float64)
+        rc = _lib().sg_chain_fwd(ctypes.byref(c), out.data_ptr(), rowsum.data_ptr(), N.stream_ptr(dev))
         N.check(rc, "sg_chain_fwd")
+        out._sg_rowsum = (rowsum, out._version)  # for loss_nll on exactly these values
         ctx.meta = (n0, kf, B)
         ctx.save_for_backward(base, states, *filters)
         return out
@@ -299,6 +301,20 @@ def _nll_scratch(dev, n: int, B: int) -> torch.Tensor:
     return buf
 
 
+def known_rowsum(probs_nb: torch.Tensor):
+    """Per-sample row sums a fused chain forward wrote beside ``probs_nb``'s values, if
+    ``probs_nb`` is exactly that output and unmodified since (else None)."""
+    base = probs_nb._base if probs_nb._base is not None else probs_nb
+    tag = getattr(base, "_sg_rowsum", None)
+    if tag is None:
+        return None
+    rowsum, version = tag
+    if (base._version != version or probs_nb.data_ptr() != base.data_ptr() or probs_nb.shape != base.shape
+            or probs_nb.stride() != base.stride()):
+        return None
+    return rowsum
+
+
 class NllLoss(torch.autograd.Function):
     """Fused get_probs -> loss_nll (learn.py:92-119) over an (n, B) probability view."""
 
@@ -309,10 +325,16 @@ class NllLoss(torch.autograd.Function):
         dev = probs_nb.device
         loss = torch.empty((), device=dev, dtype=torch.float64)
         scratch = _nll_scratch(dev, n, B)
-        rowsum = torch.empty((B,), device=dev, dtype=torch.float64)
-        rc = _lib().sg_nll_fwd(N.rows(probs_nb), n, B, targets.data_ptr(), loss.data_ptr(), scratch.data_ptr(),
-                               rowsum.data_ptr(), N.stream_ptr(dev))
-        N.check(rc, "sg_nll_fwd")
+        rowsum = known_rowsum(probs_nb)
+        if rowsum is not None:  # a fused chain forward already summed these rows
+            rc = _lib().sg_nll_fwd_rowsum(N.rows(probs_nb), n, B, targets.data_ptr(), rowsum.data_ptr(),
+                                          loss.data_ptr(), scratch.data_ptr(), N.stream_ptr(dev))
+            N.check(rc, "sg_nll_fwd_rowsum")
+        else:
+            rowsum = torch.empty((B,), device=dev, dtype=torch.float64)
+            rc = _lib().sg_nll_fwd(N.rows(probs_nb), n, B, targets.data_ptr(), loss.data_ptr(), scratch.data_ptr(),
+                                   rowsum.data_ptr(), N.stream_ptr(dev))
+            N.check(rc, "sg_nll_fwd")
         ctx.save_for_backward(probs_nb, targets, rowsum)
         return loss
 

@@ -571,3 +571,39 @@ def test_sum15_step_launches_four_native_kernels(cuda):
     step()
     torch.cuda.synchronize()
     assert N.launch_count() - n0 == 4
+
+
+def test_chain_rowsum_feeds_the_loss(cuda):
+    """The fused chain forward's fp64 row sums (a side output) let loss_nll skip its row
+    pass; the loss and gradients equal the general path's, and an in-place change of the
+    probabilities invalidates the shortcut."""
+    S = sg()
+    from paper_2410_03348_b200 import ops
+    from paper_2410_03348_b200 import programs as P
+    from paper_2410_03348_b200.learn import loss_nll
+
+    rng = np.random.default_rng(4)
+    B = 777
+    xs = [torch.tensor(G.rows(rng, B, 10), device=cuda, requires_grad=True) for _ in range(6)]
+    t = torch.tensor(rng.integers(-1, 46, size=B), device=cuda)
+
+    def run(detour):
+        ctx = S.ProgramContext(S.Damp(), device=cuda)
+        probs = S.get_probs(P.sum_n(ctx, [S.make_distribution(ctx, x, range(10)) for x in xs]))
+        assert ops.known_rowsum(probs.t()) is not None
+        if detour:
+            probs = probs * 1.0  # a different tensor: the loss computes its own row sums
+            assert ops.known_rowsum(probs.t()) is None
+        loss = loss_nll(probs, t)
+        return float(loss), [g.cpu().numpy() for g in torch.autograd.grad(loss, xs)]
+
+    l_fused, g_fused = run(False)
+    l_gen, g_gen = run(True)
+    assert l_fused == pytest.approx(l_gen, rel=1e-12)
+    for a, b in zip(g_fused, g_gen):
+        assert_close_rel(a, b, 1e-9, 1e-12)
+    ctx = S.ProgramContext(S.Damp(), device=cuda)
+    out = P.sum_n(ctx, [S.make_distribution(ctx, x.detach(), range(10)) for x in xs])
+    probs = S.get_probs(out)
+    probs.mul_(0.5)
+    assert ops.known_rowsum(probs.t()) is None
