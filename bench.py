@@ -274,6 +274,18 @@ def ncu_traffic(kernel):
         return None
 
 
+def allreduce_max(x, world, device, backend):
+    """Max over ranks of a host float (device timing of each rank)."""
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return float(x)
+    t = torch.tensor([x], dtype=torch.float64, device=device if backend == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_gpu_arm(args):
     import torch
     import torch.distributed as dist
@@ -281,10 +293,17 @@ def run_gpu_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU (the driver's launch); SG_BENCH_BACKEND=gloo lets ranks share a
+    # device to exercise the N>1 control flow where only one GPU exists
+    backend = os.environ.get("SG_BENCH_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend != "nccl" else local
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
 
     import paper_2410_03348_b200 as sg
     from paper_2410_03348_b200 import _native as N
@@ -344,10 +363,7 @@ def run_gpu_arm(args):
     dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     if world > 1:
         dist.barrier()
-    t = torch.tensor([dev_ms], device=device, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = allreduce_max(dev_ms, world, device, backend)
     units = world * B * combos_per_sample() * args.steps
     value = units / (max_ms * 1e-3)
 
@@ -425,10 +441,7 @@ def run_gpu_arm(args):
                 fn()
         b.record()
         torch.cuda.synchronize(device)
-        tt = torch.tensor([a.elapsed_time(b)], device=device, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        return float(tt.item())
+        return allreduce_max(a.elapsed_time(b), world, device, backend)
 
     e2e_ms = e2e_time(e2e_pipelined, e2e_steps, loop=True)
     e2e_value = world * B * combos_per_sample() * e2e_steps / (e2e_ms * 1e-3)
