@@ -152,6 +152,33 @@ def damp_apply(kplan: KernelPlan, inputs, B: int) -> torch.Tensor:
     return DampApply.apply(kplan, B, *inputs)
 
 
+# Opt-in per-launch CUDA-event timers (bench.py): while LAUNCH_TIMERS is a dict, the
+# launches below are bracketed by timing events on their stream — also inside a CUDA-graph
+# capture, where they become event-record nodes replayed with the step.
+LAUNCH_TIMERS = None
+
+
+class launch_timer:
+    __slots__ = ("name", "e0")
+
+    def __init__(self, name):
+        self.name = name
+        self.e0 = None
+
+    def __enter__(self):
+        if LAUNCH_TIMERS is not None:
+            self.e0 = torch.cuda.Event(enable_timing=True, external=True)
+            self.e0.record()
+        return self
+
+    def __exit__(self, *exc):
+        if self.e0 is not None:
+            e1 = torch.cuda.Event(enable_timing=True, external=True)  # a timing node when captured
+            e1.record()
+            LAUNCH_TIMERS.setdefault(self.name, []).append((self.e0, e1))
+        return False
+
+
 @functools.lru_cache(maxsize=None)
 def chain_max_rows(kf: int) -> int:
     return int(_lib().sg_chain_max_rows(kf))
@@ -174,7 +201,8 @@ class ConvChainFn(torch.autograd.Function):
         out = torch.empty((n0 + m * (kf - 1), B), device=dev, dtype=F32)
         c = _chain_struct(n0, kf, B, base, filters, states)
         rowsum = torch.empty((B,), device=dev, dtype=torch.float64)
-        rc = _lib().sg_chain_fwd(ctypes.byref(c), out.data_ptr(), rowsum.data_ptr(), N.stream_ptr(dev))
+        with launch_timer("chain_fwd"):
+            rc = _lib().sg_chain_fwd(ctypes.byref(c), out.data_ptr(), rowsum.data_ptr(), N.stream_ptr(dev))
         N.check(rc, "sg_chain_fwd")
         out._sg_rowsum = (rowsum, out._version)  # for loss_nll on exactly these values
         ctx.meta = (n0, kf, B)
@@ -192,7 +220,8 @@ class ConvChainFn(torch.autograd.Function):
         arr = (N.SgRows * N.CHAIN_MAX_STEPS)()
         for i, t in enumerate(gfilt):
             arr[i] = N.rows(t)
-        rc = _lib().sg_chain_bwd(ctypes.byref(c), g.data_ptr(), N.rows(gbase), arr, N.stream_ptr(g.device))
+        with launch_timer("chain_bwd"):
+            rc = _lib().sg_chain_bwd(ctypes.byref(c), g.data_ptr(), N.rows(gbase), arr, N.stream_ptr(g.device))
         N.check(rc, "sg_chain_bwd")
         return (None, None, None, gbase, *gfilt)
 
