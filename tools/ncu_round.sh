@@ -9,7 +9,7 @@ timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   python bench.py --quick --steps 2 --warmup 1 > gpurun_out/${TAG}_ncu_quick.out 2>&1; echo "launches rc=$?"
 # --set full of one launch of each hot kernel inside the captured Sum-15 step (B=16384);
 # default cache control (flushed before the launch): the cold per-launch roofline case
-for KS in k_chain_bwd:4 k_chain_fwd:4 k_nll_fwd1:4 k_nll_bwd:4; do
+for KS in k_chain_bwd:4 k_chain_fwd:4 k_nll_fwd_given:4 k_nll_bwd:4; do
   K=${KS%%:*}; S=${KS##*:}
   timeout 300 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 \
     -o gpurun_out/${TAG}_full_$K -f python bench.py --quick --steps 2 --warmup 1 > gpurun_out/${TAG}_ncu_$K.out 2>&1

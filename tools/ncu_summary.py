@@ -51,7 +51,7 @@ def launch_table(path: Path):
         except ValueError:
             pass
     L = list(launches.values())
-    # the last complete captured step: from the last k_nll_fwd back to the previous one
+    # the last complete captured step: from the last loss-forward launch back to the previous one
     idx = [i for i, l in enumerate(L) if "k_nll_fwd" in l["name"]]
     if len(idx) >= 2:
         a, b = idx[-2], idx[-1]
