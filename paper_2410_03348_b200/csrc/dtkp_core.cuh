@@ -4,6 +4,10 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef SG_DTKP_UNROLL_K
+#define SG_DTKP_UNROLL_K 4
+#endif
+
 namespace sg {
 
 // Running top-k of distinct proofs ordered by (key desc, stream position asc).
@@ -199,6 +203,9 @@ __device__ __forceinline__ int rec_row(const DtkpK& a, int c, int i) { return __
 
 template <int K, int WT>
 __global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
+  // loops over the K proof rows are unrolled for small K: every row / top-k entry is then
+  // a compile-time register index instead of a runtime select
+  constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
   extern __shared__ __align__(16) unsigned char ptile_raw[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -229,7 +236,7 @@ __global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
       for (int c = item.y; c < item.z; ++c) {
         const bool more = c + 1 < item.z;
         if (more) fetch(c + 1, nxt);
-#pragma unroll 1
+#pragma unroll (kUnrollK)
         for (int q = 0; q < K; ++q) {
           if (!((cur.pres >> q) & 1u)) continue;
           uint64_t mm[WT];
@@ -253,12 +260,12 @@ __global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
         }
         TopK<K, WT> T;
         T.clear();
-#pragma unroll 1
+#pragma unroll (kUnrollK)
         for (int qa = 0; qa < K; ++qa) {
           if (!((A.pres >> qa) & 1u)) continue;
           uint64_t ma[WT];
           A.row(qa, ma);
-#pragma unroll 1
+#pragma unroll (kUnrollK)
           for (int qb = 0; qb < K; ++qb) {
             if (!((Bt.pres >> qb) & 1u)) continue;
             uint64_t mm[WT];
@@ -274,12 +281,13 @@ __global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
           Ci.load(a.ops[i], a.B, b, rec_row(a, c, i));
           TopK<K, WT> U;
           U.clear();
-#pragma unroll 1
-          for (int qa = 0; qa < T.n; ++qa) {
+#pragma unroll (kUnrollK)
+          for (int qa = 0; qa < K; ++qa) {
+            if (qa >= T.n) break;
             uint64_t ma[WT];
             double ka;
             T.get(qa, ma, ka);
-#pragma unroll 1
+#pragma unroll (kUnrollK)
             for (int qb = 0; qb < K; ++qb) {
               if (!((Ci.pres >> qb) & 1u)) continue;
               uint64_t mm[WT];
@@ -291,8 +299,9 @@ __global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
           }
           T = U;
         }
-#pragma unroll 1
-        for (int q = 0; q < T.n; ++q) {
+#pragma unroll (kUnrollK)
+        for (int q = 0; q < K; ++q) {
+          if (q >= T.n) break;
           uint64_t mm[WT];
           double kk;
           T.get(q, mm, kk);
