@@ -168,9 +168,9 @@ __device__ __forceinline__ void stage_filter(float2* F, int slot, const CRows& S
 template <int KF, int R>
 __device__ __forceinline__ void conv_tile(float2 (&acc)[R], const float2 (&w)[R + KF - 1], const float2 (&f)[KF]) {
 #pragma unroll
-  for (int r = 0; r < R; ++r) acc[r] = zero2();
+  for (int r = 0; r < R; ++r) acc[r] = __fmul2_rn(w[r + KF - 1], f[0]);  // == fma(w, f, 0)
 #pragma unroll
-  for (int j = 0; j < KF; ++j)
+  for (int j = 1; j < KF; ++j)
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = ffma2(w[r + KF - 1 - j], f[j], acc[r]);
 }
@@ -342,15 +342,15 @@ __device__ __forceinline__ void load_prev(float2 (&pv)[R], const ChainArgs& a, c
 // (deterministic, no atomics).
 template <int KF, int R, bool FIRST>
 __device__ __forceinline__ void bwd_round(float2* G, const float2 (&f)[KF], const float2 (&pv)[R], float2 (&d2)[KF],
-                                          int s0, int nin, const ChainArgs& a, const Lane& L) {
+                                          int s0, int nin, bool full, const ChainArgs& a, const Lane& L) {
   float2 gw[R + KF - 1];
 #pragma unroll
   for (int u = 0; u < R + KF - 1; ++u) gw[u] = G[(s0 + u) * kCP];
   float2 acc[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) acc[r] = zero2();
+  for (int r = 0; r < R; ++r) acc[r] = __fmul2_rn(gw[r], f[0]);  // == fma(gw, f, 0)
 #pragma unroll
-  for (int j = 0; j < KF; ++j)
+  for (int j = 1; j < KF; ++j)
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = ffma2(gw[r + j], f[j], acc[r]);
 #pragma unroll
@@ -359,8 +359,13 @@ __device__ __forceinline__ void bwd_round(float2* G, const float2 (&f)[KF], cons
     for (int j = 0; j < KF; ++j) d2[j] = ffma2(gw[r + j], pv[r], d2[j]);
   if constexpr (!FIRST) {
     __syncwarp();  // every group's window is loaded before any group stores
+    if (full) {  // warp-uniform: every row of this round is a real row
 #pragma unroll
-    for (int r = 0; r < R; ++r) G[(s0 + r) * kCP] = s0 + r < nin ? acc[r] : zero2();
+      for (int r = 0; r < R; ++r) G[(s0 + r) * kCP] = acc[r];
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) G[(s0 + r) * kCP] = s0 + r < nin ? acc[r] : zero2();
+    }
   } else {
 #pragma unroll
     for (int r = 0; r < R; ++r)
@@ -382,10 +387,10 @@ __device__ __forceinline__ void bwd_step(float2* G, float2* scratch, const float
   for (int k = 0; k < kr; k += 2) {
     const int s0 = k * STEP + s0g;
     if (k + 1 < kr) load_prev<R, FIRST>(pvB, a, sblk, L, i, s0 + STEP);
-    bwd_round<KF, R, FIRST>(G, f, pvA, d2, s0, nin, a, L);
+    bwd_round<KF, R, FIRST>(G, f, pvA, d2, s0, nin, (k + 1) * STEP <= nin, a, L);
     if (k + 1 >= kr) break;
     if (k + 2 < kr) load_prev<R, FIRST>(pvA, a, sblk, L, i, s0 + 2 * STEP);
-    bwd_round<KF, R, FIRST>(G, f, pvB, d2, s0 + STEP, nin, a, L);
+    bwd_round<KF, R, FIRST>(G, f, pvB, d2, s0 + STEP, nin, (k + 2) * STEP <= nin, a, L);
   }
   if constexpr (!FIRST) {
     // rows [kr*STEP, kr*STEP + KF - 1) may still hold G_i; the next step's windows reach them
