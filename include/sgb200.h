@@ -57,7 +57,7 @@ typedef struct sg_segsum {
   int32_t n_split;    /* segments spread over more than one item                */
   int32_t n_partial;  /* partial rows needed in scratch ([n_partial][B] floats)  */
   int32_t staged;     /* 1: stage operand tiles in shared memory                */
-  int32_t pad_;
+  int32_t n_recs;     /* records (rows of recs)                                 */
   const int32_t* recs;  /* [n_recs][rec_words]                                  */
   const int32_t* items; /* [n_items][4] = seg, rec_begin, rec_end, dest (-1 = direct) */
   const int32_t* blk;   /* [n_blocks + 1] item range of each CTA chunk            */
@@ -108,10 +108,11 @@ int sg_segsum_run(const sg_segsum* prob, const sg_rows* ops, const int32_t* op_r
 /* out: contiguous [n_out][B]; scratch: [fwd.n_partial][B] floats (may be NULL if 0). */
 int sg_damp_apply_fwd(const sg_damp_plan* plan, const sg_rows* inputs, int64_t B,
                       float* out, float* scratch, sg_stream_t stream);
-/* grad_out: contiguous [n_out][B]; grad_in[k].ptr == NULL skips input k (the Toeplitz
- * path needs both); scratch: [max_k bwd[k].n_partial][B] floats. */
+/* grad_out: [n_out][B] rows with any strides (the short-filter Toeplitz path, conv == 1,
+ * needs stride_b == 1 and stride_row == B); grad_in[k].ptr == NULL skips input k (conv == 1
+ * needs both); scratch: [max_k bwd[k].n_partial][B] floats. */
 int sg_damp_apply_bwd(const sg_damp_plan* plan, const sg_rows* inputs,
-                      const float* grad_out, int64_t B, const sg_rows* grad_in,
+                      sg_rows grad_out, int64_t B, const sg_rows* grad_in,
                       float* scratch, sg_stream_t stream);
 /* out[r][b] = clamp01(A[ia[r]][b] + Bm[ib[r]][b]) into contiguous [n_rows][B];
  * index -1 contributes 0. */

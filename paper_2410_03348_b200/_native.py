@@ -32,7 +32,7 @@ class SgSegsum(Structure):
         ("n_split", c_int32),
         ("n_partial", c_int32),
         ("staged", c_int32),
-        ("pad_", c_int32),
+        ("n_recs", c_int32),
         ("recs", c_void_p),
         ("items", c_void_p),
         ("blk", c_void_p),
@@ -114,7 +114,7 @@ EXPORTS = {
     "sg_damp_apply_fwd": (c_int32, [POINTER(SgDampPlan), POINTER(SgRows), c_int64, c_void_p, c_void_p, c_void_p]),
     "sg_damp_apply_bwd": (
         c_int32,
-        [POINTER(SgDampPlan), POINTER(SgRows), c_void_p, c_int64, POINTER(SgRows), c_void_p, c_void_p],
+        [POINTER(SgDampPlan), POINTER(SgRows), SgRows, c_int64, POINTER(SgRows), c_void_p, c_void_p],
     ),
     "sg_damp_rows_add": (
         c_int32,

@@ -78,6 +78,7 @@ static cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_
 struct SegsumK {
   Rows ops[SG_MAX_ARITY];
   int32_t op_off[SG_MAX_ARITY];  // row offset of operand i inside the shared tile
+  int32_t op_fo[SG_MAX_ARITY];   // resident kernel: float offset of operand i inside a group tile
   int32_t op_rows[SG_MAX_ARITY];
   int32_t clamp;
   int64_t B;
@@ -173,6 +174,186 @@ __global__ void __launch_bounds__(256) k_segsum(const SegsumK a) {
 #undef SG_VAL
 }
 
+// Plan-resident persistent variant for small plans (north-star kernel 1/2 on the HBM-bound
+// shapes: tens of symbols, a few hundred records).  The whole plan — items and records —
+// is staged once per CTA into shared memory, and each persistent CTA then walks sample
+// groups of 32: the operand rows of the NEXT group stream in with cp.async while the
+// current group's segments are summed from shared memory (records are warp-broadcast
+// reads, operands conflict-free [row][32] lane reads), and every output row leaves as one
+// coalesced 128-byte store.  No dependent global load chain per item, no re-staging per
+// item chunk.  Same record order and accumulator pairing as k_segsum (bit-identical).
+constexpr int kResWarps = 4;
+
+// One record of RW int32 words from shared memory (warp-broadcast vector read).
+template <int RW>
+__device__ __forceinline__ Rec<RW> load_rec_s(const int32_t* p) {
+  Rec<RW> r;
+  if constexpr (RW == 1) {
+    r.v[0] = p[0];
+  } else if constexpr (RW == 2) {
+    const int2 t = *reinterpret_cast<const int2*>(p);
+    r.v[0] = t.x; r.v[1] = t.y;
+  } else {
+#pragma unroll
+    for (int k = 0; k < RW; k += 4) {
+      const int4 t = *reinterpret_cast<const int4*>(p + k);
+      r.v[k] = t.x; r.v[k + 1] = t.y; r.v[k + 2] = t.z; r.v[k + 3] = t.w;
+    }
+  }
+  return r;
+}
+
+__device__ __forceinline__ void cp_async4_res(float* dst, const float* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16_res(void* dst, const void* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(src) : "memory");
+}
+
+// SM count of the current device (cached per device).
+static int sm_count_cur() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = v > 0 ? v : 148;
+  }
+  return cache[dev];
+}
+
+__host__ __device__ inline size_t res_plan_bytes(int n_items, int n_recs, int rw) {
+  return ((size_t)n_items * 16 + (size_t)n_recs * rw * 4 + 15) / 16 * 16;
+}
+
+template <int NOPS, int RW, bool VEC, int SM>
+__global__ void __launch_bounds__(kResWarps * 32) k_segsum_res(const SegsumK a, int n_items, int n_recs,
+                                                               int tile_floats, int64_t n_groups) {
+  // A sample group is 64 samples: lane l holds the PAIR (b0, b0 + 1), b0 = 64 g + 2 l, so
+  // every product / accumulation is one packed FMUL2 / FADD2.  Operand i is staged
+  //  * symbol-major (bit i of SM clear): [row][64 samples], one conflict-free LDS.64 per
+  //    read; or
+  //  * sample-major (bit i set; a (B, n) block such as a user softmax output or the
+  //    upstream gradient of get_probs): the group's 64 contiguous sample rows copied in
+  //    16-byte chunks and read with the sample stride — no transposition copy anywhere.
+  extern __shared__ __align__(16) unsigned char res_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int4* items = reinterpret_cast<int4*>(res_smem);
+  int32_t* recs = reinterpret_cast<int32_t*>(items + n_items);
+  float* tiles = reinterpret_cast<float*>(res_smem + res_plan_bytes(n_items, n_recs, RW));
+  pdl_wait();
+  {  // the plan, once per CTA
+    for (int i = threadIdx.x; i < n_items; i += blockDim.x) cp_async16_res(items + i, a.items + 4 * (size_t)i);
+    const int rn = n_recs * RW;
+    for (int i = threadIdx.x; i < rn; i += blockDim.x)
+      cp_async4_res(reinterpret_cast<float*>(recs + i), reinterpret_cast<const float*>(a.recs + i));
+  }
+  auto stage = [&](int64_t grp, float* t) {
+    const int64_t first = grp * 2 * kWarp;
+    const int64_t b0 = first + 2 * lane;
+    const int64_t ba = b0 < a.B ? b0 : a.B - 1;
+    const int64_t bb = b0 + 1 < a.B ? b0 + 1 : a.B - 1;
+#pragma unroll
+    for (int i = 0; i < NOPS; ++i) {
+      const Rows src = a.ops[i];
+      if ((SM >> i) & 1) {
+        const int64_t valid = (a.B - first) < 2 * kWarp ? (a.B - first) : 2 * kWarp;  // samples in this group
+        const int64_t nfl = valid * src.sb;                                            // floats to copy
+        const float* q = src.p + first * src.sb;
+        float* d = t + a.op_fo[i];
+        const int chunks = (int)(2 * kWarp * src.sb / 4);
+        for (int k = threadIdx.x; k < chunks; k += blockDim.x) {
+          const int64_t f0 = 4 * (int64_t)k;
+          if (f0 < nfl && f0 + 4 > nfl) continue;    // straddles the end: element-wise below
+          const int bytes = f0 + 4 <= nfl ? 16 : 0;  // past the last sample: zero fill
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(d + f0);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(bytes ? q + f0 : src.p),
+                       "r"(bytes) : "memory");
+        }
+        if (nfl % 4) {  // a straddling tail chunk: element-wise
+          for (int64_t f = nfl & ~3ll; f < nfl; ++f)
+            if (threadIdx.x == 0) cp_async4_res(d + f, q + f);
+        }
+      } else {
+        float* d = t + a.op_fo[i] + 2 * lane;
+        const float* qa = src.p + ba * src.sb;
+        const float* qb = src.p + bb * src.sb;
+        for (int r = warp; r < a.op_rows[i]; r += kResWarps) {
+          cp_async4_res(d + (size_t)r * 2 * kWarp, qa + (int64_t)r * src.sr);
+          cp_async4_res(d + (size_t)r * 2 * kWarp + 1, qb + (int64_t)r * src.sr);
+        }
+      }
+    }
+  };
+  // operand i, row r, for the lane's pair
+  auto opv = [&](const float* t, int i, int r) -> float2 {
+    if ((SM >> i) & 1) {
+      const int64_t sb = a.ops[i].sb;
+      const float* q = t + a.op_fo[i] + (int64_t)(2 * lane) * sb + r;
+      return make_float2(q[0], q[sb]);
+    }
+    return *reinterpret_cast<const float2*>(t + a.op_fo[i] + (size_t)r * 2 * kWarp + 2 * lane);
+  };
+  int64_t grp = blockIdx.x;
+  if (grp < n_groups) stage(grp, tiles);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int it = 0; grp < n_groups; ++it, grp += gridDim.x) {
+    const int64_t nxt = grp + gridDim.x;
+    if (nxt < n_groups) stage(nxt, tiles + (size_t)((it + 1) & 1) * tile_floats);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // the plan + this group's operands landed
+    __syncthreads();
+    const float* t = tiles + (size_t)(it & 1) * tile_floats;
+    const int64_t b0 = grp * 2 * kWarp + 2 * lane;
+    const int nv = b0 >= a.B ? 0 : (b0 + 1 < a.B ? 2 : 1);
+    for (int itm = warp; itm < n_items; itm += kResWarps) {
+      const int4 item = items[itm];
+      float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+      int c = item.y;
+      for (; c + 1 < item.z; c += 2) {
+        const Rec<RW> r0 = load_rec_s<RW>(recs + (size_t)c * RW);
+        const Rec<RW> r1 = load_rec_s<RW>(recs + (size_t)(c + 1) * RW);
+        float2 q0 = opv(t, 0, r0.v[0]);
+        float2 q1 = opv(t, 0, r1.v[0]);
+#pragma unroll
+        for (int i = 1; i < NOPS; ++i) {
+          q0 = __fmul2_rn(q0, opv(t, i, r0.v[i]));
+          q1 = __fmul2_rn(q1, opv(t, i, r1.v[i]));
+        }
+        acc0 = __fadd2_rn(acc0, q0);
+        acc1 = __fadd2_rn(acc1, q1);
+      }
+      if (c < item.z) {
+        const Rec<RW> r0 = load_rec_s<RW>(recs + (size_t)c * RW);
+        float2 q0 = opv(t, 0, r0.v[0]);
+#pragma unroll
+        for (int i = 1; i < NOPS; ++i) q0 = __fmul2_rn(q0, opv(t, i, r0.v[i]));
+        acc0 = __fadd2_rn(acc0, q0);
+      }
+      float2 acc = __fadd2_rn(acc0, acc1);
+      if (item.w < 0) {
+        if (a.clamp) acc = make_float2(clamp01(acc.x), clamp01(acc.y));
+        float* o = a.out.p + (int64_t)item.x * a.out.sr;
+        if (VEC) {
+          if (nv == 2) *reinterpret_cast<float2*>(o + b0) = acc;
+        } else {
+          if (nv > 0) o[b0 * a.out.sb] = acc.x;
+          if (nv > 1) o[(b0 + 1) * a.out.sb] = acc.y;
+        }
+      } else {
+        float* o = a.scratch + (size_t)item.w * a.B;
+        if (nv > 0) o[b0] = acc.x;
+        if (nv > 1) o[b0 + 1] = acc.y;
+      }
+    }
+    __syncthreads();  // this group's tile is restaged two groups later
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 // Deterministic finish of segments spread over several items (pieces summed in order).
 __global__ void k_segsum_fixup(const int32_t* __restrict__ split, int n_split, const float* __restrict__ scratch,
                                int64_t B, int clamp, WRows out) {
@@ -198,6 +379,62 @@ static int launch_segsum_t(const SegsumK& k, int n_blocks, size_t smem, cudaStre
   return (int)e;
 }
 
+// Operand i is staged sample-major when it is a (B, n) row per sample (stride_row 1),
+// 16-byte aligned, without a huge padding stride, and wide enough (n >= 16) that a
+// per-element gather would touch a new line for nearly every sample (narrow blocks such as
+// a 10-digit softmax gather better per element: their lines are reused across rows).  The
+// sample stride must be odd: lane l then reads at 2 l * stride, 16 distinct banks (2-way).
+static bool sample_major_ok(const Rows& r, int rows, int64_t B) {
+  return B > 1 && r.sr == 1 && r.sb >= rows && rows >= 16 && (r.sb & 1) && r.sb <= 2 * (int64_t)rows + 8 &&
+         ((uintptr_t)r.p % 16) == 0;
+}
+
+template <int NOPS, int RW, int SM>
+static int launch_segsum_res_sm(SegsumK k, int n_items, int n_recs, cudaStream_t st) {
+  int fo = 0;
+  for (int i = 0; i < NOPS; ++i) {
+    k.op_fo[i] = fo;
+    fo += ((SM >> i) & 1) ? (int)(2 * kWarp * k.ops[i].sb) : k.op_rows[i] * 2 * kWarp;
+    fo = (fo + 3) & ~3;  // 16-byte aligned operand tiles
+  }
+  const int tile_floats = fo;
+  const size_t smem = res_plan_bytes(n_items, n_recs, RW) + 2 * (size_t)tile_floats * sizeof(float);
+  const bool vec = k.out.sb == 1 && (k.out.sr % 2 == 0) && ((uintptr_t)k.out.p % 8 == 0);
+  auto kern = vec ? k_segsum_res<NOPS, RW, true, SM> : k_segsum_res<NOPS, RW, false, SM>;
+  cudaError_t e = ensure_smem((const void*)kern, smem);
+  if (e != cudaSuccess) return (int)e;
+  const int64_t groups = ceil_div(k.B, 2 * kWarp);
+  int per_sm = (int)((227 * 1024) / (smem + 1024));
+  if (per_sm > 16) per_sm = 16;
+  int64_t grid = (int64_t)sm_count_cur() * per_sm;
+  if (grid > groups) grid = groups;
+  return (int)launch(kern, dim3((unsigned)grid), dim3(kResWarps * kWarp), smem, st, k, n_items, n_recs, tile_floats,
+                     groups);
+}
+
+template <int NOPS, int RW>
+static int launch_segsum_res(const SegsumK& k, int n_items, int n_recs, cudaStream_t st) {
+  int sm = 0;
+  for (int i = 0; i < NOPS; ++i)
+    if (sample_major_ok(k.ops[i], k.op_rows[i], k.B)) sm |= 1 << i;
+  switch (sm) {
+    case 0: return launch_segsum_res_sm<NOPS, RW, 0>(k, n_items, n_recs, st);
+    case 1: return launch_segsum_res_sm<NOPS, RW, 1>(k, n_items, n_recs, st);
+    case 2: if constexpr (NOPS >= 2) return launch_segsum_res_sm<NOPS, RW, 2>(k, n_items, n_recs, st); break;
+    case 3: if constexpr (NOPS >= 2) return launch_segsum_res_sm<NOPS, RW, 3>(k, n_items, n_recs, st); break;
+    default:
+      if constexpr (NOPS >= 3) {
+        switch (sm) {
+          case 4: return launch_segsum_res_sm<NOPS, RW, 4>(k, n_items, n_recs, st);
+          case 5: return launch_segsum_res_sm<NOPS, RW, 5>(k, n_items, n_recs, st);
+          case 6: return launch_segsum_res_sm<NOPS, RW, 6>(k, n_items, n_recs, st);
+          case 7: return launch_segsum_res_sm<NOPS, RW, 7>(k, n_items, n_recs, st);
+        }
+      }
+  }
+  return launch_segsum_res_sm<NOPS, RW, 0>(k, n_items, n_recs, st);
+}
+
 template <int NOPS, int RW>
 static int launch_segsum_s(const SegsumK& k, bool staged, int n_blocks, size_t smem, cudaStream_t st) {
   return staged ? launch_segsum_t<NOPS, RW, true>(k, n_blocks, smem, st)
@@ -205,6 +442,15 @@ static int launch_segsum_s(const SegsumK& k, bool staged, int n_blocks, size_t s
 }
 
 static constexpr size_t kMaxStageBytes = 200 * 1024;
+
+// SG_SEGSUM_RESIDENT=0 forces the item-chunked kernel (A/B runs)
+static bool res_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SG_SEGSUM_RESIDENT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 static int run_segsum(const sg_segsum* p, const sg_rows* ops, const int32_t* op_rows, int n_ops, int64_t B, int clamp,
                       sg_rows out, float* scratch, cudaStream_t st) {
@@ -229,7 +475,23 @@ static int run_segsum(const sg_segsum* p, const sg_rows* ops, const int32_t* op_
   const size_t smem = (size_t)total * kWarp * sizeof(float);
   const bool staged = p->staged && smem <= kMaxStageBytes;
   int rc = 0;
-  if (p->n_items > 0) {
+  // small plan, many sample groups: the plan-resident persistent kernel
+  size_t res_tiles = 0;  // two group tiles, each operand in its staging layout (bounded by 2x)
+  for (int i = 0; i < n_ops; ++i)
+    res_tiles += 2 * (size_t)2 * kWarp * sizeof(float) *
+                 (sample_major_ok(k.ops[i], op_rows[i], B) ? (size_t)k.ops[i].sb : (size_t)op_rows[i]);
+  const size_t res_smem = res_plan_bytes(p->n_items, p->n_recs, p->rec_words) + res_tiles;
+  const bool resident = res_enabled() && p->n_items > 0 && n_ops <= 3 && res_smem <= 64 * 1024 &&
+                        ceil_div(B, 2 * kWarp) >= 2 * sm_count_cur();
+  if (resident) {
+    const int rw = p->rec_words, ni = p->n_items, nr = p->n_recs;
+    switch (n_ops) {
+      case 1: rc = rw == 1 ? launch_segsum_res<1, 1>(k, ni, nr, st) : launch_segsum_res<1, 2>(k, ni, nr, st); break;
+      case 2: rc = launch_segsum_res<2, 2>(k, ni, nr, st); break;
+      default: rc = launch_segsum_res<3, 4>(k, ni, nr, st); break;
+    }
+    if (rc) return rc;
+  } else if (p->n_items > 0) {
     const int rw = p->rec_words;
     switch (n_ops) {
       case 1: rc = rw == 1 ? launch_segsum_s<1, 1>(k, staged, p->n_blocks, smem, st)
@@ -817,8 +1079,9 @@ int sg_damp_apply_fwd(const sg_damp_plan* plan, const sg_rows* inputs, int64_t B
   return run_segsum(&plan->fwd, inputs, plan->sizes, plan->arity, B, 1, o, scratch, st);
 }
 
-int sg_damp_apply_bwd(const sg_damp_plan* plan, const sg_rows* inputs, const float* grad_out, int64_t B,
+int sg_damp_apply_bwd(const sg_damp_plan* plan, const sg_rows* inputs, sg_rows grad_rows, int64_t B,
                       const sg_rows* grad_in, float* scratch, sg_stream_t stream) {
+  const Rows g = rows_of(grad_rows);
   cudaStream_t st = (cudaStream_t)stream;
   const int n = plan->arity;
   SG_RETURN_IF(n < 1 || n > SG_MAX_ARITY, cudaErrorInvalidValue);
@@ -828,7 +1091,6 @@ int sg_damp_apply_bwd(const sg_damp_plan* plan, const sg_rows* inputs, const flo
     const int n0 = plan->sizes[0], n1 = plan->sizes[1], n2 = plan->sizes[2], n01 = n0 + n1 - 1;
     float* t = scratch;
     float* dt = scratch + (size_t)n01 * B;
-    const Rows g{grad_out, B, 1};
     int rc = 0;
     if (grad_in[2].ptr != nullptr) {
       rc = lconv(rows_of(inputs[0]), n0, rows_of(inputs[1]), n1, 0, WRows{t, B, 1}, n01, B, 0, st);
@@ -849,7 +1111,6 @@ int sg_damp_apply_bwd(const sg_damp_plan* plan, const sg_rows* inputs, const flo
     return rc;
   }
   if (plan->conv == 2) {  // d in_k[s] = sum_j g[s + j] in_other[j]: correlation = conv with the other reversed
-    const Rows g{grad_out, B, 1};
     for (int k = 0; k < 2; ++k) {
       if (grad_in[k].ptr == nullptr) continue;
       const int o = 1 - k;
@@ -862,14 +1123,16 @@ int sg_damp_apply_bwd(const sg_damp_plan* plan, const sg_rows* inputs, const flo
   if (plan->conv) {
     const int sh = plan->conv_short, lo = 1 - sh;
     SG_RETURN_IF(grad_in[0].ptr == nullptr || grad_in[1].ptr == nullptr, cudaErrorInvalidValue);
-    return conv_bwd(plan->sizes[sh], grad_out, plan->n_out, rows_of(inputs[lo]), plan->sizes[lo], rows_of(inputs[sh]),
+    SG_RETURN_IF((B > 1 && grad_rows.stride_b != 1) || (plan->n_out > 1 && grad_rows.stride_row != B),
+                 cudaErrorInvalidValue);
+    return conv_bwd(plan->sizes[sh], grad_rows.ptr, plan->n_out, rows_of(inputs[lo]), plan->sizes[lo], rows_of(inputs[sh]),
                     wrows_of(grad_in[lo]), wrows_of(grad_in[sh]), B, st);
   }
   for (int k = 0; k < n; ++k) {
     if (grad_in[k].ptr == nullptr) continue;
     sg_rows ops[SG_MAX_ARITY];
     int32_t rows[SG_MAX_ARITY];
-    ops[0] = sg_rows{const_cast<float*>(grad_out), B, 1};
+    ops[0] = grad_rows;
     rows[0] = plan->n_out;
     int m = 1;
     for (int j = 0; j < n; ++j) {

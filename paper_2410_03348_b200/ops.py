@@ -125,7 +125,8 @@ class DampApply(torch.autograd.Function):
         inputs = ctx.saved_tensors
         kplan: KernelPlan = ctx.kplan
         B = ctx.B
-        g = g.contiguous()
+        if kplan.conv == 1:  # the short-filter Toeplitz backward reads contiguous rows
+            g = g.contiguous()
         dev = g.device
         need = [i for i in range(len(inputs)) if ctx.needs_input_grad[2 + i]]
         grads = [None] * len(inputs)
@@ -139,7 +140,7 @@ class DampApply(torch.autograd.Function):
             if kplan.conv == 3:
                 n_partial = 2 * (kplan.sizes[0] + kplan.sizes[1] - 1)
             scratch = torch.empty((n_partial, B), device=dev, dtype=F32) if n_partial else None
-            rc = _lib().sg_damp_apply_bwd(ctypes.byref(s), N.rows_array(inputs), g.data_ptr(), B,
+            rc = _lib().sg_damp_apply_bwd(ctypes.byref(s), N.rows_array(inputs), N.rows(g), B,
                                           N.rows_array(grads), N.ptr(scratch), N.stream_ptr(dev))
             N.check(rc, "sg_damp_apply_bwd")
             if kplan.conv:

@@ -404,6 +404,7 @@ class DeviceSegsum:
         s.n_split = len(h.split)
         s.n_partial = h.n_partial
         s.staged = 1 if self.staged else 0
+        s.n_recs = len(h.recs)
         s.recs = self.recs.data_ptr() if self.recs.numel() else None
         s.items = self.items.data_ptr() if self.items.numel() else None
         s.blk = blk.data_ptr()

@@ -87,7 +87,7 @@ def main():
 
         def bwd(j):
             a, b, out, g, ga, gb = sets[j % nsets]
-            N.check(lib.sg_damp_apply_bwd(ctypes.byref(st), N.rows_array([a, b]), g.data_ptr(), B,
+            N.check(lib.sg_damp_apply_bwd(ctypes.byref(st), N.rows_array([a, b]), N.rows(g), B,
                                           N.rows_array([ga, gb]), None, torch.cuda.current_stream(dev).cuda_stream),
                     "bwd")
 
