@@ -607,3 +607,29 @@ def test_chain_rowsum_feeds_the_loss(cuda):
     probs = S.get_probs(out)
     probs.mul_(0.5)
     assert ops.known_rowsum(probs.t()) is None
+
+
+@pytest.mark.parametrize("fn,size", [("prod", 10), ("lin", 17), ("undef", 12)])
+def test_generic_apply_resident_one_pass_backward(cuda, fn, size):
+    """Large-batch arity-2 generic applies run on the plan-resident kernel (forward and the
+    per-input backward problems, the upstream gradient read in place as the (B, n) block a
+    torch loss produces): vs the oracle."""
+    S = sg()
+    from oracle import algebra as A
+    f = {"prod": lambda x, y: x * y, "lin": lambda x, y: (x + 3 * y) % 17,
+         "undef": lambda x, y: S.UNDEFINED if (x + y) % 5 == 0 else (x * y) % 23}[fn]
+    B = 2 * 64 * 148 + 77  # >= 2 sample groups of 64 per SM: the resident kernel
+    rng = np.random.default_rng(size)
+    xs = [G.rows(rng, B, size) for _ in range(2)]
+    ctx = S.ProgramContext(S.Damp())
+    leaves = [torch.tensor(x, device=cuda, dtype=torch.float32, requires_grad=True) for x in xs]
+    out = S.apply(f, *[S.make_distribution(ctx, lf, range(size)) for lf in leaves])
+    syms, combos, idx = A.map_shuffle(f, None, [list(range(size))] * 2, S.UNDEFINED)
+    assert out.symbols == syms
+    ref = A.damp_apply(xs, combos, idx, len(syms))
+    got = S.get_probs(out)
+    assert_close_rel(got.detach().cpu().numpy(), ref, 1e-5, 1e-7, what="probs")
+    w = rng.uniform(-1, 1, size=ref.shape).astype(np.float32)
+    torch.autograd.backward(got, torch.as_tensor(w, device=cuda))
+    for lf, gr in zip(leaves, A.damp_apply_grad(xs, combos, idx, w.astype(np.float64))):
+        assert_close_rel(lf.grad.cpu().numpy(), gr, 1e-5, 1e-6, what="grad")
