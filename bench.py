@@ -191,6 +191,20 @@ def chain_bytes(B, n0=10, kf=10, m=N_DIGITS - 1):
     return fwd, bwd
 
 
+def survey_chain_bytes(B, n0=10, kf=10, m=N_DIGITS - 1):
+    """SURVEY.md §8(d)'s algorithmic bytes for the same chain counted the unfused way:
+    every apply reads its inputs and writes its output (DAMP fwd = 4B(Σ|S_i| + N_out) + 4C,
+    bwd = 4B(N_out + 2Σ|S_i|) + 4C per apply).  The fused kernels never move the
+    intermediate states more than once, so this exceeds what they must move."""
+    fwd = bwd = 0
+    for i in range(m):
+        n_in = n0 + i * (kf - 1)
+        n_out = n_in + kf - 1
+        fwd += 4 * B * (n_in + kf + n_out) + 4 * n_in * kf
+        bwd += 4 * B * (n_out + 2 * (n_in + kf)) + 4 * n_in * kf
+    return fwd, bwd
+
+
 def kernel_roofline(torch, device, B, hbm_gbs, reps=12):
     """Per-launch time of the fused Sum-15 chain kernels (the step's two dominant
     launches), measured with CUDA events around a CUDA-graph replay of back-to-back
@@ -495,6 +509,12 @@ def run_gpu_arm(args):
                           "L2 flushed before each step; 'kernels' also gives each kernel timed alone, "
                           "cold (HBM-streamed rotating buffers)",
                 "share_of_step": step_us / (max_ms * 1e3 / args.steps), "kernels": kr}
+        sv = dict(zip(("chain_fwd", "chain_bwd"), survey_chain_bytes(B)))
+        if dom_name in sv:
+            roof["survey_8d"] = {"bytes_per_launch": sv[dom_name],
+                                 "frac": sv[dom_name] / (step_us * 1e-6) / 1e9 / hbm,
+                                 "note": "SURVEY §8(d) per-apply bytes (unfused I/O); 'achieved' uses the "
+                                         "fused chain's own minimum bytes_per_launch, the stricter figure"}
         if world == 1 and not args.no_cpu_baseline:
             try:
                 ref = cpu_reference(args.cpu_batch, repeats=3)
