@@ -2,8 +2,12 @@
 // See dtkp.cu for the semantics; this header is instantiated once per K (dtkp_apply_k.cu)
 // so the eight K variants compile in parallel.
 #pragma once
+#include <algorithm>
 #include "common.cuh"
 
+#ifndef SG_DTKP_WAVES  // resident waves of apply CTAs per launch (each strides over work blocks)
+#define SG_DTKP_WAVES 3
+#endif
 #ifndef SG_DTKP_UNROLL_K
 #define SG_DTKP_UNROLL_K 4
 #endif
@@ -96,12 +100,26 @@ __host__ __device__ inline int ptile_mode(int I) {
 __device__ __forceinline__ PCol stage_pcol(void* tile, const float* __restrict__ p, int I, int64_t B, int64_t b,
                                            int lane, int warp, int nwarps) {
   const bool dbl = ptile_mode(I) == 2;
-  if (dbl) {
-    double* t = reinterpret_cast<double*>(tile);
-    for (int j = warp; j < I; j += nwarps) t[(size_t)j * kWarp + lane] = (double)__ldg(p + (size_t)j * B + b);
-  } else {
-    float* t = reinterpret_cast<float*>(tile);
-    for (int j = warp; j < I; j += nwarps) t[(size_t)j * kWarp + lane] = __ldg(p + (size_t)j * B + b);
+  // eight independent loads in flight per thread (a serial load -> store loop here was
+  // ~40% of a short DTKP launch: one L2 round trip per column)
+  constexpr int U = 8;
+  for (int j0 = warp; j0 < I; j0 += U * nwarps) {
+    float v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * nwarps;
+      v[u] = j < I ? __ldg(p + (size_t)j * B + b) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * nwarps;
+      if (j < I) {
+        if (dbl)
+          reinterpret_cast<double*>(tile)[(size_t)j * kWarp + lane] = (double)v[u];
+        else
+          reinterpret_cast<float*>(tile)[(size_t)j * kWarp + lane] = v[u];
+      }
+    }
   }
   return PCol{reinterpret_cast<const double*>(tile) + lane, reinterpret_cast<const float*>(tile) + lane, dbl};
 }
@@ -145,6 +163,7 @@ struct DtkpK {
   int32_t rec_words;
   const int32_t* items;
   const int32_t* blk;
+  int32_t n_blk;  // work blocks; CTAs stride over them (set by the launcher)
   uint64_t* out_m;
   uint8_t* out_p;
   uint64_t* scr_m;
@@ -216,7 +235,9 @@ __global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
   const PCol pc = stage_pcol(ptile_raw, a.p, a.I, a.B, b, lane, warp, nwarps);
   __syncthreads();
 
-  const int it0 = __ldg(a.blk + blockIdx.y), it1 = __ldg(a.blk + blockIdx.y + 1);
+  // persistent over the work blocks: the probability tile above is staged once per CTA
+  for (int bk = blockIdx.y; bk < a.n_blk; bk += gridDim.y) {
+  const int it0 = __ldg(a.blk + bk), it1 = __ldg(a.blk + bk + 1);
   for (int it = it0 + warp; it < it1; it += nwarps) {
     const int4 item = __ldg(reinterpret_cast<const int4*>(a.items) + it);
     TopK<K, WT> S;
@@ -333,6 +354,7 @@ __global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
       }
     }
   }
+  }
 }
 
 template <int K, int WT>
@@ -340,13 +362,23 @@ static int launch_apply_kw(const DtkpK& k, int n_blocks, cudaStream_t st) {
   const int mode = ptile_mode(k.I);
   if (mode == 0) return (int)cudaErrorNotSupported;
   const size_t smem = (size_t)k.I * kWarp * (mode == 2 ? sizeof(double) : sizeof(float));
-  dim3 grid(ceil_div(k.B, kWarp), n_blocks);
   {
     cudaError_t e = ensure_smem((const void*)k_dtkp_apply<K, WT>, smem);
     if (e != cudaSuccess) return (int)e;
   }
+  // one resident wave of CTAs (x: 32-sample columns, y: strided over the work blocks)
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dtkp_apply<K, WT>, 128, smem);
+  const int64_t gx = ceil_div(k.B, kWarp);
+  const int64_t resident = (int64_t)std::max(occ, 1) * std::max(sms, 1) * SG_DTKP_WAVES;
+  const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(n_blocks, ceil_div(resident, gx)));
+  DtkpK kk = k;
+  kk.n_blk = n_blocks;
+  dim3 grid((unsigned)gx, gy);
   count_launch();
-  k_dtkp_apply<K, WT><<<grid, 128, smem, st>>>(k);
+  k_dtkp_apply<K, WT><<<grid, 128, smem, st>>>(kk);
   SG_LAUNCH_CHECK();
   return 0;
 }

@@ -6,16 +6,22 @@ import subprocess
 import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
-top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--kernel-name",
                       f"regex:{kern}"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h = rows[1]
+# --launch N: the N-th captured launch of the kernel (0-based; default the first)
+want = int(sys.argv[sys.argv.index("--launch") + 1]) if "--launch" in sys.argv else 0
+top = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3].isdigit() else 40
 data = []
+seen = 0
 for r in rows[2:]:
     if r and r[0] == "Kernel Name":
-        break  # first captured launch only
-    if len(r) == len(h) and r[0] != "Address":
+        seen += 1
+        if seen > want:
+            break
+        continue
+    if seen == want and len(r) == len(h) and r[0] != "Address":
         data.append(dict(zip(h, r)))
 stall_cols = [c for c in h if c.startswith("stall_")]
 tot = sum(float(d["Warp Stall Sampling (All Samples)"] or 0) for d in data)
