@@ -191,6 +191,11 @@ typedef struct sg_dtkp_apply_desc {
   uint64_t* scratch_member;/* [seg.n_partial][K][W][B] partial top-k of split segments      */
   uint8_t* scratch_present;/* [seg.n_partial][K][B] */
   sg_segsum merge;         /* arity-1 merge of partial rows (seg.n_split segments)           */
+  int32_t* sched;          /* optional work counters, ceil(B/32) + 1 int32, zero before the
+                            * first use and left zero by every launch (the last CTA resets
+                            * them): warps then take items dynamically instead of by the
+                            * static seg.blk partition.  Launches that may run concurrently
+                            * need distinct buffers.  NULL = static partition.            */
 } sg_dtkp_apply_desc;
 
 int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream);

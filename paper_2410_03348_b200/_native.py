@@ -97,6 +97,7 @@ class SgDtkpApplyDesc(Structure):
         ("scratch_member", c_void_p),
         ("scratch_present", c_void_p),
         ("merge", SgSegsum),
+        ("sched", c_void_p),
     ]
 
 

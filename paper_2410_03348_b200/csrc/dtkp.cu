@@ -253,6 +253,8 @@ int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream) {
   k.out_p = d->out_present;
   k.scr_m = d->scratch_member;
   k.scr_p = d->scratch_present;
+  k.sched = d->sched;
+  k.n_items = d->seg.n_items;
   if (d->seg.n_items > 0) {
     int rc = launch_apply(k, d->seg.n_blocks, st);
     if (rc) return rc;
@@ -269,6 +271,7 @@ int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream) {
     m.rec_words = d->merge.rec_words;
     m.items = d->merge.items;
     m.blk = d->merge.blk;
+    m.n_items = d->merge.n_items;
     m.scr_m = nullptr;
     m.scr_p = nullptr;
     int rc = launch_apply(m, d->merge.n_blocks, st);

@@ -164,6 +164,8 @@ struct DtkpK {
   const int32_t* items;
   const int32_t* blk;
   int32_t n_blk;  // work blocks; CTAs stride over them (set by the launcher)
+  int32_t n_items;
+  int32_t* sched;  // optional [gx + 1] zeroed counters: dynamic item schedule
   uint64_t* out_m;
   uint8_t* out_p;
   uint64_t* scr_m;
@@ -220,11 +222,129 @@ struct TagRows {
 
 __device__ __forceinline__ int rec_row(const DtkpK& a, int c, int i) { return __ldg(a.recs + (size_t)c * a.rec_words + i); }
 
+// One work item (an output segment, or a piece of a split one) for one sample: stream its
+// records through the top-k set and write the retained rows.
+template <int K, int WT>
+__device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, int64_t b0, bool bval, const PCol& pc) {
+  constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
+  const int4 item = __ldg(reinterpret_cast<const int4*>(a.items) + it);
+  TopK<K, WT> S;
+  S.clear();
+  if (a.arity == 1) {
+    // group_disj / union / merge: stream the stored rows of every record, in order;
+    // the next record's rows are loaded before the current one is ranked.
+    TagRows<K, WT> cur, nxt;
+    auto fetch = [&](int c, TagRows<K, WT>& t) {
+      int r = rec_row(a, c, 0);
+      if (r >= a.ops[0].rows)
+        t.load(a.tail, a.B, b, r - a.ops[0].rows);
+      else
+        t.load(a.ops[0], a.B, b, r);
+    };
+    if (item.y < item.z) fetch(item.y, cur);
+    for (int c = item.y; c < item.z; ++c) {
+      const bool more = c + 1 < item.z;
+      if (more) fetch(c + 1, nxt);
+#pragma unroll (kUnrollK)
+      for (int q = 0; q < K; ++q) {
+        if (!((cur.pres >> q) & 1u)) continue;
+        uint64_t mm[WT];
+        cur.row(q, mm);
+        S.insert(mm, proof_key<WT>(mm, pc), 0);
+      }
+      if (more) cur = nxt;
+    }
+  } else {
+    // conj fold, normalised after every step (candidate order ra*kb + rb)
+    TagRows<K, WT> A, Bt, An, Bn;
+    if (item.y < item.z) {
+      A.load(a.ops[0], a.B, b, rec_row(a, item.y, 0));
+      Bt.load(a.ops[1], a.B, b, rec_row(a, item.y, 1));
+    }
+    for (int c = item.y; c < item.z; ++c) {
+      const bool more = c + 1 < item.z;
+      if (more) {
+        An.load(a.ops[0], a.B, b, rec_row(a, c + 1, 0));
+        Bn.load(a.ops[1], a.B, b, rec_row(a, c + 1, 1));
+      }
+      TopK<K, WT> T;
+      T.clear();
+#pragma unroll (kUnrollK)
+      for (int qa = 0; qa < K; ++qa) {
+        if (!((A.pres >> qa) & 1u)) continue;
+        uint64_t ma[WT];
+        A.row(qa, ma);
+#pragma unroll (kUnrollK)
+        for (int qb = 0; qb < K; ++qb) {
+          if (!((Bt.pres >> qb) & 1u)) continue;
+          uint64_t mm[WT];
+          Bt.row(qb, mm);
+#pragma unroll
+          for (int w = 0; w < WT; ++w) mm[w] |= ma[w];
+          T.insert(mm, proof_key<WT>(mm, pc), 0);
+        }
+      }
+#pragma unroll 1
+      for (int i = 2; i < a.arity; ++i) {
+        TagRows<K, WT> Ci;
+        Ci.load(a.ops[i], a.B, b, rec_row(a, c, i));
+        TopK<K, WT> U;
+        U.clear();
+#pragma unroll (kUnrollK)
+        for (int qa = 0; qa < K; ++qa) {
+          if (qa >= T.n) break;
+          uint64_t ma[WT];
+          double ka;
+          T.get(qa, ma, ka);
+#pragma unroll (kUnrollK)
+          for (int qb = 0; qb < K; ++qb) {
+            if (!((Ci.pres >> qb) & 1u)) continue;
+            uint64_t mm[WT];
+            Ci.row(qb, mm);
+#pragma unroll
+            for (int w = 0; w < WT; ++w) mm[w] |= ma[w];
+            U.insert(mm, proof_key<WT>(mm, pc), 0);
+          }
+        }
+        T = U;
+      }
+#pragma unroll (kUnrollK)
+      for (int q = 0; q < K; ++q) {
+        if (q >= T.n) break;
+        uint64_t mm[WT];
+        double kk;
+        T.get(q, mm, kk);
+        S.insert(mm, kk, 0);  // same mask, same p -> same key as a recomputation
+      }
+      if (more) {
+        A = An;
+        Bt = Bn;
+      }
+    }
+  }
+  if (bval) {
+    uint64_t* om;
+    uint8_t* opr;
+    if (item.w < 0) {
+      om = a.out_m + (size_t)item.x * K * a.W * a.B;
+      opr = a.out_p + (size_t)item.x * K * a.B;
+    } else {
+      om = a.scr_m + (size_t)item.w * K * a.W * a.B;
+      opr = a.scr_p + (size_t)item.w * K * a.B;
+    }
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      const bool live = q < S.n;
+      opr[(size_t)q * a.B + b0] = live ? 1 : 0;
+#pragma unroll
+      for (int w = 0; w < WT; ++w)
+        if (w < a.W) om[((size_t)q * a.W + w) * a.B + b0] = live ? S.m[q][w] : 0ull;
+    }
+  }
+}
+
 template <int K, int WT>
 __global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
-  // loops over the K proof rows are unrolled for small K: every row / top-k entry is then
-  // a compile-time register index instead of a runtime select
-  constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
   extern __shared__ __align__(16) unsigned char ptile_raw[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -235,125 +355,33 @@ __global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
   const PCol pc = stage_pcol(ptile_raw, a.p, a.I, a.B, b, lane, warp, nwarps);
   __syncthreads();
 
-  // persistent over the work blocks: the probability tile above is staged once per CTA
-  for (int bk = blockIdx.y; bk < a.n_blk; bk += gridDim.y) {
-  const int it0 = __ldg(a.blk + bk), it1 = __ldg(a.blk + bk + 1);
-  for (int it = it0 + warp; it < it1; it += nwarps) {
-    const int4 item = __ldg(reinterpret_cast<const int4*>(a.items) + it);
-    TopK<K, WT> S;
-    S.clear();
-    if (a.arity == 1) {
-      // group_disj / union / merge: stream the stored rows of every record, in order;
-      // the next record's rows are loaded before the current one is ranked.
-      TagRows<K, WT> cur, nxt;
-      auto fetch = [&](int c, TagRows<K, WT>& t) {
-        int r = rec_row(a, c, 0);
-        if (r >= a.ops[0].rows)
-          t.load(a.tail, a.B, b, r - a.ops[0].rows);
-        else
-          t.load(a.ops[0], a.B, b, r);
-      };
-      if (item.y < item.z) fetch(item.y, cur);
-      for (int c = item.y; c < item.z; ++c) {
-        const bool more = c + 1 < item.z;
-        if (more) fetch(c + 1, nxt);
-#pragma unroll (kUnrollK)
-        for (int q = 0; q < K; ++q) {
-          if (!((cur.pres >> q) & 1u)) continue;
-          uint64_t mm[WT];
-          cur.row(q, mm);
-          S.insert(mm, proof_key<WT>(mm, pc), 0);
-        }
-        if (more) cur = nxt;
-      }
-    } else {
-      // conj fold, normalised after every step (candidate order ra*kb + rb)
-      TagRows<K, WT> A, Bt, An, Bn;
-      if (item.y < item.z) {
-        A.load(a.ops[0], a.B, b, rec_row(a, item.y, 0));
-        Bt.load(a.ops[1], a.B, b, rec_row(a, item.y, 1));
-      }
-      for (int c = item.y; c < item.z; ++c) {
-        const bool more = c + 1 < item.z;
-        if (more) {
-          An.load(a.ops[0], a.B, b, rec_row(a, c + 1, 0));
-          Bn.load(a.ops[1], a.B, b, rec_row(a, c + 1, 1));
-        }
-        TopK<K, WT> T;
-        T.clear();
-#pragma unroll (kUnrollK)
-        for (int qa = 0; qa < K; ++qa) {
-          if (!((A.pres >> qa) & 1u)) continue;
-          uint64_t ma[WT];
-          A.row(qa, ma);
-#pragma unroll (kUnrollK)
-          for (int qb = 0; qb < K; ++qb) {
-            if (!((Bt.pres >> qb) & 1u)) continue;
-            uint64_t mm[WT];
-            Bt.row(qb, mm);
-#pragma unroll
-            for (int w = 0; w < WT; ++w) mm[w] |= ma[w];
-            T.insert(mm, proof_key<WT>(mm, pc), 0);
-          }
-        }
-#pragma unroll 1
-        for (int i = 2; i < a.arity; ++i) {
-          TagRows<K, WT> Ci;
-          Ci.load(a.ops[i], a.B, b, rec_row(a, c, i));
-          TopK<K, WT> U;
-          U.clear();
-#pragma unroll (kUnrollK)
-          for (int qa = 0; qa < K; ++qa) {
-            if (qa >= T.n) break;
-            uint64_t ma[WT];
-            double ka;
-            T.get(qa, ma, ka);
-#pragma unroll (kUnrollK)
-            for (int qb = 0; qb < K; ++qb) {
-              if (!((Ci.pres >> qb) & 1u)) continue;
-              uint64_t mm[WT];
-              Ci.row(qb, mm);
-#pragma unroll
-              for (int w = 0; w < WT; ++w) mm[w] |= ma[w];
-              U.insert(mm, proof_key<WT>(mm, pc), 0);
-            }
-          }
-          T = U;
-        }
-#pragma unroll (kUnrollK)
-        for (int q = 0; q < K; ++q) {
-          if (q >= T.n) break;
-          uint64_t mm[WT];
-          double kk;
-          T.get(q, mm, kk);
-          S.insert(mm, kk, 0);  // same mask, same p -> same key as a recomputation
-        }
-        if (more) {
-          A = An;
-          Bt = Bn;
-        }
+  if (a.sched != nullptr) {
+    // dynamic: every warp takes the next item of its 32-sample column from a counter, so
+    // the CTAs of one resident wave stay busy until the column's items run out
+    int* ctr = a.sched + blockIdx.x;
+    for (;;) {
+      int it = 0;
+      if (lane == 0) it = atomicAdd(ctr, 1);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (it >= a.n_items) break;
+      apply_item<K, WT>(a, it, b, b0, bval, pc);
+    }
+    // the last CTA out re-zeroes the counters for the next launch that uses the buffer
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned total = gridDim.x * gridDim.y;
+      if (atomicAdd(reinterpret_cast<unsigned*>(a.sched + gridDim.x), 1u) == total - 1) {
+        for (unsigned x = 0; x < gridDim.x; ++x) a.sched[x] = 0;
+        a.sched[gridDim.x] = 0;
       }
     }
-    if (bval) {
-      uint64_t* om;
-      uint8_t* opr;
-      if (item.w < 0) {
-        om = a.out_m + (size_t)item.x * K * a.W * a.B;
-        opr = a.out_p + (size_t)item.x * K * a.B;
-      } else {
-        om = a.scr_m + (size_t)item.w * K * a.W * a.B;
-        opr = a.scr_p + (size_t)item.w * K * a.B;
-      }
-#pragma unroll
-      for (int q = 0; q < K; ++q) {
-        const bool live = q < S.n;
-        opr[(size_t)q * a.B + b0] = live ? 1 : 0;
-#pragma unroll
-        for (int w = 0; w < WT; ++w)
-          if (w < a.W) om[((size_t)q * a.W + w) * a.B + b0] = live ? S.m[q][w] : 0ull;
-      }
-    }
+    return;
   }
+  // static: CTAs stride over the work blocks; the probability tile is staged once per CTA
+  for (int bk = blockIdx.y; bk < a.n_blk; bk += gridDim.y) {
+    const int it0 = __ldg(a.blk + bk), it1 = __ldg(a.blk + bk + 1);
+    for (int it = it0 + warp; it < it1; it += nwarps) apply_item<K, WT>(a, it, b, b0, bval, pc);
   }
 }
 
@@ -372,8 +400,14 @@ static int launch_apply_kw(const DtkpK& k, int n_blocks, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dtkp_apply<K, WT>, 128, smem);
   const int64_t gx = ceil_div(k.B, kWarp);
-  const int64_t resident = (int64_t)std::max(occ, 1) * std::max(sms, 1) * SG_DTKP_WAVES;
-  const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(n_blocks, ceil_div(resident, gx)));
+  const int64_t resident = (int64_t)std::max(occ, 1) * std::max(sms, 1) * (k.sched ? 1 : SG_DTKP_WAVES);
+  int gy;
+  if (k.sched != nullptr) {
+    // dynamic item schedule: one resident wave, no more warps than items
+    gy = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(resident, gx), ceil_div((int64_t)k.n_items, 4)));
+  } else {
+    gy = (int)std::max<int64_t>(1, std::min<int64_t>(n_blocks, ceil_div(resident, gx)));
+  }
   DtkpK kk = k;
   kk.n_blk = n_blocks;
   dim3 grid((unsigned)gx, gy);

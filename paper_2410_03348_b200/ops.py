@@ -397,6 +397,26 @@ def index_tensor(indices, device) -> torch.Tensor:
 
 
 # ------------------------------------------------------------------------ DTKP
+_SCHED: "dict[tuple, torch.Tensor]" = {}
+_SCHED_RETIRED: "list[torch.Tensor]" = []  # outgrown buffers a captured graph may still use
+DTKP_DYNAMIC = True  # False: the static block partition (sched = NULL), kept for tests
+
+
+def dtkp_sched(device, n: int) -> torch.Tensor:
+    """Zeroed work counters for sg_dtkp_apply's dynamic item schedule, one buffer per
+    (device, stream): launches on one stream are ordered, and every launch leaves the
+    counters zero again.  A buffer first made during CUDA-graph capture is zeroed by a
+    captured memset, which is harmless on replay."""
+    key = (torch.device(device), N.stream_ptr(device))
+    t = _SCHED.get(key)
+    if t is None or t.numel() < n:
+        if t is not None:
+            _SCHED_RETIRED.append(t)
+        t = torch.zeros(max(n, 64), device=device, dtype=torch.int32)
+        _SCHED[key] = t
+    return t
+
+
 def dtkp_apply(kplan_host, dseg, dmerge, operands, tail, K: int, W: int, I: int, B: int, p: torch.Tensor,
                arity: int):
     """Run sg_dtkp_apply; operands are (member, present) pairs with full batch B."""
@@ -432,6 +452,7 @@ def dtkp_apply(kplan_host, dseg, dmerge, operands, tail, K: int, W: int, I: int,
         d.scratch_member = scr_m.data_ptr()
         d.scratch_present = scr_p.data_ptr()
         d.merge = dmerge.struct(B)
+    d.sched = dtkp_sched(dev, -(-B // 32) + 1).data_ptr() if DTKP_DYNAMIC else None
     rc = _lib().sg_dtkp_apply(ctypes.byref(d), N.stream_ptr(dev))
     N.check(rc, "sg_dtkp_apply")
     return out_m, out_p

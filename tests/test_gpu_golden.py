@@ -44,3 +44,26 @@ def test_gpu_matches_oracle_fresh_inputs(cuda, name):
     if "member" in ref:
         np.testing.assert_array_equal(got["member"], ref["member"])
         np.testing.assert_array_equal(got["present"], ref["present"])
+
+
+@pytest.mark.parametrize("name", ["dtkp_hwf5", "dtkp_path_k5"])
+def test_dtkp_dynamic_and_static_schedules_agree(cuda, name):
+    """The apply's dynamic item schedule (per-column work counters) and the static block
+    partition produce the same proofs bit for bit; the counters are left zeroed."""
+    import torch
+
+    from paper_2410_03348_b200 import ops
+
+    prov, k, prog, syms_fn, make, seed = G.CASES[name]
+    inputs = make(np.random.default_rng(4242 + seed))
+    try:
+        ops.DTKP_DYNAMIC = False
+        static = run_gpu(name, inputs)
+    finally:
+        ops.DTKP_DYNAMIC = True
+    dynamic = run_gpu(name, inputs)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(dynamic["member"], static["member"])
+    np.testing.assert_array_equal(dynamic["present"], static["present"])
+    np.testing.assert_array_equal(dynamic["probs"], static["probs"])
+    assert ops._SCHED and all(int(t.abs().sum()) == 0 for t in ops._SCHED.values())
