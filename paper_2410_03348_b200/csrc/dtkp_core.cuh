@@ -8,6 +8,9 @@
 #ifndef SG_DTKP_WAVES  // resident waves of apply CTAs per launch (each strides over work blocks)
 #define SG_DTKP_WAVES 3
 #endif
+#ifndef SG_DTKP_MINB  // minimum resident apply CTAs per SM (register cap)
+#define SG_DTKP_MINB 1
+#endif
 #ifndef SG_DTKP_UNROLL_K
 #define SG_DTKP_UNROLL_K 4
 #endif
@@ -224,13 +227,16 @@ __device__ __forceinline__ int rec_row(const DtkpK& a, int c, int i) { return __
 
 // One work item (an output segment, or a piece of a split one) for one sample: stream its
 // records through the top-k set and write the retained rows.
-template <int K, int WT>
+// AR: 1 = union / group_disj streaming, 2 = binary conj fold, 0 = conj fold of >= 3
+// operands.  Each is its own kernel, so the streaming kernel does not carry the
+// conj fold's registers (occupancy) or code (instruction cache).
+template <int K, int WT, int AR>
 __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, int64_t b0, bool bval, const PCol& pc) {
   constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
   const int4 item = __ldg(reinterpret_cast<const int4*>(a.items) + it);
   TopK<K, WT> S;
   S.clear();
-  if (a.arity == 1) {
+  if constexpr (AR == 1) {
     // group_disj / union / merge: stream the stored rows of every record, in order;
     // the next record's rows are loaded before the current one is ranked.
     TagRows<K, WT> cur, nxt;
@@ -285,7 +291,7 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
         }
       }
 #pragma unroll 1
-      for (int i = 2; i < a.arity; ++i) {
+      for (int i = 2; AR != 2 && i < a.arity; ++i) {
         TagRows<K, WT> Ci;
         Ci.load(a.ops[i], a.B, b, rec_row(a, c, i));
         TopK<K, WT> U;
@@ -343,8 +349,8 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
   }
 }
 
-template <int K, int WT>
-__global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
+template <int K, int WT, int AR>
+__global__ void __launch_bounds__(128, SG_DTKP_MINB) k_dtkp_apply(const DtkpK a) {
   extern __shared__ __align__(16) unsigned char ptile_raw[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -364,7 +370,7 @@ __global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
       if (lane == 0) it = atomicAdd(ctr, 1);
       it = __shfl_sync(0xffffffffu, it, 0);
       if (it >= a.n_items) break;
-      apply_item<K, WT>(a, it, b, b0, bval, pc);
+      apply_item<K, WT, AR>(a, it, b, b0, bval, pc);
     }
     // the last CTA out re-zeroes the counters for the next launch that uses the buffer
     __syncthreads();
@@ -381,24 +387,24 @@ __global__ void __launch_bounds__(128) k_dtkp_apply(const DtkpK a) {
   // static: CTAs stride over the work blocks; the probability tile is staged once per CTA
   for (int bk = blockIdx.y; bk < a.n_blk; bk += gridDim.y) {
     const int it0 = __ldg(a.blk + bk), it1 = __ldg(a.blk + bk + 1);
-    for (int it = it0 + warp; it < it1; it += nwarps) apply_item<K, WT>(a, it, b, b0, bval, pc);
+    for (int it = it0 + warp; it < it1; it += nwarps) apply_item<K, WT, AR>(a, it, b, b0, bval, pc);
   }
 }
 
-template <int K, int WT>
-static int launch_apply_kw(const DtkpK& k, int n_blocks, cudaStream_t st) {
+template <int K, int WT, int AR>
+static int launch_apply_kwa(const DtkpK& k, int n_blocks, cudaStream_t st) {
   const int mode = ptile_mode(k.I);
   if (mode == 0) return (int)cudaErrorNotSupported;
   const size_t smem = (size_t)k.I * kWarp * (mode == 2 ? sizeof(double) : sizeof(float));
   {
-    cudaError_t e = ensure_smem((const void*)k_dtkp_apply<K, WT>, smem);
+    cudaError_t e = ensure_smem((const void*)k_dtkp_apply<K, WT, AR>, smem);
     if (e != cudaSuccess) return (int)e;
   }
   // one resident wave of CTAs (x: 32-sample columns, y: strided over the work blocks)
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dtkp_apply<K, WT>, 128, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dtkp_apply<K, WT, AR>, 128, smem);
   const int64_t gx = ceil_div(k.B, kWarp);
   const int64_t resident = (int64_t)std::max(occ, 1) * std::max(sms, 1) * (k.sched ? 1 : SG_DTKP_WAVES);
   int gy;
@@ -412,9 +418,16 @@ static int launch_apply_kw(const DtkpK& k, int n_blocks, cudaStream_t st) {
   kk.n_blk = n_blocks;
   dim3 grid((unsigned)gx, gy);
   count_launch();
-  k_dtkp_apply<K, WT><<<grid, 128, smem, st>>>(kk);
+  k_dtkp_apply<K, WT, AR><<<grid, 128, smem, st>>>(kk);
   SG_LAUNCH_CHECK();
   return 0;
+}
+
+template <int K, int WT>
+static int launch_apply_kw(const DtkpK& k, int n_blocks, cudaStream_t st) {
+  if (k.arity == 1) return launch_apply_kwa<K, WT, 1>(k, n_blocks, st);
+  if (k.arity == 2) return launch_apply_kwa<K, WT, 2>(k, n_blocks, st);
+  return launch_apply_kwa<K, WT, 0>(k, n_blocks, st);
 }
 
 template <int K>
