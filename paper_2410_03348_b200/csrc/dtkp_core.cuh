@@ -8,8 +8,8 @@
 #ifndef SG_DTKP_WAVES  // resident waves of apply CTAs per launch (each strides over work blocks)
 #define SG_DTKP_WAVES 3
 #endif
-#ifndef SG_DTKP_MINB  // minimum resident apply CTAs per SM (register cap)
-#define SG_DTKP_MINB 1
+#ifndef SG_DTKP_MINB  // > 0 overrides the per-variant register policy (dtkp_min_blocks)
+#define SG_DTKP_MINB 0
 #endif
 #ifndef SG_DTKP_UNROLL_K
 #define SG_DTKP_UNROLL_K 4
@@ -349,8 +349,17 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
   }
 }
 
+// Resident CTAs per SM the register allocator is asked for: the highest that compiles
+// without spills at K <= 3 / K <= 5 and W <= 2 (ptxas -v), else whatever the kernel needs.
+__host__ __device__ constexpr int dtkp_min_blocks(int K, int WT, int AR) {
+  return SG_DTKP_MINB > 0 ? SG_DTKP_MINB
+         : (WT <= 2 && K <= 3) ? (AR == 1 ? 5 : AR == 2 ? 4 : 1)
+         : (WT <= 2 && K <= 5 && AR == 1) ? 4
+         : 1;
+}
+
 template <int K, int WT, int AR>
-__global__ void __launch_bounds__(128, SG_DTKP_MINB) k_dtkp_apply(const DtkpK a) {
+__global__ void __launch_bounds__(128, dtkp_min_blocks(K, WT, AR)) k_dtkp_apply(const DtkpK a) {
   extern __shared__ __align__(16) unsigned char ptile_raw[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
