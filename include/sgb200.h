@@ -119,6 +119,31 @@ int sg_damp_apply_bwd(const sg_damp_plan* plan, const sg_rows* inputs,
 int sg_damp_rows_add(const sg_rows A, const int32_t* ia, const sg_rows Bm, const int32_t* ib,
                      int64_t n_rows, int64_t B, int32_t clamp01, float* out, sg_stream_t stream);
 
+/* ---- max-product apply (the north star's "max/DAMP variant") ----------------------
+ * conj = product (left to right), disj = max over the output's records with the gradient
+ * to the FIRST maximal record (tensor.py:319-325 reduce "max"); empty output = 0;
+ * optional clamp01 after the max (gradient passes through).  Records of output s are
+ * recs[seg_off[s] .. seg_off[s+1]) in first-derivation order; rec_out[c] is the output
+ * of record c; in_off[k] / in_recs[k] list, per row of input k, the records that use it
+ * (ascending).  The backward writes (overwrites) grad_in[k] for every non-NULL entry. */
+typedef struct sg_maxprod_plan {
+  int32_t arity;
+  int32_t n_out;
+  int32_t n_recs;
+  int32_t sizes[SG_MAX_ARITY];
+  const int32_t* seg_off;                /* [n_out + 1]        */
+  const int32_t* recs;                   /* [n_recs][arity]    */
+  const int32_t* rec_out;                /* [n_recs]           */
+  const int32_t* in_off[SG_MAX_ARITY];   /* [sizes[k] + 1]     */
+  const int32_t* in_recs[SG_MAX_ARITY];  /* [n_recs]           */
+} sg_maxprod_plan;
+
+/* out, argmax: contiguous [n_out][B]. */
+int sg_maxprod_fwd(const sg_maxprod_plan* plan, const sg_rows* inputs, int64_t B, int32_t clamp01, float* out,
+                   int32_t* argmax, sg_stream_t stream);
+int sg_maxprod_bwd(const sg_maxprod_plan* plan, const sg_rows* inputs, int64_t B, const int32_t* argmax,
+                   sg_rows grad_out, const sg_rows* grad_in, sg_stream_t stream);
+
 /* ---- fused Toeplitz apply chains ---------------------------------------------------
  * v_i = clamp01(v_{i-1} (*) S_i), i = 1..m — a left fold of Toeplitz applies (every Sum-N
  * fold step) as ONE forward and ONE backward launch; per-step arithmetic is the one of

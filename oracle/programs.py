@@ -48,12 +48,12 @@ class ODist:
 
     @property
     def batch(self):
-        return self.tag.shape[0] if self.ctx.prov == "damp" else self.tag[0].shape[0]
+        return self.tag.shape[0] if self.ctx.prov in ("damp", "max") else self.tag[0].shape[0]
 
     def filter(self, pred):
         keep = [i for i, s in enumerate(self.symbols) if pred(s)]
         syms = [self.symbols[i] for i in keep]
-        if self.ctx.prov == "damp":
+        if self.ctx.prov in ("damp", "max"):
             val = self.tag[:, keep]
             return ODist(self.ctx, syms, val, self.ctx._node("gather", (self.node, keep, self.tag.shape[1]), val))
         return ODist(self.ctx, syms, A.dtkp_gather(self.tag, keep))
@@ -64,13 +64,13 @@ def make_distribution(ctx: OContext, probs, symbols) -> ODist:
     start = ctx.width
     ctx.blocks.append(probs)
     ctx.width += probs.shape[1]
-    if ctx.prov == "damp":
+    if ctx.prov in ("damp", "max"):
         return ODist(ctx, symbols, probs, ctx._node("input", len(ctx.blocks) - 1, probs))
     return ODist(ctx, symbols, A.dtkp_input_tags(start, probs.shape[1], ctx.width, probs.shape[0], ctx.k))
 
 
 def _empty(ctx, batch):
-    if ctx.prov == "damp":
+    if ctx.prov in ("damp", "max"):
         v = np.zeros((batch, 0))
         return ODist(ctx, (), v, ctx._node("const", None, v))
     return ODist(ctx, (), (np.zeros((batch, 0, ctx.k, ctx.width), np.uint8), np.zeros((batch, 0, ctx.k), np.uint8)))
@@ -87,6 +87,10 @@ def apply_if(f, cond, *dists) -> ODist:
     if ctx.prov == "damp":
         val = A.damp_apply([d.tag for d in dists], combos, out_idx, len(syms))
         node = ctx._node("apply", ([d.node for d in dists], combos, out_idx, [d.tag for d in dists]), val)
+        return ODist(ctx, syms, val, node)
+    if ctx.prov == "max":
+        val, arg = A.max_apply([d.tag for d in dists], combos, out_idx, len(syms))
+        node = ctx._node("apply_max", ([d.node for d in dists], combos, arg, [d.tag for d in dists]), val)
         return ODist(ctx, syms, val, node)
     tags = [A.pad_width(d.tag, ctx.width) for d in dists]
     return ODist(ctx, syms, A.dtkp_apply(tags, combos, out_idx, len(syms), ctx.p(), ctx.k))
@@ -118,12 +122,19 @@ def union(d1: ODist, d2: ODist) -> ODist:
         ib = [(g[-1] - n1) if g[-1] >= n1 else -1 for g in groups]
         val = A.damp_union(d1.tag, d2.tag, ia, ib)
         return ODist(ctx, symbols, val, ctx._node("union", (d1.node, d2.node, ia, ib, d1.tag, d2.tag), val))
+    if ctx.prov == "max":
+        n1 = len(d1.symbols)
+        ia = [g[0] if g[0] < n1 else -1 for g in groups]
+        ib = [(g[-1] - n1) if g[-1] >= n1 else -1 for g in groups]
+        val, which = A.max_union(d1.tag, d2.tag, ia, ib)
+        return ODist(ctx, symbols, val,
+                     ctx._node("union_max", (d1.node, d2.node, ia, ib, d1.tag, d2.tag, which), val))
     both = A.dtkp_concat([A.pad_width(d1.tag, ctx.width), A.pad_width(d2.tag, ctx.width)])
     return ODist(ctx, symbols, A.dtkp_group_disj(both, groups, ctx.p(), ctx.k))
 
 
 def get_probs(d: ODist) -> np.ndarray:
-    if d.ctx.prov == "damp":
+    if d.ctx.prov in ("damp", "max"):
         return d.tag
     return A.dtkp_probs(A.pad_width(d.tag, d.ctx.width), d.ctx.p())
 
@@ -157,6 +168,25 @@ def grad_inputs(d: ODist, g: np.ndarray):
             parents, combos, out_idx, vals = payload
             for parent, gi in zip(parents, A.damp_apply_grad(vals, combos, out_idx, gn)):
                 grads[parent] = grads.get(parent, 0) + gi
+        elif kind == "apply_max":
+            parents, combos, arg, vals = payload
+            for parent, gi in zip(parents, A.max_apply_grad(vals, combos, arg, gn)):
+                grads[parent] = grads.get(parent, 0) + gi
+        elif kind == "union_max":
+            n1_node, n2_node, ia, ib, a, b, which = payload
+            ga = np.zeros((gn.shape[0], a.shape[1]))
+            gb = np.zeros((gn.shape[0], b.shape[1]))
+            for r, (i, j) in enumerate(zip(ia, ib)):
+                if i >= 0:
+                    ga[:, i] += np.where(which[:, r] == 0, gn[:, r], 0.0)
+                if j >= 0:
+                    gb[:, j] += np.where(which[:, r] == 1, gn[:, r], 0.0)
+            if a.shape[0] == 1 and ga.shape[0] > 1:
+                ga = ga.sum(axis=0, keepdims=True)
+            if b.shape[0] == 1 and gb.shape[0] > 1:
+                gb = gb.sum(axis=0, keepdims=True)
+            grads[n1_node] = grads.get(n1_node, 0) + ga
+            grads[n2_node] = grads.get(n2_node, 0) + gb
         elif kind == "gather":
             parent, keep, n = payload
             buf = np.zeros((gn.shape[0], n))

@@ -39,6 +39,7 @@ def _units():
         ("damp.o", CSRC / "damp.cu", []),
         ("chain.o", CSRC / "chain.cu", []),
         ("dtkp.o", CSRC / "dtkp.cu", []),
+        ("maxprod.o", CSRC / "maxprod.cu", []),
     ]
     for k in range(1, 9):
         units.append((f"dtkp_apply_k{k}.o", CSRC / "dtkp_apply_k.cu", [f"-DSG_DTKP_K={k}"]))

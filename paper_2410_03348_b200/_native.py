@@ -101,6 +101,20 @@ class SgDtkpApplyDesc(Structure):
     ]
 
 
+class SgMaxprodPlan(Structure):
+    _fields_ = [
+        ("arity", c_int32),
+        ("n_out", c_int32),
+        ("n_recs", c_int32),
+        ("sizes", c_int32 * MAX_ARITY),
+        ("seg_off", c_void_p),
+        ("recs", c_void_p),
+        ("rec_out", c_void_p),
+        ("in_off", c_void_p * MAX_ARITY),
+        ("in_recs", c_void_p * MAX_ARITY),
+    ]
+
+
 # (name, restype, argtypes) of every exported entry point in include/sgb200.h
 EXPORTS = {
     "sg_version": (c_int32, []),
@@ -129,6 +143,10 @@ EXPORTS = {
     "sg_nll_fwd": (c_int32, [SgRows, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "sg_nll_bwd": (c_int32, [SgRows, c_int64, c_int64, c_void_p, c_void_p, c_void_p, SgRows, c_void_p]),
     "sg_nll_fwd_rowsum": (c_int32, [SgRows, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sg_maxprod_fwd": (c_int32, [POINTER(SgMaxprodPlan), POINTER(SgRows), c_int64, c_int32, c_void_p, c_void_p,
+                                 c_void_p]),
+    "sg_maxprod_bwd": (c_int32, [POINTER(SgMaxprodPlan), POINTER(SgRows), c_int64, c_void_p, SgRows, POINTER(SgRows),
+                                 c_void_p]),
     "sg_rows_gather": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "sg_dtkp_apply": (c_int32, [POINTER(SgDtkpApplyDesc), c_void_p]),
     "sg_dtkp_probs_fwd": (

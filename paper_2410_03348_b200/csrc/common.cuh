@@ -29,6 +29,24 @@ constexpr int kWarp = 32;
 
 __device__ __forceinline__ float clamp01(float x) { return fminf(fmaxf(x, 0.0f), 1.0f); }
 
+// A strided (rows, B) fp32 operand: row stride and sample stride (0 = broadcast sample).
+struct Rows {
+  const float* p;
+  int64_t sr;  // stride between rows (symbols)
+  int64_t sb;  // stride between samples (0 = broadcast)
+  __device__ __forceinline__ float ld(int64_t r, int64_t b) const { return __ldg(p + r * sr + b * sb); }
+};
+
+struct WRows {
+  float* p;
+  int64_t sr;
+  int64_t sb;
+  __device__ __forceinline__ void st(int64_t r, int64_t b, float v) const { p[r * sr + b * sb] = v; }
+};
+
+__host__ __forceinline__ Rows rows_of(const sg_rows& r) { return Rows{r.ptr, r.stride_row, r.stride_b}; }
+__host__ __forceinline__ WRows wrows_of(const sg_rows& r) { return WRows{r.ptr, r.stride_row, r.stride_b}; }
+
 // Load one record of RW int32 words (RW in {1,2,4,8}); the address is warp-uniform.
 template <int RW>
 struct Rec {

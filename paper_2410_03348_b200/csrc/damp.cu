@@ -28,22 +28,6 @@
 
 namespace sg {
 
-struct Rows {
-  const float* p;
-  int64_t sr;  // stride between rows (symbols)
-  int64_t sb;  // stride between samples (0 = broadcast)
-  __device__ __forceinline__ float ld(int64_t r, int64_t b) const { return __ldg(p + r * sr + b * sb); }
-};
-
-struct WRows {
-  float* p;
-  int64_t sr;
-  int64_t sb;
-  __device__ __forceinline__ void st(int64_t r, int64_t b, float v) const { p[r * sr + b * sb] = v; }
-};
-
-__host__ __forceinline__ Rows rows_of(const sg_rows& r) { return Rows{r.ptr, r.stride_row, r.stride_b}; }
-__host__ __forceinline__ WRows wrows_of(const sg_rows& r) { return WRows{r.ptr, r.stride_row, r.stride_b}; }
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }

@@ -148,6 +148,47 @@ class DampApply(torch.autograd.Function):
         return (None, None, *grads)
 
 
+class MaxProdApply(torch.autograd.Function):
+    """Max-product apply (the north star's max variant): per output the max over its
+    records of the product of the inputs, gradient to the first maximal record
+    (tensor.py:319-325); sg_maxprod_fwd / sg_maxprod_bwd."""
+
+    @staticmethod
+    def forward(ctx, kplan: KernelPlan, B: int, *inputs):
+        dev = inputs[0].device
+        for i, x in enumerate(inputs):
+            _check_operand(x, f"max apply input {i}")
+        s = kplan.device(dev).maxprod_struct()
+        out = torch.empty((kplan.n_out, B), device=dev, dtype=F32)
+        arg = torch.empty((kplan.n_out, B), device=dev, dtype=torch.int32)
+        rc = _lib().sg_maxprod_fwd(ctypes.byref(s), N.rows_array(inputs), B, int(kplan.clamp), N.ptr(out),
+                                   N.ptr(arg), N.stream_ptr(dev))
+        N.check(rc, "sg_maxprod_fwd")
+        ctx.kplan = kplan
+        ctx.B = B
+        ctx.save_for_backward(arg, *inputs)
+        ctx.mark_non_differentiable(arg)
+        return out
+
+    @staticmethod
+    def backward(ctx, g: torch.Tensor):
+        arg, *inputs = ctx.saved_tensors
+        kplan: KernelPlan = ctx.kplan
+        grads = [torch.empty_like(x) if ctx.needs_input_grad[2 + i] else None for i, x in enumerate(inputs)]
+        if any(gr is not None for gr in grads):
+            dev = g.device
+            s = kplan.device(dev).maxprod_struct()
+            rc = _lib().sg_maxprod_bwd(ctypes.byref(s), N.rows_array(inputs), ctx.B, N.ptr(arg), N.rows(g),
+                                       N.rows_array(grads), N.stream_ptr(dev))
+            N.check(rc, "sg_maxprod_bwd")
+        return (None, None, *grads)
+
+
+def maxprod_apply(kplan: KernelPlan, inputs, B: int) -> torch.Tensor:
+    inputs = [expand_batch(x, B) for x in inputs]
+    return MaxProdApply.apply(kplan, B, *inputs)
+
+
 def damp_apply(kplan: KernelPlan, inputs, B: int) -> torch.Tensor:
     inputs = [expand_batch(x, B) for x in inputs]
     return DampApply.apply(kplan, B, *inputs)

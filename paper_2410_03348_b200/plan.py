@@ -494,6 +494,22 @@ class KernelPlan:
             self._dtkp_host = HostSegsum(off, self.records[order], DTKP_MAX_ITEM)
         return self._dtkp_host
 
+    def maxprod_host(self) -> "dict[str, np.ndarray]":
+        """CSR arrays of the max-product apply (sg_maxprod_plan): records grouped by output
+        in first-derivation order, and per input the records using each row."""
+        h = getattr(self, "_maxprod_host", None)
+        if h is None:
+            order, off = csr(self.out_idx, self.n_out)
+            recs = self.records[order]
+            h = {"seg_off": off.astype(np.int32), "recs": np.ascontiguousarray(recs, dtype=np.int32),
+                 "rec_out": np.ascontiguousarray(self.out_idx[order], dtype=np.int32)}
+            for k, n in enumerate(self.sizes):
+                o, ko = csr(recs[:, k], n)
+                h[f"in_off{k}"] = ko.astype(np.int32)
+                h[f"in_recs{k}"] = o.astype(np.int32)
+            self._maxprod_host = h
+        return h
+
     def device(self, device) -> "DevicePlan":
         key = torch.device(device)
         dp = self._dev.get(key)
@@ -544,6 +560,25 @@ class DevicePlan:
                 mh.items[:, 0] = host.split[:, 0]
                 self._dtkp_merge = DeviceSegsum(mh, self.device, True, 16, target_ctas=148 * 8)
         return self._dtkp, self._dtkp_merge
+
+    def maxprod_struct(self) -> N.SgMaxprodPlan:
+        d = getattr(self, "_maxprod", None)
+        if d is None:
+            d = {k: torch.from_numpy(v).to(self.device) for k, v in self.kp.maxprod_host().items()}
+            self._maxprod = d
+        kp = self.kp
+        s = N.SgMaxprodPlan()
+        s.arity = kp.arity
+        s.n_out = kp.n_out
+        s.n_recs = len(kp.out_idx)
+        for i, n in enumerate(kp.sizes):
+            s.sizes[i] = n
+            s.in_off[i] = d[f"in_off{i}"].data_ptr()
+            s.in_recs[i] = d[f"in_recs{i}"].data_ptr() if d[f"in_recs{i}"].numel() else None
+        s.seg_off = d["seg_off"].data_ptr()
+        s.recs = d["recs"].data_ptr() if d["recs"].numel() else None
+        s.rec_out = d["rec_out"].data_ptr() if d["rec_out"].numel() else None
+        return s
 
     def damp_struct(self, B: int, need_bwd=()) -> N.SgDampPlan:
         kp = self.kp

@@ -26,6 +26,7 @@ __all__ = [
     "ProvenanceError",
     "InputRegistry",
     "Damp",
+    "DampMax",
     "DtkpAm",
     "DampTags",
     "DtkpTags",
@@ -313,6 +314,74 @@ class Damp:
                 ops.index_map(uplan.ib, b.count, dev), True,
             )
         )
+
+
+class DampMax(Damp):
+    """Max-product probabilities: the north star's "max/DAMP variant" of kernel (1).
+
+    There is no max provenance in the reference, so it is assembled from the
+    reference's primitives: conj is the DAMP product (provenance.py:236), disj is
+    tensor.py's reduce "max" (tensor.py:319-325: gradient to the FIRST maximal entry, here
+    the earliest record in first-derivation order), followed by DAMP's clamp01 (pass-through
+    gradient, tensor.py:287).  Every operator runs on sg_maxprod_fwd / sg_maxprod_bwd;
+    tags are the same symbol-major fp32 [n][b] as Damp's."""
+
+    name = "max"
+
+    def gather(self, tags: DampTags, indices) -> DampTags:
+        rng = _as_range(indices)
+        if rng is not None:
+            return _damp(tags.sm[rng[0]:rng[1]])
+        return _damp(ops.maxprod_apply(ops.gather_plan(indices, tags.count), [tags.sm], tags.batch))
+
+    def conj(self, a: DampTags, b: DampTags) -> DampTags:
+        n = max(a.count, b.count)
+        B = max(a.batch, b.batch)
+        ia = np.arange(n) if a.count == n else np.zeros(n, dtype=np.int64)
+        ib = np.arange(n) if b.count == n else np.zeros(n, dtype=np.int64)
+        kp = KernelPlan(np.stack([ia, ib], axis=1), np.arange(n), n, (a.count, b.count), clamp=False)
+        return _damp(ops.maxprod_apply(kp, [a.sm, b.sm], B))
+
+    def _pairwise_max(self, a: DampTags, b: DampTags, ia, ib) -> DampTags:
+        """out[s] = clamp01(max(a[ia[s]], b[ib[s]])), -1 = absent; ties go to a."""
+        B = max(a.batch, b.batch)
+        ia = np.asarray(ia, dtype=np.int64)
+        ib = np.asarray(ib, dtype=np.int64)
+        recs, outs = [], []
+        for s in range(len(ia)):
+            if ia[s] >= 0:
+                recs.append(ia[s])
+                outs.append(s)
+            if ib[s] >= 0:
+                recs.append(a.count + ib[s])
+                outs.append(s)
+        kp = KernelPlan(np.asarray(recs, dtype=np.int32).reshape(-1, 1), np.asarray(outs, dtype=np.int32), len(ia),
+                        (a.count + b.count,), clamp=True)
+        both = torch.cat([ops.expand_batch(a.sm, B), ops.expand_batch(b.sm, B)], dim=0)
+        return _damp(ops.maxprod_apply(kp, [both], B))
+
+    def disj(self, a: DampTags, b: DampTags) -> DampTags:
+        n = max(a.count, b.count)
+        ia = np.arange(n) if a.count == n else np.zeros(n, dtype=np.int64)
+        ib = np.arange(n) if b.count == n else np.zeros(n, dtype=np.int64)
+        return self._pairwise_max(a, b, ia, ib)
+
+    def group_disj(self, tags: DampTags, groups) -> DampTags:
+        recs = np.asarray([c for g in groups for c in g], dtype=np.int32).reshape(-1, 1)
+        out = np.asarray([s for s, g in enumerate(groups) for _ in g], dtype=np.int32)
+        kp = KernelPlan(recs, out, len(groups), (tags.count,), clamp=True)
+        return _damp(ops.maxprod_apply(kp, [tags.sm], tags.batch))
+
+    def placed(self, tags: DampTags, placement: np.ndarray) -> DampTags:
+        return _damp(ops.maxprod_apply(ops.gather_plan(_placement_src(placement), tags.count), [tags.sm],
+                                       tags.batch))
+
+    def apply_plan(self, tags_list, plan: SymbolPlan, batch: int) -> DampTags:
+        """gather -> product fold -> max bucket (+clamp) in one sg_maxprod_fwd launch."""
+        return _damp(ops.maxprod_apply(plan.kernel_plan(), [t.sm for t in tags_list], batch))
+
+    def union_tags(self, a: DampTags, b: DampTags, uplan) -> DampTags:
+        return self._pairwise_max(a, b, uplan.ia, uplan.ib)
 
 
 def _as_range(indices):
@@ -687,4 +756,6 @@ def provenance_from_name(name: str, k: int = 1):
         return Damp()
     if name == "dtkp":
         return DtkpAm(k)
-    raise ProvenanceError(f"unknown provenance {name!r} (expected damp or dtkp)")
+    if name in ("max", "damp-max"):
+        return DampMax()
+    raise ProvenanceError(f"unknown provenance {name!r} (expected damp, dtkp or max)")

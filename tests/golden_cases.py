@@ -139,6 +139,19 @@ CASES = {
     "dtkp_clutrr_k3_e5": ("dtkp", 3, _clutrr, lambda P: [clutrr_facts(5, ("father", "mother", "son", "daughter",
                                                                           "brother", "sister", "husband", "wife"))],
                           lambda rng: [rng.uniform(0.05, 0.95, size=(2, 32)).astype(np.float32).astype(np.float64)], 22),
+    # the max-product ("max/DAMP") variant: fixtures from the reference's Tensor primitives
+    # (tools/make_golden_max.py), since the reference has no max provenance
+    "max_sum2": ("max", None, _sum, lambda P: [DIGITS] * 2, _digit_inputs(2, 16), 30),
+    "max_sum4": ("max", None, _sum, lambda P: [DIGITS] * 4, _digit_inputs(4, 8), 31),
+    "max_mod_cond_a2": ("max", None, _mod_cond, lambda P: [list(range(9))] * 2, _sized_inputs(2, 9, 8), 32),
+    "max_mod_a3": ("max", None, _mod3, lambda P: [list(range(6))] * 3, _sized_inputs(3, 6, 8), 33),
+    "max_bcast_reuse": ("max", None, _bcast_reuse, lambda P: [list(range(5)), list(range(4))],
+                        lambda rng: [rows(rng, 6, 5), rows(rng, 1, 4)], 34),
+    "max_union_filter": ("max", None, _union_filter, lambda P: [list(range(6)), list(range(3, 8))],
+                         lambda rng: [rows(rng, 8, 6), rows(rng, 8, 5)], 35),
+    "max_path": ("max", None, _path, lambda P: [[P.Coord(*e) for e in _edges(23, 4, 0.5)]],
+                 lambda rng: [rng.uniform(0.05, 0.9, size=(4, len(_edges(23, 4, 0.5)))).astype(np.float32)
+                              .astype(np.float64)], 36),
     "damp_path": ("damp", None, _path, lambda P: [[P.Coord(*e) for e in _edges(22, 4, 0.5)]],
                   lambda rng: [rng.uniform(0.05, 0.5, size=(4, len(_edges(22, 4, 0.5)))).astype(np.float32)
                                .astype(np.float64)], 20),

@@ -30,7 +30,8 @@ def test_gpu_matches_reference_golden(cuda, name):
         np.testing.assert_array_equal(got["present"], gold["present"])
 
 
-@pytest.mark.parametrize("name", ["damp_sum15", "dtkp_hwf5", "dtkp_path_k5", "damp_mod_cond_a2"])
+@pytest.mark.parametrize("name", ["damp_sum15", "dtkp_hwf5", "dtkp_path_k5", "damp_mod_cond_a2", "max_sum4",
+                                  "max_mod_cond_a2", "max_path", "max_bcast_reuse"])
 def test_gpu_matches_oracle_fresh_inputs(cuda, name):
     """Same programs on new seeded inputs: CUDA path vs the CPU oracle."""
     prov, k, prog, syms_fn, make, seed = G.CASES[name]
