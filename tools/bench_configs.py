@@ -5,7 +5,7 @@ LeNet perception forward/backward + Adam) is warmed up eagerly, captured in a CU
 and replayed; time = CUDA events around ``--iters`` replays.  Prints one JSON object per
 measurement (see DESIGN.md §Measurement for the unit definitions).
 
-    python tools/bench_configs.py [--only sum2,hwf7,clutrr,sweep,sum15train]
+    python tools/bench_configs.py [--only sum2,hwf7,clutrr,sweep,sum15train,maxsweep]
 """
 
 from __future__ import annotations
@@ -205,9 +205,55 @@ def sweep(iters):
             torch.cuda.empty_cache()
 
 
+# ------------------------------------------------------------------ max-product variant
+def maxsweep(iters):
+    """The max/DAMP variant (sg_maxprod_*) on sweep shapes and the Sum-15 chain."""
+    cases = [(2, 10, 16384), (2, 10, 65536), (2, 100, 16384), (3, 10, 16384)]
+    for arity, size, B in cases:
+        rng = np.random.default_rng(7 * size + B)
+        xs = [torch.tensor(rows(rng, B, size), device=DEV, requires_grad=True) for _ in range(arity)]
+        syms = list(range(size))
+        f = (lambda a, b: a + b) if arity == 2 else (lambda a, b, c: a + b + c)
+        n_out = arity * (size - 1) + 1
+        w = torch.tensor(rng.uniform(-1, 1, size=(B, n_out)).astype(np.float32), device=DEV)
+
+        def fwd():
+            c = sg.ProgramContext(sg.DampMax(), device=DEV)
+            return sg.get_probs(sg.apply(f, *[sg.make_distribution(c, x, syms) for x in xs]))
+
+        def step():
+            return torch.autograd.grad(fwd(), xs, grad_outputs=w)
+
+        ms_f, mode = timed(lambda: fwd(), iters)
+        ms, _ = timed(step, iters)
+        C = size ** arity
+        fb = 4 * B * (arity * size + 2 * n_out)           # inputs + probs + argmax
+        bb = 4 * B * (2 * n_out + 2 * arity * size)       # g + argmax + inputs + grads
+        emit({"config": f"max variant: sweep arity {arity} |S|={size} f=sum B={B}", "batch": B,
+              "fwd_ms": ms_f, "fwd_bwd_ms": ms, "combos_per_s_fwd": B * C / (ms_f * 1e-3),
+              "combos_per_s_fwd_bwd": B * C / (ms * 1e-3),
+              "fwd_hbm_frac": fb / (ms_f * 1e-3) / 1e9 / HBM, "fwd_bwd_hbm_frac": (fb + bb) / (ms * 1e-3) / 1e9 / HBM,
+              "mode": mode})
+        del xs, w
+        torch.cuda.empty_cache()
+    B = 16384
+    rng = np.random.default_rng(15)
+    xs = [torch.tensor(rows(rng, B, 10), device=DEV, requires_grad=True) for _ in range(15)]
+    targets = torch.tensor(rng.integers(0, 136, size=B), device=DEV)
+
+    def step15():
+        c = sg.ProgramContext(sg.DampMax(), device=DEV)
+        o = P.sum_n(c, [sg.make_distribution(c, x, list(range(10))) for x in xs])
+        return torch.autograd.grad(loss_nll(sg.get_probs(o), targets), xs)
+
+    ms, mode = timed(step15, iters)
+    emit({"config": "max variant: Sum-15 chain B=16384 (14 max-product applies) + loss, fwd+bwd",
+          "ms_per_step": ms, "combos_per_s": B * 9590 / (ms * 1e-3), "mode": mode})
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="sum2,sum15train,hwf7,clutrr,sweep")
+    ap.add_argument("--only", default="sum2,sum15train,hwf7,clutrr,sweep,maxsweep")
     ap.add_argument("--iters", type=int, default=20)
     args = ap.parse_args()
     torch.cuda.set_device(DEV)
@@ -222,6 +268,8 @@ def main():
         clutrr(4096, args.iters)
     if "sweep" in only:
         sweep(args.iters)
+    if "maxsweep" in only:
+        maxsweep(args.iters)
 
 
 if __name__ == "__main__":
