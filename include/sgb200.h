@@ -221,6 +221,13 @@ typedef struct sg_dtkp_apply_desc {
                             * them): warps then take items dynamically instead of by the
                             * static seg.blk partition.  Launches that may run concurrently
                             * need distinct buffers.  NULL = static partition.            */
+  /* Two-level merge: when merge.n_split > 0, merge items that are themselves split write
+   * their partial lists to scratch2 (merge.n_partial rows) and merge2 (merge.n_split
+   * segments, records = scratch2 rows) combines them into the output.  Every level keeps
+   * the record order, so the result equals a single serial merge bit for bit.          */
+  sg_segsum merge2;
+  uint64_t* scratch2_member; /* [merge.n_partial][K][W][B] */
+  uint8_t* scratch2_present; /* [merge.n_partial][K][B]    */
 } sg_dtkp_apply_desc;
 
 int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream);

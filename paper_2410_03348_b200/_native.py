@@ -98,6 +98,9 @@ class SgDtkpApplyDesc(Structure):
         ("scratch_present", c_void_p),
         ("merge", SgSegsum),
         ("sched", c_void_p),
+        ("merge2", SgSegsum),
+        ("scratch2_member", c_void_p),
+        ("scratch2_present", c_void_p),
     ]
 
 

@@ -272,10 +272,28 @@ int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream) {
     m.items = d->merge.items;
     m.blk = d->merge.blk;
     m.n_items = d->merge.n_items;
-    m.scr_m = nullptr;
-    m.scr_p = nullptr;
+    const bool two = d->merge.n_split > 0;
+    SG_RETURN_IF(two && (d->scratch2_member == nullptr || d->scratch2_present == nullptr), cudaErrorInvalidValue);
+    m.scr_m = two ? d->scratch2_member : nullptr;
+    m.scr_p = two ? d->scratch2_present : nullptr;
     int rc = launch_apply(m, d->merge.n_blocks, st);
     if (rc) return rc;
+    if (two) {  // second level: the split merge segments' partial lists -> the output rows
+      DtkpK m2 = m;
+      m2.ops[0].member = d->scratch2_member;
+      m2.ops[0].present = d->scratch2_present;
+      m2.ops[0].rows = d->merge.n_partial;
+      m2.tail = m2.ops[0];
+      m2.recs = d->merge2.recs;
+      m2.rec_words = d->merge2.rec_words;
+      m2.items = d->merge2.items;
+      m2.blk = d->merge2.blk;
+      m2.n_items = d->merge2.n_items;
+      m2.scr_m = nullptr;
+      m2.scr_p = nullptr;
+      rc = launch_apply(m2, d->merge2.n_blocks, st);
+      if (rc) return rc;
+    }
   }
   return 0;
 }

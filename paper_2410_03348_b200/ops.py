@@ -459,7 +459,7 @@ def dtkp_sched(device, n: int) -> torch.Tensor:
 
 
 def dtkp_apply(kplan_host, dseg, dmerge, operands, tail, K: int, W: int, I: int, B: int, p: torch.Tensor,
-               arity: int):
+               arity: int, dmerge2=None):
     """Run sg_dtkp_apply; operands are (member, present) pairs with full batch B."""
     dev = p.device
     n_out = dseg.host.n_seg
@@ -493,6 +493,12 @@ def dtkp_apply(kplan_host, dseg, dmerge, operands, tail, K: int, W: int, I: int,
         d.scratch_member = scr_m.data_ptr()
         d.scratch_present = scr_p.data_ptr()
         d.merge = dmerge.struct(B)
+        if dmerge.host.n_partial:
+            scr2_m = torch.empty((dmerge.host.n_partial, K, W, B), device=dev, dtype=torch.int64)
+            scr2_p = torch.empty((dmerge.host.n_partial, K, B), device=dev, dtype=torch.uint8)
+            d.scratch2_member = scr2_m.data_ptr()
+            d.scratch2_present = scr2_p.data_ptr()
+            d.merge2 = dmerge2.struct(B)
     d.sched = dtkp_sched(dev, -(-B // 32) + 1).data_ptr() if DTKP_DYNAMIC else None
     rc = _lib().sg_dtkp_apply(ctypes.byref(d), N.stream_ptr(dev))
     N.check(rc, "sg_dtkp_apply")

@@ -422,6 +422,7 @@ def csr(keys: np.ndarray, n_seg: int):
 
 DAMP_MAX_ITEM = 128
 DTKP_MAX_ITEM = 48
+DTKP_MERGE_ITEM = 8  # partial lists per first-level merge item (two-level merge)
 STAGE_BYTES = 200 * 1024
 
 
@@ -529,6 +530,7 @@ class DevicePlan:
         self._bwd = {}
         self._dtkp = None
         self._dtkp_merge = None
+        self._dtkp_merge2 = None
 
     def _staged(self, rows: int) -> bool:
         return rows * 32 * 4 <= STAGE_BYTES
@@ -553,13 +555,21 @@ class DevicePlan:
             # DTKP items are latency-bound per warp: ask for ~8 resident CTAs per SM
             self._dtkp = DeviceSegsum(host, self.device, True, 16, target_ctas=148 * 8)
             if len(host.split):
+                # merge of the split segments' partial lists, itself cut into pieces of
+                # DTKP_MERGE_ITEM partials whose lists a second level merges: the serial
+                # chain of a 3868-record segment drops from 48 + 81 to 48 + 8 + 11 records
                 off = np.concatenate([[0], host.split[:, 2]]).astype(np.int64)
                 merge_recs = np.arange(host.n_partial, dtype=np.int32).reshape(-1, 1)
-                mh = HostSegsum(off, merge_recs, 1 << 30)
-                # merge items write the original output segment
-                mh.items[:, 0] = host.split[:, 0]
+                mh = HostSegsum(off, merge_recs, DTKP_MERGE_ITEM)
+                # merge items that finish a segment write the original output segment
+                mh.items[:, 0] = host.split[mh.items[:, 0], 0]
                 self._dtkp_merge = DeviceSegsum(mh, self.device, True, 16, target_ctas=148 * 8)
-        return self._dtkp, self._dtkp_merge
+                if len(mh.split):
+                    off2 = np.concatenate([[0], mh.split[:, 2]]).astype(np.int64)
+                    m2 = HostSegsum(off2, np.arange(mh.n_partial, dtype=np.int32).reshape(-1, 1), 1 << 30)
+                    m2.items[:, 0] = host.split[mh.split[m2.items[:, 0], 0], 0]
+                    self._dtkp_merge2 = DeviceSegsum(m2, self.device, True, 16, target_ctas=148 * 8)
+        return self._dtkp, self._dtkp_merge, self._dtkp_merge2
 
     def maxprod_struct(self) -> N.SgMaxprodPlan:
         d = getattr(self, "_maxprod", None)

@@ -617,8 +617,8 @@ class DtkpAm:
     def _run(self, registry, kp: KernelPlan, operands, tail, arity: int, B: int) -> DtkpTags:
         W = _words(registry.size)
         p = self._p(registry, B)
-        dseg, dmerge = kp.device(p.device).dtkp()
-        pm, pp = ops.dtkp_apply(kp, dseg, dmerge, operands, tail, self.k, W, registry.size, B, p, arity)
+        dseg, dmerge, dmerge2 = kp.device(p.device).dtkp()
+        pm, pp = ops.dtkp_apply(kp, dseg, dmerge, operands, tail, self.k, W, registry.size, B, p, arity, dmerge2)
         return DtkpTags(pm, pp, registry)
 
     # ---- protocol ----------------------------------------------------------------------

@@ -633,3 +633,36 @@ def test_generic_apply_resident_one_pass_backward(cuda, fn, size):
     torch.autograd.backward(got, torch.as_tensor(w, device=cuda))
     for lf, gr in zip(leaves, A.damp_apply_grad(xs, combos, idx, w.astype(np.float64))):
         assert_close_rel(lf.grad.cpu().numpy(), gr, 1e-5, 1e-6, what="grad")
+
+
+@pytest.mark.parametrize("k", [3, 5])
+def test_dtkp_long_group_disj_two_level_merge(cuda, k):
+    """Groups long enough to be split (48 records per item) and to need the two-level merge
+    (> 8 partial lists): bit-exact against the oracle, with exact key ties included, on
+    both the dynamic and the static schedule."""
+    S = sg()
+    from oracle import algebra as A
+    from paper_2410_03348_b200 import ops
+
+    rng = np.random.default_rng(40 + k)
+    reg = S.InputRegistry()
+    prov = S.DtkpAm(k)
+    n, B = 24, 37
+    p = np.round(rng.uniform(0.05, 0.95, size=(B, n)), 1).astype(np.float32).astype(np.float64)
+    base = prov.input_tags(reg, [("x", i) for i in range(n)], torch.tensor(p))
+    obase = A.dtkp_input_tags(0, n, n, B, k)
+    perm = list(rng.permutation(n))
+    pair = prov.conj(prov.gather(base, list(range(n))), prov.gather(base, perm))
+    opair = A.dtkp_conj(A.dtkp_gather(obase, list(range(n))), A.dtkp_gather(obase, perm), p, k)
+    pair = prov.concat_syms([pair] * 60)  # 1440 rows
+    opair = A.dtkp_concat([opair] * 60)
+    groups = [list(rng.integers(0, 1440, size=int(m))) for m in (1000, 433, 385, 49, 1, 700)]
+    for dynamic in (True, False):
+        ops.DTKP_DYNAMIC = dynamic
+        try:
+            got = prov.group_disj(pair, groups)
+        finally:
+            ops.DTKP_DYNAMIC = True
+        ref = A.dtkp_group_disj(opair, groups, p, k)
+        np.testing.assert_array_equal(got.member, ref[0])
+        np.testing.assert_array_equal(got.present, ref[1])
