@@ -11,6 +11,9 @@
 #ifndef SG_DTKP_MINB  // > 0 overrides the per-variant register policy (dtkp_min_blocks)
 #define SG_DTKP_MINB 0
 #endif
+#ifndef SG_DTKP_CONJ_PREFETCH_MAXK  // conj kernels prefetch the next record for K <= this
+#define SG_DTKP_CONJ_PREFETCH_MAXK 4
+#endif
 #ifndef SG_DTKP_UNROLL_K
 #define SG_DTKP_UNROLL_K 4
 #endif
@@ -267,9 +270,11 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
       A.load(a.ops[0], a.B, b, rec_row(a, item.y, 0));
       Bt.load(a.ops[1], a.B, b, rec_row(a, item.y, 1));
     }
+    // next record's rows prefetched unless K is large (their registers cost occupancy)
+    constexpr bool kPf = K <= SG_DTKP_CONJ_PREFETCH_MAXK;
     for (int c = item.y; c < item.z; ++c) {
       const bool more = c + 1 < item.z;
-      if (more) {
+      if (kPf && more) {
         An.load(a.ops[0], a.B, b, rec_row(a, c + 1, 0));
         Bn.load(a.ops[1], a.B, b, rec_row(a, c + 1, 1));
       }
@@ -323,8 +328,13 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
         S.insert(mm, kk, 0);  // same mask, same p -> same key as a recomputation
       }
       if (more) {
-        A = An;
-        Bt = Bn;
+        if constexpr (kPf) {
+          A = An;
+          Bt = Bn;
+        } else {
+          A.load(a.ops[0], a.B, b, rec_row(a, c + 1, 0));
+          Bt.load(a.ops[1], a.B, b, rec_row(a, c + 1, 1));
+        }
       }
     }
   }
@@ -355,6 +365,7 @@ __host__ __device__ constexpr int dtkp_min_blocks(int K, int WT, int AR) {
   return SG_DTKP_MINB > 0 ? SG_DTKP_MINB
          : (WT <= 2 && K <= 3) ? (AR == 1 ? 5 : AR == 2 ? 4 : 1)
          : (WT <= 2 && K <= 5 && AR == 1) ? 4
+         : (WT <= 2 && K <= 5 && AR == 2 && K > SG_DTKP_CONJ_PREFETCH_MAXK) ? 3
          : 1;
 }
 
