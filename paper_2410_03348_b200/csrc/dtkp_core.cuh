@@ -12,7 +12,7 @@
 #define SG_DTKP_MINB 0
 #endif
 #ifndef SG_DTKP_CONJ_PREFETCH_MAXK  // conj kernels prefetch the next record for K <= this
-#define SG_DTKP_CONJ_PREFETCH_MAXK 4
+#define SG_DTKP_CONJ_PREFETCH_MAXK 2
 #endif
 #ifndef SG_DTKP_UNROLL_K
 #define SG_DTKP_UNROLL_K 4
@@ -363,7 +363,7 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
 // without spills at K <= 3 / K <= 5 and W <= 2 (ptxas -v), else whatever the kernel needs.
 __host__ __device__ constexpr int dtkp_min_blocks(int K, int WT, int AR) {
   return SG_DTKP_MINB > 0 ? SG_DTKP_MINB
-         : (WT <= 2 && K <= 3) ? (AR == 1 ? 5 : AR == 2 ? 4 : 1)
+         : (WT <= 2 && K <= 3) ? (AR == 1 ? 5 : AR == 2 ? (K > SG_DTKP_CONJ_PREFETCH_MAXK ? 5 : 4) : 1)
          : (WT <= 2 && K <= 5 && AR == 1) ? 4
          : (WT <= 2 && K <= 5 && AR == 2 && K > SG_DTKP_CONJ_PREFETCH_MAXK) ? 3
          : 1;
