@@ -14,6 +14,9 @@
 #ifndef SG_DTKP_CONJ_PREFETCH_MAXK  // conj kernels prefetch the next record for K <= this
 #define SG_DTKP_CONJ_PREFETCH_MAXK 2
 #endif
+#ifndef SG_DTKP_STREAM_PREFETCH  // streaming (arity-1) kernel loads the next record ahead
+#define SG_DTKP_STREAM_PREFETCH 0
+#endif
 #ifndef SG_DTKP_UNROLL_K
 #define SG_DTKP_UNROLL_K 4
 #endif
@@ -253,7 +256,7 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
     if (item.y < item.z) fetch(item.y, cur);
     for (int c = item.y; c < item.z; ++c) {
       const bool more = c + 1 < item.z;
-      if (more) fetch(c + 1, nxt);
+      if (SG_DTKP_STREAM_PREFETCH && more) fetch(c + 1, nxt);
 #pragma unroll (kUnrollK)
       for (int q = 0; q < K; ++q) {
         if (!((cur.pres >> q) & 1u)) continue;
@@ -261,7 +264,12 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
         cur.row(q, mm);
         S.insert(mm, proof_key<WT>(mm, pc), 0);
       }
-      if (more) cur = nxt;
+      if (more) {
+        if (SG_DTKP_STREAM_PREFETCH)
+          cur = nxt;
+        else
+          fetch(c + 1, cur);
+      }
     }
   } else {
     // conj fold, normalised after every step (candidate order ra*kb + rb)
@@ -363,8 +371,9 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
 // without spills at K <= 3 / K <= 5 and W <= 2 (ptxas -v), else whatever the kernel needs.
 __host__ __device__ constexpr int dtkp_min_blocks(int K, int WT, int AR) {
   return SG_DTKP_MINB > 0 ? SG_DTKP_MINB
-         : (WT <= 2 && K <= 3) ? (AR == 1 ? 5 : AR == 2 ? (K > SG_DTKP_CONJ_PREFETCH_MAXK ? 5 : 4) : 1)
-         : (WT <= 2 && K <= 5 && AR == 1) ? 4
+         : (WT <= 2 && K <= 3) ? (AR == 1 ? (SG_DTKP_STREAM_PREFETCH ? 5 : 6)
+                                  : AR == 2 ? (K > SG_DTKP_CONJ_PREFETCH_MAXK ? 5 : 4) : 1)
+         : (WT <= 2 && K <= 5 && AR == 1) ? (SG_DTKP_STREAM_PREFETCH ? 4 : 5)
          : (WT <= 2 && K <= 5 && AR == 2 && K > SG_DTKP_CONJ_PREFETCH_MAXK) ? 3
          : 1;
 }
