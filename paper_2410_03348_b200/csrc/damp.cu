@@ -24,6 +24,8 @@
 // global memory, hiding the launch gap between the short per-apply kernels.
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace sg {
@@ -769,7 +771,9 @@ constexpr int kNllWarps = 8;
 
 static int nll_chunks(int64_t n, int64_t B) {
   const int tiles = ceil_div(B, kWarp);
-  int want = ceil_div(2 * 148, tiles);
+  // enough CTAs to fill the GPU, but few enough partials that the per-sample finish (one
+  // thread per sample sums `chunks` partials) stays short at small batches
+  int want = std::min(ceil_div(2 * 148, tiles), 32);
   const int max_chunks = ceil_div(n, 4 * kNllWarps);
   if (want > max_chunks) want = max_chunks;
   return want < 1 ? 1 : want;
