@@ -133,6 +133,85 @@ def union(d1: ODist, d2: ODist) -> ODist:
     return ODist(ctx, symbols, A.dtkp_group_disj(both, groups, ctx.p(), ctx.k))
 
 
+def _encode_symbol(s) -> bytes:
+    """distribution.py:64-86 (canonical byte encoding; sample_symbols tie-break only)."""
+    import struct
+    from fractions import Fraction
+
+    if isinstance(s, bool):
+        return b"b1" if s else b"b0"
+    if isinstance(s, int):
+        return b"i%d" % s
+    if isinstance(s, Fraction):
+        return b"q%d/%d" % (s.numerator, s.denominator)
+    if isinstance(s, float):
+        return b"f" + repr(s).encode()
+    if isinstance(s, str):
+        return b"s" + s.encode("utf-8")
+    if s is None:
+        return b"n"
+    if isinstance(s, tuple):
+        return b"t" + b"".join(struct.pack(">I", len(e)) + e for e in map(_encode_symbol, s))
+    raise TypeError(type(s).__name__)
+
+
+def _gather_cols(d: ODist, src, symbols) -> ODist:
+    """Column gather with -1 = zero column: Damp/DtkpAm gather (provenance.py:233,
+    :320-326) and placed (:264-268, :425-433)."""
+    ctx = d.ctx
+    src = np.asarray(src, dtype=np.int64)
+    if ctx.prov in ("damp", "max"):
+        val = np.where(src[None, :] >= 0, d.tag[:, np.maximum(src, 0)], 0.0)
+        return ODist(ctx, symbols, val, ctx._node("placed", (d.node, src, d.tag.shape[1]), val))
+    m, pr = A.pad_width(d.tag, ctx.width)
+    om = np.where((src >= 0)[None, :, None, None], m[:, np.maximum(src, 0)], 0).astype(np.uint8)
+    op = np.where((src >= 0)[None, :, None], pr[:, np.maximum(src, 0)], 0).astype(np.uint8)
+    return ODist(ctx, symbols, (om, op))
+
+
+def sample_symbols(d: ODist, m: int, seed=None, strategy="top") -> ODist:
+    """distribution.py:309-342: keep m symbols by batch-mean probability (ties by the
+    canonical encoding) or by a seeded categorical draw; original order is kept."""
+    if m < 1:
+        raise ValueError(m)
+    if m >= len(d):
+        return d
+    mean = get_probs(d).mean(axis=0)
+    n = len(d)
+    if strategy == "top":
+        keep = set(sorted(range(n), key=lambda i: (-mean[i], _encode_symbol(d.symbols[i])))[:m])
+    else:
+        total = mean.sum()
+        w = mean / total if total > 0 else np.full(n, 1.0 / n)
+        keep = set(np.random.default_rng(seed).choice(n, size=m, replace=False, p=w).tolist())
+    idx = [i for i in range(n) if i in keep]
+    return _gather_cols(d, idx, [d.symbols[i] for i in idx])
+
+
+def stack(parts) -> ODist:
+    """distribution.py:345-369: align symbol sets by first appearance (missing symbols get
+    zero tags), then concatenate along the batch."""
+    ctx = parts[0].ctx
+    symbols, index = [], {}
+    for part in parts:
+        for s in part.symbols:
+            if s not in index:
+                index[s] = len(symbols)
+                symbols.append(s)
+    placed = []
+    for part in parts:
+        src = np.full(len(symbols), -1, dtype=np.int64)
+        for i, s in enumerate(part.symbols):
+            src[index[s]] = i
+        placed.append(_gather_cols(part, src, symbols))
+    if ctx.prov in ("damp", "max"):
+        val = np.concatenate([p.tag for p in placed], axis=0)
+        return ODist(ctx, symbols, val, ctx._node("stack", ([p.node for p in placed], [p.tag.shape[0] for p in placed]),
+                                                  val))
+    ms = [A.pad_width(p.tag, ctx.width) for p in placed]
+    return ODist(ctx, symbols, (np.concatenate([m for m, _ in ms], axis=0), np.concatenate([r for _, r in ms], axis=0)))
+
+
 def get_probs(d: ODist) -> np.ndarray:
     if d.ctx.prov in ("damp", "max"):
         return d.tag
@@ -187,6 +266,18 @@ def grad_inputs(d: ODist, g: np.ndarray):
                 gb = gb.sum(axis=0, keepdims=True)
             grads[n1_node] = grads.get(n1_node, 0) + ga
             grads[n2_node] = grads.get(n2_node, 0) + gb
+        elif kind == "placed":
+            parent, src, n = payload
+            buf = np.zeros((gn.shape[0], n))
+            keep = np.nonzero(src >= 0)[0]
+            np.add.at(buf.T, src[keep], gn[:, keep].T)
+            grads[parent] = grads.get(parent, 0) + buf
+        elif kind == "stack":
+            parents, sizes = payload
+            off = 0
+            for parent, bsz in zip(parents, sizes):
+                grads[parent] = grads.get(parent, 0) + gn[off: off + bsz]
+                off += bsz
         elif kind == "gather":
             parent, keep, n = payload
             buf = np.zeros((gn.shape[0], n))

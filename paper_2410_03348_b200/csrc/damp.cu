@@ -769,11 +769,13 @@ __global__ void k_rows_add(const Rows A, const int32_t* __restrict__ ia, const R
 // Backward: one pass writes every gradient row of its chunk.  Deterministic throughout.
 constexpr int kNllWarps = 8;
 
-static int nll_chunks(int64_t n, int64_t B) {
+static int nll_chunks(int64_t n, int64_t B, bool backward = false) {
   const int tiles = ceil_div(B, kWarp);
-  // enough CTAs to fill the GPU, but few enough partials that the per-sample finish (one
-  // thread per sample sums `chunks` partials) stays short at small batches
-  int want = std::min(ceil_div(2 * 148, tiles), 32);
+  // enough CTAs to fill the GPU; the forward also keeps few enough partials that its
+  // per-sample finish (one thread per sample sums `chunks` partials) stays short at small
+  // batches — the backward has no such finish, so it keeps the full 2 waves
+  int want = ceil_div(2 * 148, tiles);
+  if (!backward && want > 32) want = 32;
   const int max_chunks = ceil_div(n, 4 * kNllWarps);
   if (want > max_chunks) want = max_chunks;
   return want < 1 ? 1 : want;
@@ -809,6 +811,11 @@ __device__ __forceinline__ double nll_rowsum(const double* __restrict__ part, in
   for (int c = 0; c < chunks; ++c) s += part[(size_t)c * B + b];
   return s;
 }
+
+// Targets outside [-1, n) (the reference raises IndexError, learn.py:104-112; the host
+// wrapper checks them before launch whenever it can) never index memory: the sample's log
+// term and gradient become NaN, so a bad device-side target cannot pass silently.
+__device__ __forceinline__ bool nll_bad_target(int64_t t, int n) { return t < -1 || t >= (int64_t)n; }
 
 __device__ __forceinline__ double nll_picked(double s, double pt, int64_t t) {
   const double norm = pt / (s + 1e-8);
@@ -856,7 +863,7 @@ __device__ __forceinline__ void nll_finish(double v, double* __restrict__ loss, 
 }
 
 // Two-pass finish (chunks > 1): per-sample sums from the chunk partials.
-__global__ void __launch_bounds__(256) k_nll_fwd(const Rows p, int64_t B, const int64_t* __restrict__ targets,
+__global__ void __launch_bounds__(256) k_nll_fwd(const Rows p, int n, int64_t B, const int64_t* __restrict__ targets,
                                                  const double* __restrict__ part, int chunks,
                                                  double* __restrict__ rowsum, double* __restrict__ loss,
                                                  double* __restrict__ blocks, unsigned* __restrict__ counter) {
@@ -867,15 +874,17 @@ __global__ void __launch_bounds__(256) k_nll_fwd(const Rows p, int64_t B, const 
     const int64_t t = __ldg(targets + b0);
     const double s = nll_rowsum(part, chunks, B, b0);
     rowsum[b0] = s;
-    const double pt = t >= 0 ? (double)p.ld(t, b0) : 0.0;
-    v = log(nll_picked(s, pt, t));
+    const bool bad = nll_bad_target(t, n);
+    const double pt = t >= 0 && !bad ? (double)p.ld(t, b0) : 0.0;
+    v = bad ? __longlong_as_double(0x7ff8000000000000LL) : log(nll_picked(s, pt, t));
   }
   nll_finish(v, loss, blocks, counter, B);
 }
 
 // Row sums already known (the fused Sum-N chain forward writes them as a side output):
 // only the picked probability and the log term per sample remain.
-__global__ void __launch_bounds__(256) k_nll_fwd_given(const Rows p, int64_t B, const int64_t* __restrict__ targets,
+__global__ void __launch_bounds__(256) k_nll_fwd_given(const Rows p, int n, int64_t B,
+                                                       const int64_t* __restrict__ targets,
                                                        const double* __restrict__ rowsum, double* __restrict__ loss,
                                                        double* __restrict__ blocks, unsigned* __restrict__ counter) {
   const int64_t b0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -883,8 +892,9 @@ __global__ void __launch_bounds__(256) k_nll_fwd_given(const Rows p, int64_t B, 
   double v = 0.0;
   if (b0 < B) {
     const int64_t t = __ldg(targets + b0);
-    const double pt = t >= 0 ? (double)p.ld(t, b0) : 0.0;
-    v = log(nll_picked(__ldg(rowsum + b0), pt, t));
+    const bool bad = nll_bad_target(t, n);
+    const double pt = t >= 0 && !bad ? (double)p.ld(t, b0) : 0.0;
+    v = bad ? __longlong_as_double(0x7ff8000000000000LL) : log(nll_picked(__ldg(rowsum + b0), pt, t));
   }
   nll_finish(v, loss, blocks, counter, B);
 }
@@ -926,8 +936,9 @@ __global__ void __launch_bounds__(256) k_nll_fwd1(const Rows p, int n, int64_t B
     for (int w = 0; w < kNllWarps; ++w) s += red[w][lane];
     rowsum[b0] = s;
     const int64_t t = __ldg(targets + b0);
-    const double pt = t >= 0 ? (double)p.ld(t, b0) : 0.0;
-    v = log(nll_picked(s, pt, t));
+    const bool bad = nll_bad_target(t, n);
+    const double pt = t >= 0 && !bad ? (double)p.ld(t, b0) : 0.0;
+    v = bad ? __longlong_as_double(0x7ff8000000000000LL) : log(nll_picked(s, pt, t));
   }
   nll_finish(v, loss, blocks, counter, B);
 }
@@ -940,11 +951,12 @@ __global__ void __launch_bounds__(256) k_nll_bwd(const Rows p, int n, int64_t B,
   pdl_wait();
   if (b >= B) return;
   const int64_t t = __ldg(targets + b);
+  const bool bad = nll_bad_target(t, n);
   const double s = rowsum[b];
-  const double pt = t >= 0 ? (double)p.ld(t, b) : 0.0;
+  const double pt = t >= 0 && !bad ? (double)p.ld(t, b) : 0.0;
   const double c = nll_picked(s, pt, t);
   const double den = s + 1e-8;
-  const double coef = t >= 0 ? -(*gloss / (double)B) / c : 0.0;
+  const double coef = bad ? __longlong_as_double(0x7ff8000000000000LL) : t >= 0 ? -(*gloss / (double)B) / c : 0.0;
   const double common = -pt / (den * den);
   const int r0 = blockIdx.y * rows_per, r1 = min(n, r0 + rows_per);
   for (int r = r0 + warp; r < r1; r += kNllWarps) {
@@ -1171,16 +1183,17 @@ int sg_nll_fwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, doub
   cudaError_t e = launch(k_nll_partial, dim3(ceil_div(B, kWarp), chunks), dim3(kWarp, kNllWarps), 0, st,
                          rows_of(probs), (int)n, B, rows_per, part);
   if (e != cudaSuccess) return (int)e;
-  return (int)launch(k_nll_fwd, dim3(blocks), dim3(256), 0, st, rows_of(probs), B, targets, (const double*)part, chunks,
+  return (int)launch(k_nll_fwd, dim3(blocks), dim3(256), 0, st, rows_of(probs), (int)n, B, targets,
+                     (const double*)part, chunks,
                      rowsum, loss, blk, counter);
 }
 
 int sg_nll_fwd_rowsum(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, const double* rowsum,
                       double* loss, void* scratch, sg_stream_t stream) {
   if (B <= 0) return 0;
-  (void)n;
   double* base = (double*)scratch;
-  return (int)launch(k_nll_fwd_given, dim3(ceil_div(B, 256)), dim3(256), 0, (cudaStream_t)stream, rows_of(probs), B,
+  return (int)launch(k_nll_fwd_given, dim3(ceil_div(B, 256)), dim3(256), 0, (cudaStream_t)stream, rows_of(probs),
+                     (int)n, B,
                      targets, rowsum, loss, base + 2, (unsigned*)base);
 }
 
@@ -1188,7 +1201,7 @@ int sg_nll_bwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, cons
                const double* rowsum, sg_rows grad, sg_stream_t stream) {
   if (B <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  const int chunks = nll_chunks(n, B);
+  const int chunks = nll_chunks(n, B, /*backward=*/true);
   const int rows_per = ceil_div(n, chunks);
   return (int)launch(k_nll_bwd, dim3(ceil_div(B, kWarp), chunks), dim3(kWarp, kNllWarps), 0, st, rows_of(probs),
                      (int)n, B, targets, grad_loss, rowsum, rows_per, wrows_of(grad));

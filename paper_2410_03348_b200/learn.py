@@ -8,6 +8,8 @@ floors are ``clamp`` with a pass-through backward (tensor.py:275-287), which pla
 
 from __future__ import annotations
 
+import weakref
+
 import torch
 import torch.nn as nn
 import torch.nn.functional as F
@@ -37,12 +39,47 @@ def loss_nll(probs: torch.Tensor, targets) -> torch.Tensor:
     """
     from . import ops
 
-    if not isinstance(targets, torch.Tensor):
-        targets = torch.as_tensor([(-1 if t is None else int(t)) for t in targets], dtype=torch.int64)
+    b, n = probs.shape
+    targets = _check_targets(targets, b, n)
     targets = targets.to(device=probs.device, dtype=torch.int64).contiguous()
     if probs.dtype != torch.float32:
         probs = probs.float()
     return ops.NllLoss.apply(probs.t(), targets)
+
+
+_CHECKED = weakref.WeakKeyDictionary()  # device target tensors already range-checked
+
+
+def _check_targets(targets, b: int, n: int) -> torch.Tensor:
+    """The reference's target contract (learn.py:102-112): ``len(targets) == b``
+    (ValueError) and every target None or in [0, n) (IndexError).  Host targets are
+    checked here; device targets are checked with one reduction unless a CUDA graph is
+    being captured — the kernels additionally turn any target outside [-1, n) into a NaN
+    loss and gradient instead of reading out of bounds."""
+    if not isinstance(targets, torch.Tensor):
+        targets = list(targets)
+        if len(targets) != b:
+            raise ValueError(f"{len(targets)} targets for batch of {b}")
+        for t in targets:
+            if t is not None and not 0 <= t < n:
+                raise IndexError(f"target index {t} out of range for {n} symbols")
+        return torch.as_tensor([(-1 if t is None else int(t)) for t in targets], dtype=torch.int64)
+    if targets.ndim != 1 or targets.shape[0] != b:
+        raise ValueError(f"{targets.shape[0] if targets.ndim else 1} targets for batch of {b}")
+    if targets.is_floating_point() or targets.is_complex():
+        raise ValueError(f"targets must be integer symbol indices, got {targets.dtype}")
+    if targets.is_cuda:
+        if torch.cuda.is_current_stream_capturing():
+            return targets
+        if _CHECKED.get(targets) == (targets._version, n):
+            return targets
+    bad = (targets < -1) | (targets >= n)
+    if bool(bad.any()):
+        t = int(targets[bad][0])
+        raise IndexError(f"target index {t} out of range for {n} symbols")
+    if targets.is_cuda:
+        _CHECKED[targets] = (targets._version, n)
+    return targets
 
 
 def loss_nll_torch(probs: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:

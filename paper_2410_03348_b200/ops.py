@@ -355,6 +355,7 @@ class DampRowsAdd(torch.autograd.Function):
 
 
 _NLL_SCRATCH: "dict[tuple, torch.Tensor]" = {}
+_NLL_RETIRED: "list[torch.Tensor]" = []  # outgrown scratch a captured graph may still use
 
 
 def _nll_scratch(dev, n: int, B: int) -> torch.Tensor:
@@ -366,6 +367,10 @@ def _nll_scratch(dev, n: int, B: int) -> torch.Tensor:
     nbytes = int(_lib().sg_nll_scratch_bytes(n, B))
     buf = _NLL_SCRATCH.get(key)
     if buf is None or buf.numel() < nbytes:
+        if buf is not None:
+            # a CUDA graph captured earlier may still hold this address (its ticket counter
+            # and partials): keep the outgrown buffer alive, never recycle it
+            _NLL_RETIRED.append(buf)
         # under CUDA-graph capture this allocates from the graph pool (memset captured once)
         buf = torch.zeros(max(nbytes, 4096), device=dev, dtype=torch.uint8)
         _NLL_SCRATCH[key] = buf

@@ -86,14 +86,18 @@ class _SymbolIntern:
     Plan outputs are canonical by construction; user-made lists are interned by a
     type-aware value key (bounded LRU)."""
 
-    def __init__(self, limit=8192):
+    def __init__(self, limit=8192, large_limit=256):
         self.by_id = {}  # id(tuple) -> tuple (holds a reference so ids stay unique)
         self.by_value = OrderedDict()
+        self.large = OrderedDict()  # id -> tuple for lists too long for a value key (LRU)
         self.limit = limit
+        self.large_limit = large_limit
 
     def canon(self, symbols: tuple) -> tuple:
         hit = self.by_id.get(id(symbols))
         if hit is symbols:
+            if id(symbols) in self.large:
+                self.large.move_to_end(id(symbols))
             return symbols
         key = _typed(symbols) if len(symbols) <= 4096 else None
         if key is not None:
@@ -113,6 +117,15 @@ class _SymbolIntern:
             while len(self.by_value) > self.limit:
                 _, old = self.by_value.popitem(last=False)
                 self.by_id.pop(id(old), None)
+        else:
+            # long lists (e.g. fresh sample_symbols subsets of HWF's 8332 outputs) are
+            # known by identity only; bound them separately so they cannot accumulate
+            self.large[id(symbols)] = symbols
+            self.large.move_to_end(id(symbols))
+            while len(self.large) > self.large_limit:
+                oid, old = self.large.popitem(last=False)
+                if self.by_id.get(oid) is old:
+                    del self.by_id[oid]
 
 
 _INTERN = _SymbolIntern()

@@ -242,12 +242,8 @@ class Damp:
         return _damp(ops.damp_apply(ops.gather_plan(indices, tags.count), [tags.sm], tags.batch))
 
     def conj(self, a: DampTags, b: DampTags) -> DampTags:
-        n = max(a.count, b.count)
         B = max(a.batch, b.batch)
-        ia = np.arange(n) if a.count == n else np.zeros(n, dtype=np.int64)
-        ib = np.arange(n) if b.count == n else np.zeros(n, dtype=np.int64)
-        kp = KernelPlan(np.stack([ia, ib], axis=1), np.arange(n), n, (a.count, b.count), clamp=False)
-        return _damp(ops.damp_apply(kp, [a.sm, b.sm], B))
+        return _damp(ops.damp_apply(_colwise_conj_plan(a.count, b.count), [a.sm, b.sm], B))
 
     def disj(self, a: DampTags, b: DampTags) -> DampTags:
         n = max(a.count, b.count)
@@ -264,9 +260,7 @@ class Damp:
 
     def group_disj(self, tags: DampTags, groups) -> DampTags:
         """Bucket disjunction: clamp01 of the per-group sum (provenance.py:242-253)."""
-        recs = np.asarray([c for g in groups for c in g], dtype=np.int32).reshape(-1, 1)
-        out = np.asarray([s for s, g in enumerate(groups) for _ in g], dtype=np.int32)
-        kp = KernelPlan(recs, out, len(groups), (tags.count,), clamp=True)
+        kp = _group_plan(groups, tags.count)
         return _damp(ops.damp_apply(kp, [tags.sm], tags.batch))
 
     def concat_syms(self, parts) -> DampTags:
@@ -335,28 +329,13 @@ class DampMax(Damp):
         return _damp(ops.maxprod_apply(ops.gather_plan(indices, tags.count), [tags.sm], tags.batch))
 
     def conj(self, a: DampTags, b: DampTags) -> DampTags:
-        n = max(a.count, b.count)
         B = max(a.batch, b.batch)
-        ia = np.arange(n) if a.count == n else np.zeros(n, dtype=np.int64)
-        ib = np.arange(n) if b.count == n else np.zeros(n, dtype=np.int64)
-        kp = KernelPlan(np.stack([ia, ib], axis=1), np.arange(n), n, (a.count, b.count), clamp=False)
-        return _damp(ops.maxprod_apply(kp, [a.sm, b.sm], B))
+        return _damp(ops.maxprod_apply(_colwise_conj_plan(a.count, b.count), [a.sm, b.sm], B))
 
     def _pairwise_max(self, a: DampTags, b: DampTags, ia, ib) -> DampTags:
         """out[s] = clamp01(max(a[ia[s]], b[ib[s]])), -1 = absent; ties go to a."""
         B = max(a.batch, b.batch)
-        ia = np.asarray(ia, dtype=np.int64)
-        ib = np.asarray(ib, dtype=np.int64)
-        recs, outs = [], []
-        for s in range(len(ia)):
-            if ia[s] >= 0:
-                recs.append(ia[s])
-                outs.append(s)
-            if ib[s] >= 0:
-                recs.append(a.count + ib[s])
-                outs.append(s)
-        kp = KernelPlan(np.asarray(recs, dtype=np.int32).reshape(-1, 1), np.asarray(outs, dtype=np.int32), len(ia),
-                        (a.count + b.count,), clamp=True)
+        kp = _pairwise_max_plan(np.asarray(ia, dtype=np.int32), np.asarray(ib, dtype=np.int32), a.count, b.count)
         both = torch.cat([ops.expand_batch(a.sm, B), ops.expand_batch(b.sm, B)], dim=0)
         return _damp(ops.maxprod_apply(kp, [both], B))
 
@@ -367,9 +346,7 @@ class DampMax(Damp):
         return self._pairwise_max(a, b, ia, ib)
 
     def group_disj(self, tags: DampTags, groups) -> DampTags:
-        recs = np.asarray([c for g in groups for c in g], dtype=np.int32).reshape(-1, 1)
-        out = np.asarray([s for s, g in enumerate(groups) for _ in g], dtype=np.int32)
-        kp = KernelPlan(recs, out, len(groups), (tags.count,), clamp=True)
+        kp = _group_plan(groups, tags.count)
         return _damp(ops.maxprod_apply(kp, [tags.sm], tags.batch))
 
     def placed(self, tags: DampTags, placement: np.ndarray) -> DampTags:
@@ -382,6 +359,68 @@ class DampMax(Damp):
 
     def union_tags(self, a: DampTags, b: DampTags, uplan) -> DampTags:
         return self._pairwise_max(a, b, uplan.ia, uplan.ib)
+
+
+_GROUPS: "dict[tuple, KernelPlan]" = {}
+
+
+def _group_plan(groups, n_src: int) -> KernelPlan:
+    """group_disj's bucket plan (records in (group, ordinal) order), memoised by content."""
+    recs = np.asarray([c for g in groups for c in g], dtype=np.int32).reshape(-1, 1)
+    out = np.asarray([s for s, g in enumerate(groups) for _ in g], dtype=np.int32)
+    key = (int(n_src), len(groups), recs.tobytes(), out.tobytes())
+    kp = _GROUPS.get(key)
+    if kp is None:
+        kp = KernelPlan(recs, out, len(groups), (int(n_src),), clamp=True)
+        if len(_GROUPS) > 4096:
+            _GROUPS.clear()
+        _GROUPS[key] = kp
+    return kp
+
+
+_COLWISE: "dict[tuple, KernelPlan]" = {}
+
+
+def _colwise_conj_plan(na: int, nb: int) -> KernelPlan:
+    """Column-wise product plan of conj (provenance.py:236: a batch-1 / single-column side
+    broadcasts).  Memoised like every other plan: its device tables are uploaded once, so
+    a CUDA graph captured over conj never references freed plan memory."""
+    key = (na, nb)
+    kp = _COLWISE.get(key)
+    if kp is None:
+        n = max(na, nb)
+        ia = np.arange(n) if na == n else np.zeros(n, dtype=np.int64)
+        ib = np.arange(n) if nb == n else np.zeros(n, dtype=np.int64)
+        kp = KernelPlan(np.stack([ia, ib], axis=1), np.arange(n), n, (na, nb), clamp=False)
+        if len(_COLWISE) > 4096:
+            _COLWISE.clear()
+        _COLWISE[key] = kp
+    return kp
+
+
+_PAIRMAX: "dict[tuple, KernelPlan]" = {}
+
+
+def _pairwise_max_plan(ia: np.ndarray, ib: np.ndarray, na: int, nb: int) -> KernelPlan:
+    """out[s] = max over {a[ia[s]], b[ib[s]]} (records: a's row first, then b's), memoised
+    by (ia, ib, counts)."""
+    key = (na, nb, ia.tobytes(), ib.tobytes())
+    kp = _PAIRMAX.get(key)
+    if kp is None:
+        recs, outs = [], []
+        for s in range(len(ia)):
+            if ia[s] >= 0:
+                recs.append(int(ia[s]))
+                outs.append(s)
+            if ib[s] >= 0:
+                recs.append(na + int(ib[s]))
+                outs.append(s)
+        kp = KernelPlan(np.asarray(recs, dtype=np.int32).reshape(-1, 1), np.asarray(outs, dtype=np.int32), len(ia),
+                        (na + nb,), clamp=True)
+        if len(_PAIRMAX) > 4096:
+            _PAIRMAX.clear()
+        _PAIRMAX[key] = kp
+    return kp
 
 
 def _as_range(indices):
@@ -647,9 +686,7 @@ class DtkpAm:
         return self._run(a.registry, _IDPLANS.disj_plan(a.count), [_bcast_dtkp(a, B)], _bcast_dtkp(b, B), 1, B)
 
     def group_disj(self, tags: DtkpTags, groups) -> DtkpTags:
-        recs = np.asarray([c for g in groups for c in g], dtype=np.int32).reshape(-1, 1)
-        out = np.asarray([s for s, g in enumerate(groups) for _ in g], dtype=np.int32)
-        kp = KernelPlan(recs, out, len(groups), (tags.count,), clamp=True)
+        kp = _group_plan(groups, tags.count)
         B = tags.batch
         return self._run(tags.registry, kp, [_bcast_dtkp(tags, B)], None, 1, B)
 
@@ -666,7 +703,9 @@ class DtkpAm:
         p = tags.registry.prob_tensor()
         B = max(tags.batch, p.shape[1])
         pm, pp = _bcast_dtkp(tags, B)
-        p = ops.expand_batch(p, B)
+        # the kernels read p as contiguous [I][B]: a batch-1 registry (e.g. stack() of
+        # per-sample parts) is materialised, and torch sums its gradient back over b
+        p = ops.expand_batch(p, B).contiguous()
         return ops.DtkpProbs.apply(pm, pp, p).t()
 
     def forward_probs(self, tags: DtkpTags) -> np.ndarray:
@@ -674,7 +713,7 @@ class DtkpAm:
         B = max(tags.batch, p.shape[1])
         pm, pp = _bcast_dtkp(tags, B)
         with torch.no_grad():
-            out = ops.DtkpProbs.apply(pm, pp, ops.expand_batch(p, B))
+            out = ops.DtkpProbs.apply(pm, pp, ops.expand_batch(p, B).contiguous())
         return out.t().double().cpu().numpy()
 
     def placed(self, tags: DtkpTags, placement: np.ndarray) -> DtkpTags:

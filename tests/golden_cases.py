@@ -87,6 +87,34 @@ def clutrr_facts(n_entities, rels=None):
     return [Fact(i, i + 1, r) for i in range(n_entities - 1) for r in rels]
 
 
+def _sample(m, strategy, seed=None):
+    """sum of two lists, then sample_symbols (distribution.py:309-342), then one more
+    apply so the gather's backward is exercised through a downstream op."""
+
+    def prog(api, P, ctx, d):
+        out = api.apply(lambda x, y: x + y, d[0], d[1])
+        kept = api.sample_symbols(out, m, seed=seed, strategy=strategy)
+        return api.apply(lambda s: s % 5, kept)
+
+    return prog
+
+
+def _stack_parts(api, P, ctx, d):
+    """Per-sample parts with DIFFERENT symbol sets (each a batch-1 apply of a part with
+    itself), aligned by stack (distribution.py:345-369, placed/stack_parts
+    provenance.py:264-271, :425-440), then a batched apply over the stacked result."""
+    parts = [api.apply(lambda x, y: x + y, di, di) for di in d]
+    out = api.stack(parts)
+    return api.apply(lambda s: s // 2, out)
+
+
+def _stack_inputs(n_parts, width):
+    def make(rng):
+        return [rows(rng, 1, width) for _ in range(n_parts)]
+
+    return make
+
+
 def _edges(seed, nodes, prob):
     rng = np.random.default_rng(seed)
     return [(i, j) for i in range(nodes) for j in range(nodes) if i != j and rng.uniform() < prob]
@@ -136,9 +164,28 @@ CASES = {
                                   .astype(np.float64)], 19),
     "dtkp_clutrr_k5": ("dtkp", 5, _clutrr, lambda P: [clutrr_facts(4)],
                        lambda rng: [rng.uniform(0.05, 0.95, size=(3, 60)).astype(np.float32).astype(np.float64)], 21),
+    # BASELINE configs[2] / [3] at their full program shape (small batch: the reference
+    # runs them in minutes): HWF-7 k=3 (8 applies, step 7 = 30712 x 10 -> 208767 symbols,
+    # eval -> 8332) and the benchmarked CLUTRR closure, 5 entities x 20 relations, k=5
+    "dtkp_hwf7": ("dtkp", 3, _hwf(7), lambda P: [TOKENS] * 7, _sized_inputs(7, 14, 4), 23),
+    "dtkp_clutrr_e5_r20_k5": ("dtkp", 5, _clutrr, lambda P: [clutrr_facts(5)],
+                              lambda rng: [rng.uniform(0.05, 0.95, size=(6, 80)).astype(np.float32)
+                                           .astype(np.float64)], 24),
     "dtkp_clutrr_k3_e5": ("dtkp", 3, _clutrr, lambda P: [clutrr_facts(5, ("father", "mother", "son", "daughter",
                                                                           "brother", "sister", "husband", "wife"))],
                           lambda rng: [rng.uniform(0.05, 0.95, size=(2, 32)).astype(np.float32).astype(np.float64)], 22),
+    # sample_symbols (top / seeded categorical) and stack over parts with different
+    # symbol sets; the reference's own examples are test_distribution.py:329-392
+    "damp_sample_top": ("damp", None, _sample(7, "top"), lambda P: [list(range(8)), list(range(6))],
+                        lambda rng: [rows(rng, 6, 8), rows(rng, 6, 6)], 25),
+    "damp_sample_cat": ("damp", None, _sample(5, "categorical", seed=7), lambda P: [list(range(8)), list(range(6))],
+                        lambda rng: [rows(rng, 6, 8), rows(rng, 6, 6)], 26),
+    "dtkp_sample_top_k3": ("dtkp", 3, _sample(6, "top"), lambda P: [list(range(7)), list(range(5))],
+                           lambda rng: [rows(rng, 5, 7), rows(rng, 5, 5)], 27),
+    "damp_stack": ("damp", None, _stack_parts, lambda P: [list(range(i, i + 3 + i % 2)) for i in range(4)],
+                   lambda rng: [rows(rng, 1, 3 + i % 2) for i in range(4)], 28),
+    "dtkp_stack_k3": ("dtkp", 3, _stack_parts, lambda P: [list(range(i, i + 3 + i % 2)) for i in range(4)],
+                      lambda rng: [rows(rng, 1, 3 + i % 2) for i in range(4)], 29),
     # the max-product ("max/DAMP") variant: fixtures from the reference's Tensor primitives
     # (tools/make_golden_max.py), since the reference has no max provenance
     "max_sum2": ("max", None, _sum, lambda P: [DIGITS] * 2, _digit_inputs(2, 16), 30),

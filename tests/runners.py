@@ -42,6 +42,18 @@ class OracleAPI:
 
         return OP.union(a, b)
 
+    @staticmethod
+    def sample_symbols(d, m, seed=None, strategy="top"):
+        from oracle import programs as OP
+
+        return OP.sample_symbols(d, m, seed=seed, strategy=strategy)
+
+    @staticmethod
+    def stack(parts):
+        from oracle import programs as OP
+
+        return OP.stack(parts)
+
 
 class OracleP:
     from paper_2410_03348_b200.programs import Coord

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import json
 import sys
+import time
 from pathlib import Path
 
 import numpy as np
@@ -61,6 +62,40 @@ def run_case(name):
     return res
 
 
+def loss_nll_cases():
+    """The reference's learn.loss_nll (learn.py:92-119) and its tape gradient on fp32-
+    representable probabilities: rows short of and past 1 (clamped disjunctions), None
+    targets (floor penalty), and shapes that take each kernel schedule of the fused loss
+    (one-pass, chunked row sums at small batch / many symbols)."""
+    from symgrad.learn import loss_nll
+
+    rng = np.random.default_rng(31)
+    specs = [(8, 12, 1.0, 2), (3, 8, None, 0), (64, 300, 1.0, 1), (1000, 20, 3.0, 17), (40, 2500, 0.5, 3),
+             (5, 7, 0.0, 1)]
+    out = {"n_cases": len(specs)}
+    for c, (b, n, scale, n_none) in enumerate(specs):
+        if scale is None:
+            probs = np.full((b, n), 1.0 / n)
+        elif scale == 0.0:
+            probs = rng.uniform(0.0, 1.0, size=(b, n)) * (rng.uniform(size=(b, n)) < 0.3)
+        else:
+            probs = rng.uniform(0.0, 1.0, size=(b, n))
+            probs = probs / probs.sum(axis=1, keepdims=True) * scale * rng.uniform(0.5, 1.5, size=(b, 1))
+        probs = probs.astype(np.float32).astype(np.float64)
+        targets = rng.integers(0, n, size=b).tolist()
+        for i in rng.choice(b, size=n_none, replace=False):
+            targets[int(i)] = None
+        tape = T.GradientTape()
+        leaf = tape.leaf(probs)
+        loss = loss_nll(leaf, targets)
+        grad = tape.backward(loss)[leaf].data
+        out[f"c{c}_probs"] = probs
+        out[f"c{c}_targets"] = np.asarray([-1 if t is None else t for t in targets], dtype=np.int64)
+        out[f"c{c}_loss"] = np.float64(loss.item())
+        out[f"c{c}_grad"] = grad
+    return out
+
+
 def save(name, **arrays):
     OUT.mkdir(parents=True, exist_ok=True)
     np.savez_compressed(OUT / f"{name}.npz", **{k: np.asarray(v) for k, v in arrays.items()})
@@ -68,10 +103,19 @@ def save(name, **arrays):
 
 
 def main():
+    only = [a for a in sys.argv[1:] if not a.startswith("-")]
     for name in G.CASES:
         if G.CASES[name][0] == "max":  # no max provenance in the reference: tools/make_golden_max.py
             continue
+        if only and name not in only:
+            continue
+        t0 = time.perf_counter()
         save(name, **run_case(name))
+        print(f"  {name}: {time.perf_counter() - t0:.1f} s", flush=True)
+    if only:
+        if "loss_nll" in only:
+            save("loss_nll", **loss_nll_cases())
+        return
     # dedup_topk: compiled-reference outputs on fuzz cases with exact ties (test_kernels.py:98-111)
     cases = {}
     rng = np.random.default_rng(30)
@@ -85,6 +129,7 @@ def main():
         cases.update({f"c{c}_member": member, f"c{c}_present": present, f"c{c}_p": p, f"c{c}_k": k,
                       f"c{c}_om": om, f"c{c}_op": op})
     save("dedup_topk_fuzz", n_cases=80, **cases)
+    save("loss_nll", **loss_nll_cases())
     print("reference backend:", S.backend_name())
 
 
