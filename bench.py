@@ -2,19 +2,24 @@
 
 Workload (BASELINE.json configs[1]): MNIST Sum-15 chained apply — 15 digit
 distributions folded by 14 ``apply(+)`` calls (output symbols 0..135), DAMP
-provenance, batch 16384 per GPU, synthetic digit probabilities resident in HBM.
-A step = forward (make_distribution x15, 14 applies, get_probs, loss_nll) + backward
-to the 15 input probability tensors.  The metric is symbol-combinations/s through
-``Distribution.apply``: units per step = B * sum_i |S1_i| * |S2_i| = B * 9590.
+provenance, batch 16384 per GPU (``--scaling strong``: 16384 global), synthetic digit
+probabilities resident in HBM.  A step = forward (make_distribution x15, 14 applies,
+get_probs, loss_nll) + backward to the 15 input probability tensors.  The metric is
+symbol-combinations/s through ``Distribution.apply``: units per step = B * 9590.
 
 value      device-timed (CUDA events) replay of the captured step (CUDA graph),
            L2 flushed (512 MB write) before every timed step, max over ranks.
-e2e        the same step through the public Python API with host buffers: pinned
-           H2D of the inputs + targets, eager API calls, D2H of the loss, every step.
-roofline   dominant kernel of the step, algorithmic bytes / CUDA-event
-           duration per launch (cold L2), vs MEASURED_PEAKS.json hbm_gbs.
-cpu_baseline  the reference symgrad (baseline/_ref, compiled backend) on a bounded
-           sample of the same workload on this host's cores (tools/ref_bench.py).
+e2e        the same step through the public API with host buffers (GraphedStep; pinned
+           H2D of the inputs + targets and D2H of the loss every step).
+roofline   dominant kernel of the step: algorithmic bytes / its CUDA-event
+           duration inside the step, vs MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the reference symgrad (baseline/_ref, compiled backend) on the SAME config
+           (B=16384), the batch split over one process per host core (tools/ref_bench.py).
+train      the data-parallel train step (perception Mlp + symbolic + loss + backward + ONE
+           NCCL all_reduce + Adam), captured, device-timed, max over ranks.
+configs    every other BASELINE config (Sum-2 train, HWF-7, CLUTRR, the sweep): device
+           time, e2e, whole-step roofline fraction, and the reference CPU number of the same
+           config from the same run (tools/bench_configs.py); rank 0 at N=1.
 
 ``--impl reference`` runs only the reference CPU arm (rank 0) and prints its line.
 """
@@ -37,6 +42,7 @@ sys.path.insert(0, str(ROOT))
 N_DIGITS = 15
 DIGITS = list(range(10))
 METRIC = "apply symbol-combos/sec & train samples/sec (Sum-N, HWF) at 1/2/4/8 B200 vs host CPU"
+GLOBAL_STRONG_BATCH = 16384  # --scaling strong: the global batch is fixed, per-GPU = 16384 / N
 
 
 def combos_per_sample(n=N_DIGITS):
@@ -108,43 +114,53 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU arm
-def cpu_reference(batch, repeats=3, port=False):
+def cpu_reference(batch, steps=2, warmup=1, workload="sum15"):
+    """The reference symgrad (baseline/_ref, compiled backend) on this host: the batch is
+    split over one worker process per available core (tools/ref_bench.py).  Fails loudly
+    when the reference is not installed — there is no substitute implementation."""
     env = dict(os.environ)
-    cores = len(os.sched_getaffinity(0))
-    env["OPENBLAS_NUM_THREADS"] = str(cores)
-    cmd = [sys.executable, str(ROOT / "tools" / "ref_bench.py"), "--batch", str(batch), "--repeats", str(repeats)]
-    if port:
-        cmd.append("--port")
-    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900)
+    env["OPENBLAS_NUM_THREADS"] = "1"  # one core per shard process
+    cmd = [sys.executable, str(ROOT / "tools" / "ref_bench.py"), "--workload", workload, "--batch", str(batch),
+           "--steps", str(steps), "--warmup", str(warmup)]
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=1800)
     if out.returncode != 0:
         raise RuntimeError(f"reference CPU arm failed:\n{out.stderr[-2000:]}")
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
 def run_reference_arm(args):
+    """``--impl reference``: the reference's own CPU implementation of the path on this
+    box's host cores, on our arm's workload (Sum-15 chain, DAMP, fwd + loss_nll + bwd) at
+    our per-GPU batch (16384: the same config at N=1; at N>1 a bounded 16384-sample slice
+    of the N*16384 global batch per step).  Rank 0 alone runs; other ranks exit."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    ref = cpu_reference(args.cpu_batch, repeats=max(1, args.steps), port=False)
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    B = args.batch if args.scaling == "weak" else max(1, GLOBAL_STRONG_BATCH // max(world, 1))
+    steps, warmup = max(1, args.steps), min(max(0, args.warmup), 2)
+    ref = cpu_reference(B, steps=steps, warmup=warmup)
     line = {
         "impl": "reference",
         "metric": METRIC,
         "value": ref["value"],
         "unit": ref["unit"],
-        "n_gpus": args.gpus,
-        "steps": max(1, args.steps),
-        "warmup": 1,
+        "n_gpus": world,
+        "steps": steps,
+        "warmup": warmup,
         "ms_per_step": ref["seconds_per_step"] * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "MNIST Sum-15 chained apply, DAMP, fwd+bwd (BASELINE configs[1])",
-                   "global_batch": args.cpu_batch, "per_gpu_batch": None, "seq_len": None,
-                   "parallelism": "cpu", "l2": "n/a"},
+        "config": {"workload": "MNIST Sum-15 chained apply (output symbols 0..135), DAMP, fwd+loss+bwd "
+                               "(BASELINE configs[1])",
+                   "global_batch": B * (world if args.scaling == "weak" else 1), "per_step_sample_batch": B,
+                   "same_config": world == 1 or args.scaling == "strong", "seq_len": None,
+                   "parallelism": f"cpu: batch split over {ref['cores']} reference processes", "l2": "n/a"},
         "cpu_baseline": {"value": ref["value"], "unit": ref["unit"], "cores": ref["cores"], "kind": ref["kind"],
-                         "sample": ref["sample"]},
+                         "sample": ref["sample"], "backend": ref["backend"]},
         "e2e": {"value": ref["value"], "unit": ref["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "samples_per_s": ref["samples_per_s"],
     }
@@ -288,6 +304,100 @@ def ncu_traffic(kernel):
         return None
 
 
+def measure_train(torch, sg, device, B, steps, warmup, world, backend, flush):
+    """The data-parallel TRAIN step of the Sum-15 config: the reference's perception model
+    (Mlp 784-128-10, learn.py:36-70 / tasks.py:50-51; bf16 autocast GEMMs) on synthetic
+    28x28 Gaussian-cluster digits (datasets.py:113-153) resident in HBM -> 15 softmax blocks
+    -> sum_n (fused DAMP chain) -> loss_nll -> backward -> ONE all_reduce of the flat
+    gradient buffer (NCCL over NVLink; dp.FlatGradReducer) -> Adam.  Captured whole in a
+    CUDA graph (collective included) when the backend is NCCL; device-timed, max over
+    ranks.  Also times the all_reduce alone."""
+    from paper_2410_03348_b200 import programs as P
+    from paper_2410_03348_b200.dp import FlatGradReducer
+    from paper_2410_03348_b200.learn import Mlp, loss_nll
+
+    rank = int(os.environ.get("RANK", "0"))
+    model = Mlp(784, 128, 10, seed=0).to(device)
+    red = FlatGradReducer(model.parameters())
+    opt = torch.optim.Adam(model.parameters(), lr=1e-3, capturable=True, foreach=True)
+    g = torch.Generator(device="cpu").manual_seed(4321 + rank)
+    labels = torch.randint(0, 10, (N_DIGITS, B), generator=g)
+    centers = torch.randn(10, 784, generator=g)
+    feats = torch.empty((N_DIGITS, B, 784), dtype=torch.bfloat16, device=device)
+    for i in range(N_DIGITS):  # built digit by digit to bound host memory
+        feats[i] = (centers[labels[i]] * (5.0 / 28.0) + torch.randn(B, 784, generator=g)).to(torch.bfloat16)
+    targets = labels.sum(0).to(device)
+
+    def step():
+        red.zero_()
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            probs = model(feats.view(-1, 784)).float().view(N_DIGITS, B, 10)
+        ctx = sg.ProgramContext(sg.Damp(), device=device)
+        out = P.sum_n(ctx, [sg.make_distribution(ctx, probs[i], DIGITS) for i in range(N_DIGITS)])
+        loss = loss_nll(sg.get_probs(out), targets)
+        loss.backward()
+        red.all_reduce_()
+        opt.step()
+        return loss
+
+    side = torch.cuda.Stream(device)
+    side.wait_stream(torch.cuda.current_stream(device))
+    with torch.cuda.stream(side):
+        for _ in range(max(3, warmup)):
+            step()
+    torch.cuda.current_stream(device).wait_stream(side)
+    torch.cuda.synchronize(device)
+    graph, mode = None, "eager"
+    if backend == "nccl" or world == 1:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        graph.replay()
+        torch.cuda.synchronize(device)
+        mode = "cuda_graph (all_reduce captured)" if world > 1 else "cuda_graph"
+    if world > 1:
+        dist_barrier(torch, world)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in ev:
+        flush()
+        a.record()
+        graph.replay() if graph is not None else step()
+        b.record()
+    torch.cuda.synchronize(device)
+    ms = allreduce_max(sum(a.elapsed_time(b) for a, b in ev), world, device, backend) / steps
+    # the collective alone (same flat buffer), for its share of the step
+    ar_ms = None
+    if world > 1:
+        import torch.distributed as dist
+
+        for _ in range(5):
+            dist.all_reduce(red.flat)
+        torch.cuda.synchronize(device)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(20):
+            dist.all_reduce(red.flat)
+        b.record()
+        torch.cuda.synchronize(device)
+        ar_ms = allreduce_max(a.elapsed_time(b) / 20, world, device, backend)
+    del feats
+    torch.cuda.empty_cache()
+    return {"metric": "train samples/s", "value": world * B / (ms * 1e-3), "ms_per_step": ms, "per_gpu_batch": B,
+            "global_batch": world * B, "mode": mode, "images_per_step": world * B * N_DIGITS,
+            "perception": "Mlp 784-128-10 (reference learn.py:36-70), bf16 autocast, synthetic 28x28 digits",
+            "optimizer": "Adam (capturable)", "collective": {"op": "all_reduce (mean) of the flat fp32 gradient",
+                                                            "bytes": red.nbytes, "backend": backend,
+                                                            "ms_alone": ar_ms},
+            "timing": "CUDA events per step, L2 flushed before each, max over ranks"}
+
+
+def dist_barrier(torch, world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
 def allreduce_max(x, world, device, backend):
     """Max over ranks of a host float (device timing of each rank)."""
     import torch
@@ -322,7 +432,7 @@ def run_gpu_arm(args):
     import paper_2410_03348_b200 as sg
     from paper_2410_03348_b200 import _native as N
 
-    B = args.batch
+    B = args.batch if args.scaling == "weak" else max(1, GLOBAL_STRONG_BATCH // world)
     pk, pk_src = peaks()
     hbm = float(pk["hbm_gbs"])
     x_h, t_h = make_inputs(torch, B, device, seed=1234 + rank)
@@ -517,12 +627,30 @@ def run_gpu_arm(args):
                                          "fused chain's own minimum bytes_per_launch, the stricter figure"}
         if world == 1 and not args.no_cpu_baseline:
             try:
-                ref = cpu_reference(args.cpu_batch, repeats=3)
+                ref = cpu_reference(B, steps=2, warmup=1)
                 cpu = {"value": ref["value"], "unit": ref["unit"], "cores": ref["cores"], "kind": ref["kind"],
-                       "sample": ref["sample"]}
+                       "sample": ref["sample"], "backend": ref["backend"], "same_config": True}
             except Exception as exc:  # noqa: BLE001 - reported, not fatal
                 cpu = {"value": None, "unit": "symbol-combos/s", "cores": None, "kind": "reference",
                        "sample": f"failed: {exc}"[:300]}
+    # ---- the data-parallel train step (perception + symbolic + all_reduce + Adam)
+    train = None
+    if not args.no_train:
+        train = measure_train(torch, sg, device, B, args.steps, args.warmup, world, backend, flush)
+    # ---- every other BASELINE config (rank 0 at N=1): device, e2e, roofline, CPU reference
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        sys.path.insert(0, str(ROOT / "tools"))
+        import bench_configs
+
+        try:
+            configs = bench_configs.all_configs(device, iters=max(3, min(args.steps, 20)),
+                                                cpu=not args.no_cpu_baseline)
+        except Exception as exc:  # noqa: BLE001 - reported in the line, never silently
+            import traceback
+
+            traceback.print_exc()
+            configs = {"error": f"{type(exc).__name__}: {exc}"[:500]}
     if rank == 0:
         ms_per_step = max_ms / args.steps
         line = {
@@ -534,7 +662,7 @@ def run_gpu_arm(args):
             "warmup": args.warmup,
             "ms_per_step": ms_per_step,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": args.scaling,
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic",
@@ -562,6 +690,8 @@ def run_gpu_arm(args):
                                "graph-replayed back to back over rotating buffer sets > 2x L2 (cold)",
             "cpu_baseline": cpu,
             "clocks": clk,
+            "train": train,
+            "configs": configs,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -575,9 +705,12 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=16384, help="per-GPU batch")
-    ap.add_argument("--cpu-batch", type=int, default=2048, help="reference CPU sample batch")
+    ap.add_argument("--batch", type=int, default=16384, help="per-GPU batch (weak scaling)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: --batch per GPU; strong: global batch 16384 split over the GPUs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config measurements")
+    ap.add_argument("--no-train", action="store_true", help="skip the data-parallel train step")
     ap.add_argument("--quick", action="store_true",
                     help="profiling runs: only warm-up + the timed graph steps (no e2e/roofline/cpu/clock soak)")
     args = ap.parse_args()

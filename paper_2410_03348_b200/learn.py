@@ -8,13 +8,11 @@ floors are ``clamp`` with a pass-through backward (tensor.py:275-287), which pla
 
 from __future__ import annotations
 
-import weakref
-
 import torch
 import torch.nn as nn
 import torch.nn.functional as F
 
-__all__ = ["PassClamp", "loss_nll", "loss_nll_torch", "LeNet"]
+__all__ = ["PassClamp", "loss_nll", "loss_nll_torch", "LeNet", "Mlp"]
 
 
 class PassClamp(torch.autograd.Function):
@@ -47,9 +45,6 @@ def loss_nll(probs: torch.Tensor, targets) -> torch.Tensor:
     return ops.NllLoss.apply(probs.t(), targets)
 
 
-_CHECKED = weakref.WeakKeyDictionary()  # device target tensors already range-checked
-
-
 def _check_targets(targets, b: int, n: int) -> torch.Tensor:
     """The reference's target contract (learn.py:102-112): ``len(targets) == b``
     (ValueError) and every target None or in [0, n) (IndexError).  Host targets are
@@ -71,14 +66,14 @@ def _check_targets(targets, b: int, n: int) -> torch.Tensor:
     if targets.is_cuda:
         if torch.cuda.is_current_stream_capturing():
             return targets
-        if _CHECKED.get(targets) == (targets._version, n):
+        if getattr(targets, "_sg_checked", None) == (targets._version, n):  # already range-checked
             return targets
     bad = (targets < -1) | (targets >= n)
     if bool(bad.any()):
         t = int(targets[bad][0])
         raise IndexError(f"target index {t} out of range for {n} symbols")
     if targets.is_cuda:
-        _CHECKED[targets] = (targets._version, n)
+        targets._sg_checked = (targets._version, n)
     return targets
 
 
@@ -114,3 +109,22 @@ class LeNet(nn.Module):
         x = F.relu(self.fc1(x))
         x = F.relu(self.fc2(x))
         return F.softmax(self.fc3(x), dim=1)
+
+
+class Mlp(nn.Module):
+    """The reference's perception model (learn.py:36-70): 784 -> 128 ReLU -> C softmax,
+    with its initialisation (normal(0, 1/sqrt(fan_in)) weights, zero biases)."""
+
+    def __init__(self, in_dim: int = 784, hidden: int = 128, n_classes: int = 10, seed: int = 0):
+        super().__init__()
+        g = torch.Generator().manual_seed(seed)
+        self.fc1 = nn.Linear(in_dim, hidden)
+        self.fc2 = nn.Linear(hidden, n_classes)
+        with torch.no_grad():
+            self.fc1.weight.copy_(torch.randn(hidden, in_dim, generator=g) / in_dim**0.5)
+            self.fc2.weight.copy_(torch.randn(n_classes, hidden, generator=g) / hidden**0.5)
+            self.fc1.bias.zero_()
+            self.fc2.bias.zero_()
+
+    def forward(self, x):
+        return F.softmax(self.fc2(F.relu(self.fc1(x))), dim=-1)

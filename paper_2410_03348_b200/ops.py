@@ -115,6 +115,8 @@ class DampApply(torch.autograd.Function):
             rows = (ctypes.c_int32 * N.MAX_ARITY)(*kplan.sizes)
             rc = _lib().sg_segsum_run(ctypes.byref(seg), ops_, rows, kplan.arity, B, 0, N.rows(out), N.ptr(scratch), st)
             N.check(rc, "sg_segsum_run")
+        _ledger("damp_apply_fwd", 4 * B * (sum(kplan.sizes) + kplan.n_out) + 4 * kplan.n_rec * kplan.arity,
+                B * kplan.n_rec)
         ctx.kplan = kplan
         ctx.B = B
         ctx.save_for_backward(*inputs)
@@ -143,6 +145,8 @@ class DampApply(torch.autograd.Function):
             rc = _lib().sg_damp_apply_bwd(ctypes.byref(s), N.rows_array(inputs), N.rows(g), B,
                                           N.rows_array(grads), N.ptr(scratch), N.stream_ptr(dev))
             N.check(rc, "sg_damp_apply_bwd")
+            _ledger("damp_apply_bwd", 4 * B * (kplan.n_out + sum(2 * kplan.sizes[i] for i in need))
+                    + 4 * kplan.n_rec * kplan.arity, B * kplan.n_rec)
             if kplan.conv:
                 grads = [gr if ctx.needs_input_grad[2 + i] else None for i, gr in enumerate(grads)]
         return (None, None, *grads)
@@ -192,6 +196,18 @@ def maxprod_apply(kplan: KernelPlan, inputs, B: int) -> torch.Tensor:
 def damp_apply(kplan: KernelPlan, inputs, B: int) -> torch.Tensor:
     inputs = [expand_batch(x, B) for x in inputs]
     return DampApply.apply(kplan, B, *inputs)
+
+
+# Opt-in algorithmic-traffic ledger (bench.py): while ALG_BYTES is a list, every launch
+# below appends (kernel, compulsory HBM bytes, work units) with the SURVEY §8(d) formulas
+# evaluated on the launch's shapes — inputs read once, outputs written once, plan tables
+# read once per launch — so a step's roofline fraction is sum(bytes) / step time.
+ALG_BYTES = None
+
+
+def _ledger(kernel: str, nbytes: int, units: int = 0):
+    if ALG_BYTES is not None:
+        ALG_BYTES.append((kernel, int(nbytes), int(units)))
 
 
 # Opt-in per-launch CUDA-event timers (bench.py): while LAUNCH_TIMERS is a dict, the
@@ -246,6 +262,8 @@ class ConvChainFn(torch.autograd.Function):
         with launch_timer("chain_fwd"):
             rc = _lib().sg_chain_fwd(ctypes.byref(c), out.data_ptr(), rowsum.data_ptr(), N.stream_ptr(dev))
         N.check(rc, "sg_chain_fwd")
+        _ledger("chain_fwd", 4 * B * (n0 + m * kf + (elems // B if B else 0) + out.shape[0]) + 8 * B,
+                B * sum((n0 + i * (kf - 1)) * kf for i in range(m)))
         out._sg_rowsum = (rowsum, out._version)  # for loss_nll on exactly these values
         ctx.meta = (n0, kf, B)
         ctx.save_for_backward(base, states, *filters)
@@ -265,6 +283,9 @@ class ConvChainFn(torch.autograd.Function):
         with launch_timer("chain_bwd"):
             rc = _lib().sg_chain_bwd(ctypes.byref(c), g.data_ptr(), N.rows(gbase), arr, N.stream_ptr(g.device))
         N.check(rc, "sg_chain_bwd")
+        m = len(filters)
+        _ledger("chain_bwd", 4 * B * (g.shape[0] + 2 * m * kf + states.numel() // max(B, 1) + 2 * n0),
+                B * sum((n0 + i * (kf - 1)) * kf for i in range(m)))
         return (None, None, None, gbase, *gfilt)
 
 
@@ -343,6 +364,7 @@ class DampRowsAdd(torch.autograd.Function):
         rc = _lib().sg_damp_rows_add(N.rows(A), ma.idx.data_ptr(), N.rows(Bm), mb.idx.data_ptr(), n, B,
                                      1 if clamp else 0, out.data_ptr(), N.stream_ptr(A.device))
         N.check(rc, "sg_damp_rows_add")
+        _ledger("damp_rows_add", 4 * B * (A.shape[0] + Bm.shape[0] + n), B * n)
         ctx.maps = (ma, mb)
         return out
 
@@ -411,6 +433,7 @@ class NllLoss(torch.autograd.Function):
             rc = _lib().sg_nll_fwd(N.rows(probs_nb), n, B, targets.data_ptr(), loss.data_ptr(), scratch.data_ptr(),
                                    rowsum.data_ptr(), N.stream_ptr(dev))
             N.check(rc, "sg_nll_fwd")
+        _ledger("nll_fwd", 4 * B * n + 16 * B, B * n)
         ctx.save_for_backward(probs_nb, targets, rowsum)
         return loss
 
@@ -423,6 +446,7 @@ class NllLoss(torch.autograd.Function):
         rc = _lib().sg_nll_bwd(N.rows(probs_nb), n, B, targets.data_ptr(), g.data_ptr(), rowsum.data_ptr(),
                                N.rows(grad), N.stream_ptr(probs_nb.device))
         N.check(rc, "sg_nll_bwd")
+        _ledger("nll_bwd", 8 * B * n + 16 * B, B * n)
         return grad, None
 
 
@@ -435,6 +459,7 @@ def rows_gather(src: torch.Tensor, idx: torch.Tensor, out: torch.Tensor):
     rc = _lib().sg_rows_gather(src.data_ptr() if src.numel() else None, idx.data_ptr(), n, row_bytes, out.data_ptr(),
                                N.stream_ptr(out.device))
     N.check(rc, "sg_rows_gather")
+    _ledger("rows_gather", 2 * n * row_bytes, n)
     return out
 
 
@@ -507,6 +532,14 @@ def dtkp_apply(kplan_host, dseg, dmerge, operands, tail, K: int, W: int, I: int,
     d.sched = dtkp_sched(dev, -(-B // 32) + 1).data_ptr() if DTKP_DYNAMIC else None
     rc = _lib().sg_dtkp_apply(ctypes.byref(d), N.stream_ptr(dev))
     N.check(rc, "sg_dtkp_apply")
+    if ALG_BYTES is not None:
+        row = 8 * K * W + K  # one tag per sample: K rows of W words + K present bytes
+        rows_in = sum(m.shape[0] for m, _ in operands) + (tail[0].shape[0] if tail is not None else 0)
+        partial = dseg.host.n_partial + (dmerge.host.n_partial if dseg.host.n_partial else 0)
+        n_rec = kplan_host.n_rec
+        cand = n_rec * (K ** arity if arity >= 2 else K)  # candidate rows ranked (upper bound)
+        _ledger("dtkp_apply", B * (rows_in + n_out + 2 * partial) * row + 4 * B * I + 4 * n_rec * max(arity, 1),
+                B * cand)
     return out_m, out_p
 
 
@@ -523,6 +556,7 @@ class DtkpProbs(torch.autograd.Function):
                                       p.data_ptr() if p.numel() else None, I, B, out.data_ptr() if out.numel() else None,
                                       N.stream_ptr(p.device))
         N.check(rc, "sg_dtkp_probs_fwd")
+        _ledger("dtkp_probs_fwd", B * Nn * (8 * K * W + K) + 4 * B * I + 4 * B * Nn, B * Nn * K)
         ctx.save_for_backward(member, present, p)
         return out
 
@@ -540,6 +574,7 @@ class DtkpProbs(torch.autograd.Function):
                                       g.data_ptr() if g.numel() else None, gp.data_ptr(), scratch.data_ptr(),
                                       N.stream_ptr(p.device))
         N.check(rc, "sg_dtkp_probs_bwd")
+        _ledger("dtkp_probs_bwd", B * Nn * (8 * K * W + K) + 8 * B * I + 4 * B * Nn, B * Nn * K)
         return None, None, gp
 
 

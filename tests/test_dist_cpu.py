@@ -96,7 +96,17 @@ def _worker(rank, world, port, q):
         loss.backward()
         grads = [p.grad.clone() for p in model.parameters()]
         worst = max_over_ranks(float(rank + 1))
-        q.put((rank, fps, (lo, hi), [g.numpy() for g in grads], worst))
+        # the bench's train step: grads as views of one flat buffer, ONE all_reduce
+        from paper_2410_03348_b200.dp import FlatGradReducer
+
+        m2 = _model().float()
+        red = FlatGradReducer(m2.parameters())
+        red.zero_()
+        loss2 = _SymbolicLoss.apply(m2(x[:, lo:hi].float()), t[lo:hi])
+        loss2.backward()
+        red.all_reduce_()
+        flat = [p.grad.detach().double().clone().numpy() for p in m2.parameters()]
+        q.put((rank, fps, (lo, hi), [g.numpy() for g in grads], worst, flat))
     finally:
         dist.destroy_process_group()
 
@@ -126,7 +136,7 @@ def test_ddp_gloo_world2_matches_single_process():
         p.join(timeout=60)
         assert p.exitcode == 0
     results.sort()
-    (_, fp0, span0, g0, w0), (_, fp1, span1, g1, w1) = results
+    (_, fp0, span0, g0, w0, f0), (_, fp1, span1, g1, w1, f1) = results
     assert fp0 == fp1
     assert span0 == (0, 6) and span1 == (6, 12)
     assert w0 == w1 == 2.0
@@ -134,3 +144,6 @@ def test_ddp_gloo_world2_matches_single_process():
     for a, b, r in zip(g0, g1, ref):
         np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-14)  # DDP leaves identical grads
         np.testing.assert_allclose(a, r.numpy(), rtol=1e-9, atol=1e-12)  # == global-batch gradient
+    for a, b, r in zip(f0, f1, ref):  # flat-buffer all_reduce == DDP == global batch (fp32)
+        np.testing.assert_array_equal(a, b)
+        np.testing.assert_allclose(a, r.numpy(), rtol=2e-5, atol=1e-6)

@@ -74,7 +74,7 @@ def test_graphed_clutrr_closure_matches_eager_and_reference(cuda):
     assert [repr(s) for s in gc.symbols] == gold["symbols"]
     np.testing.assert_array_equal(g.double().cpu().numpy(), eager["grads"][0])
     assert_close_rel(g.double().cpu().numpy(), gold["grad0"], 1e-5, floor_frac=1e-6, what="graphed grad")
-    assert float(loss) == pytest.approx(float((gold["probs"] * gold["w"]).sum()), rel=1e-5)
+    assert float(loss.detach()) == pytest.approx(float((gold["probs"] * gold["w"]).sum()), rel=1e-5)
     gp = _graphed(cuda, x)
     probs = gp(torch.tensor(x, device=cuda, dtype=torch.float32))
     torch.cuda.synchronize()

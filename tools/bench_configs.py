@@ -1,17 +1,28 @@
-"""Measure every BASELINE.json config on one B200 (the headline line is bench.py's).
+"""Per-config measurements for bench.py's ``configs`` key (BASELINE.json configs[0], [2],
+[3], [4]; configs[1] is bench.py's headline) — also runnable on its own:
 
-Each workload step (symbolic forward + loss + backward, and for the train configs the
-LeNet perception forward/backward + Adam) is warmed up eagerly, captured in a CUDA graph
-and replayed; time = CUDA events around ``--iters`` replays.  Prints one JSON object per
-measurement (see DESIGN.md §Measurement for the unit definitions).
+    python tools/bench_configs.py [--only sum2,hwf7,clutrr,sweep,maxsweep] [--no-cpu]
 
-    python tools/bench_configs.py [--only sum2,hwf7,clutrr,sweep,sum15train,maxsweep]
+For every config, on one B200:
+  device     the step (symbolic forward + loss + backward; for Sum-2 also the LeNet
+             perception forward/backward and Adam) captured in a CUDA graph, replayed
+             ``iters`` times with L2 flushed (512 MB write) before each replay; CUDA events
+             on the launching stream around each replay.
+  e2e        the same step through the public API, eager, with the step's inputs copied
+             H2D from pinned host memory and the loss read back D2H every step.
+  roofline   the step's algorithmic HBM bytes (ops.ALG_BYTES ledger: SURVEY §8(d)
+             formulas evaluated per launch — inputs read once, outputs written once) /
+             the device step time, vs MEASURED_PEAKS.json hbm_gbs; per-kernel shares.
+  cpu        the reference symgrad (baseline/_ref) on the same config, batch split over
+             the host's cores (tools/ref_bench.py), same run.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
+import os
+import subprocess
 import sys
 import time
 from pathlib import Path
@@ -23,49 +34,116 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 import paper_2410_03348_b200 as sg  # noqa: E402
+from paper_2410_03348_b200 import ops  # noqa: E402
 from paper_2410_03348_b200 import programs as P  # noqa: E402
 from paper_2410_03348_b200.learn import LeNet, loss_nll  # noqa: E402
 
-DEV = torch.device("cuda", 0)
-HBM = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
+HWF7_SIZES = [(10,), (10, 4), (40, 10), (283, 4), (1132, 10), (7678, 4), (30712, 10), (208767,)]
 
 
-def timed(step, iters=20, graph=True):
-    """ms per step: eager warm-up, CUDA-graph capture, replay timing (eager if capture fails)."""
-    side = torch.cuda.Stream(DEV)
-    side.wait_stream(torch.cuda.current_stream(DEV))
+def hbm_peak():
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]), "measured"
+    except (OSError, ValueError, KeyError):
+        return 6650.0, "fallback"
+
+
+class Flusher:
+    def __init__(self, dev):
+        self.buf = torch.empty(512 * 1024 * 1024 // 4, device=dev, dtype=torch.float32)
+
+    def __call__(self):
+        self.buf.zero_()
+
+
+def graph_time(step, dev, iters, flush):
+    """ms per step of ``step`` captured in a CUDA graph, L2 flushed before every replay
+    (outside the events).  Falls back to eager replays if capture fails (reported)."""
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
     with torch.cuda.stream(side):
         for _ in range(3):
             step()
-    torch.cuda.current_stream(DEV).wait_stream(side)
-    torch.cuda.synchronize(DEV)
-    mode = "eager"
-    g = None
-    if graph:
-        try:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, capture_error_mode="thread_local"):
-                step()
-            g.replay()
-            torch.cuda.synchronize(DEV)
-            mode = "cuda_graph"
-        except Exception as exc:  # noqa: BLE001 - report and fall back to eager timing
-            import traceback
-
-            traceback.print_exc(limit=15)
-            g = None
-            mode = f"eager (capture failed: {type(exc).__name__}: {str(exc)[:160]})"
-            torch.cuda.synchronize(DEV)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(iters):
+    torch.cuda.current_stream(dev).wait_stream(side)
+    torch.cuda.synchronize(dev)
+    mode, g = "cuda_graph", None
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, capture_error_mode="thread_local"):
+            step()
+        g.replay()
+        torch.cuda.synchronize(dev)
+    except Exception as exc:  # noqa: BLE001 - reported in the line
+        g = None
+        mode = f"eager (capture failed: {type(exc).__name__}: {str(exc)[:120]})"
+        torch.cuda.synchronize(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+    for a, b in ev:
+        flush()
+        a.record()
         if g is not None:
             g.replay()
         else:
             step()
-    e1.record()
-    torch.cuda.synchronize(DEV)
-    return e0.elapsed_time(e1) / iters, mode
+        b.record()
+    torch.cuda.synchronize(dev)
+    return sum(a.elapsed_time(b) for a, b in ev) / iters, mode
+
+
+def ledger(step):
+    """Algorithmic bytes / work units of one eager step, per kernel."""
+    ops.ALG_BYTES = []
+    try:
+        step()
+        torch.cuda.synchronize()
+        rec = ops.ALG_BYTES
+    finally:
+        ops.ALG_BYTES = None
+    by = {}
+    for k, nbytes, units in rec:
+        e = by.setdefault(k, {"launches": 0, "bytes": 0, "units": 0})
+        e["launches"] += 1
+        e["bytes"] += nbytes
+        e["units"] += units
+    return sum(e["bytes"] for e in by.values()), by
+
+
+def e2e_time(step_host, dev, iters):
+    """ms per step of the eager public-API step fed from pinned host memory, the loss read
+    back every step (host wall clock around ``iters`` steps after 2 warm-ups)."""
+    for _ in range(2):
+        step_host()
+    torch.cuda.synchronize(dev)
+    t = time.perf_counter()
+    for _ in range(iters):
+        step_host()
+    torch.cuda.synchronize(dev)
+    return (time.perf_counter() - t) * 1e3 / iters
+
+
+def cpu_reference(workload, batch, steps=1, warmup=0, procs=0, **kw):
+    env = dict(os.environ)
+    env["OPENBLAS_NUM_THREADS"] = "1"
+    cmd = [sys.executable, str(ROOT / "tools" / "ref_bench.py"), "--workload", workload, "--batch", str(batch),
+           "--steps", str(steps), "--warmup", str(warmup), "--procs", str(procs)]
+    for k, v in kw.items():
+        cmd += [f"--{k}", str(v)]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600)
+        if out.returncode != 0:
+            return {"value": None, "error": out.stderr[-400:]}
+        r = json.loads(out.stdout.strip().splitlines()[-1])
+        return {k: r[k] for k in ("value", "unit", "seconds_per_step", "cores", "kind", "backend", "sample")}
+    except Exception as exc:  # noqa: BLE001 - reported, not fatal
+        return {"value": None, "error": str(exc)[:300]}
+
+
+def roofline(alg_bytes, by_kernel, ms, hbm, peak_src):
+    gbs = alg_bytes / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "alg_bytes_per_step": alg_bytes, "achieved_gbs": gbs, "peak": hbm, "unit": "GB/s",
+            "frac": gbs / hbm, "peak_source": peak_src, "by_kernel": by_kernel,
+            "method": "sum of per-launch algorithmic bytes (ops.ALG_BYTES, SURVEY 8(d) formulas) / graph-replayed "
+                      "step time with L2 flushed"}
 
 
 def rows(rng, B, n):
@@ -73,203 +151,247 @@ def rows(rng, B, n):
     return (r / r.sum(axis=1, keepdims=True)).astype(np.float32)
 
 
-def emit(d):
-    print(json.dumps(d), flush=True)
-
-
-# ------------------------------------------------------------------ configs 1 / 2: training
-def train_sum(n_digits, B, iters, label):
-    """LeNet perception in bf16 autocast + channels_last (cuDNN autotuned); the softmax
-    outputs and the whole symbolic path are fp32."""
+# ------------------------------------------------------------------ configs[0]: Sum-2 train
+def sum2_train(dev, iters=20, cpu=True, B=64):
+    """LeNet (bf16 autocast, channels_last) on synthetic 28x28 digits -> 2 softmax blocks ->
+    apply(+) (DAMP) -> loss_nll -> backward -> Adam.  The reference arm trains its own Mlp
+    (it has no convolution primitive)."""
     torch.manual_seed(0)
     torch.backends.cudnn.benchmark = True
-    model = LeNet(10).to(DEV).to(memory_format=torch.channels_last)
+    model = LeNet(10).to(dev).to(memory_format=torch.channels_last)
     opt = torch.optim.Adam(model.parameters(), lr=1e-3, capturable=True)
     rng = np.random.default_rng(0)
-    imgs = torch.tensor(rng.normal(size=(n_digits * B, 1, 28, 28)).astype(np.float32), device=DEV)
-    imgs = imgs.to(memory_format=torch.channels_last)
-    targets = torch.tensor(rng.integers(0, 9 * n_digits + 1, size=B), device=DEV)
+    labels = rng.integers(0, 10, size=(2, B))
+    centers = rng.normal(size=(10, 28 * 28))
+    imgs_h = (centers[labels] * (5.0 / 28) + rng.normal(size=(2, B, 28 * 28))).astype(np.float32)
+    imgs_h = torch.tensor(imgs_h.reshape(2 * B, 1, 28, 28))
+    tgt_h = torch.tensor(labels.sum(axis=0))
+    imgs = imgs_h.to(dev).to(memory_format=torch.channels_last)
+    targets = tgt_h.to(dev)
 
-    def step():
+    def step_on(x, t):
         opt.zero_grad(set_to_none=False)
         with torch.autocast("cuda", dtype=torch.bfloat16):
-            probs = model(imgs).float().view(n_digits, B, 10)
-        ctx = sg.ProgramContext(sg.Damp(), device=DEV)
-        out = P.sum_n(ctx, [sg.make_distribution(ctx, probs[i], range(10)) for i in range(n_digits)])
-        loss = loss_nll(sg.get_probs(out), targets)
+            probs = model(x).float().view(2, B, 10)
+        ctx = sg.ProgramContext(sg.Damp(), device=dev)
+        out = P.sum_n(ctx, [sg.make_distribution(ctx, probs[i], range(10)) for i in range(2)])
+        loss = loss_nll(sg.get_probs(out), t)
         loss.backward()
         opt.step()
         return loss
 
-    ms, mode = timed(step, iters)
-    emit({"config": label, "metric": "train samples/s", "value": B / (ms * 1e-3), "ms_per_step": ms, "batch": B,
-          "mode": mode, "perception": "LeNet-5 (synthetic 28x28), bf16 autocast + channels_last",
-          "optimizer": "Adam", "symbolic_dtype": "f32"})
+    flush = Flusher(dev)
+    ms, mode = graph_time(lambda: step_on(imgs, targets), dev, iters, flush)
+    alg, by = ledger(lambda: step_on(imgs, targets))
+    pin_x, pin_t = imgs_h.pin_memory(), tgt_h.pin_memory()
+
+    def host_step():
+        x = pin_x.to(dev, non_blocking=True).to(memory_format=torch.channels_last)
+        loss = step_on(x, pin_t.to(dev, non_blocking=True))
+        return loss.item()
+
+    e2e_ms = e2e_time(host_step, dev, iters)
+    hbm, src = hbm_peak()
+    res = {"config": "MNIST Sum-2 train: synthetic 28x28 digits, random-init LeNet, DAMP, B=64 (BASELINE configs[0])",
+           "metric": "train samples/s", "batch": B,
+           "device": {"ms_per_step": ms, "value": B / (ms * 1e-3), "mode": mode},
+           "e2e": {"ms_per_step": e2e_ms, "value": B / (e2e_ms * 1e-3), "h2d_bytes_per_step": pin_x.numel() * 4 + B * 8,
+                   "d2h_bytes_per_step": 8, "api": "eager: LeNet -> make_distribution -> sum_n -> get_probs -> "
+                                                   "loss_nll -> backward -> Adam, images H2D + loss.item() per step"},
+           "roofline": roofline(alg, by, ms, hbm, src) | {"note": "symbolic kernels only; the step is launch-bound "
+                                                                  "(LeNet + Adam dominate)"}}
+    if cpu:
+        res["cpu"] = cpu_reference("sum2train", B, steps=10, warmup=2, procs=1)
+    return res
 
 
-# ------------------------------------------------------------------ config 3: HWF-7 DTKP k=3
-def hwf7(B, iters):
+# ------------------------------------------------------------------ configs[2]: HWF-7
+def hwf7(dev, iters=20, cpu=True, B=64):
     rng = np.random.default_rng(1)
-    xs = [torch.tensor(rows(rng, B, 14), device=DEV, requires_grad=True) for _ in range(7)]
+    xs_h = torch.tensor(np.stack([rows(rng, B, 14) for _ in range(7)]))
+    xs = [xs_h[i].to(dev).requires_grad_(True) for i in range(7)]
     t0 = time.perf_counter()
-    ctx = sg.ProgramContext(sg.DtkpAm(3), device=DEV)
+    ctx = sg.ProgramContext(sg.DtkpAm(3), device=dev)
     out = P.hwf(ctx, [sg.make_distribution(ctx, x, P.TOKEN_ALPHABET) for x in xs], 7)
-    torch.cuda.synchronize(DEV)
+    torch.cuda.synchronize(dev)
     first = time.perf_counter() - t0
     n_out = len(out)
-    del out, ctx  # drop the first call's autograd graph (its AccumulateGrad nodes live on the default stream)
-    targets = torch.tensor(rng.integers(0, n_out, size=B), device=DEV)
-    combos = 0
-    from paper_2410_03348_b200.plan import plan_cache_info
+    del out, ctx
+    tgt_h = torch.tensor(rng.integers(0, n_out, size=B))
+    targets = tgt_h.to(dev)
 
-    def step():
-        c = sg.ProgramContext(sg.DtkpAm(3), device=DEV)
-        o = P.hwf(c, [sg.make_distribution(c, x, P.TOKEN_ALPHABET) for x in xs], 7)
-        loss = loss_nll(sg.get_probs(o), targets)
-        return torch.autograd.grad(loss, xs)
+    def step_on(xl, t):
+        c = sg.ProgramContext(sg.DtkpAm(3), device=dev)
+        o = P.hwf(c, [sg.make_distribution(c, x, P.TOKEN_ALPHABET) for x in xl], 7)
+        loss = loss_nll(sg.get_probs(o), t)
+        return loss, torch.autograd.grad(loss, xl)
 
-    ms, mode = timed(step, iters)
-    sizes = [(10,), (10, 4), (40, 10), (283, 4), (1132, 10), (7678, 4), (30712, 10), (208767,)]
-    combos = sum(int(np.prod(s)) for s in sizes)
-    emit({"config": "HWF-7 DTKP k=3 (BASELINE configs[2])", "metric": "samples/s (symbolic fwd+bwd)",
-          "value": B / (ms * 1e-3), "ms_per_step": ms, "batch": B, "mode": mode, "output_symbols": n_out,
-          "symbol_combos_per_s": B * combos / (ms * 1e-3), "first_call_s_incl_host_plans": first,
-          "plan_cache": plan_cache_info()})
+    flush = Flusher(dev)
+    ms, mode = graph_time(lambda: step_on(xs, targets), dev, iters, flush)
+    alg, by = ledger(lambda: step_on(xs, targets))
+    pin_x, pin_t = xs_h.pin_memory(), tgt_h.pin_memory()
+
+    def host_step():
+        xd = pin_x.to(dev, non_blocking=True)
+        loss, _ = step_on([xd[i].requires_grad_(True) for i in range(7)], pin_t.to(dev, non_blocking=True))
+        return loss.item()
+
+    e2e_ms = e2e_time(host_step, dev, max(3, iters // 2))
+    hbm, src = hbm_peak()
+    combos = sum(int(np.prod(s)) for s in HWF7_SIZES)
+    cand = by.get("dtkp_apply", {}).get("units", 0)
+    res = {"config": "HWF-7 formula eval, DTKP k=3, B=64 (BASELINE configs[2])", "metric": "samples/s (symbolic "
+           "fwd+loss+bwd)", "batch": B, "output_symbols": n_out,
+           "device": {"ms_per_step": ms, "value": B / (ms * 1e-3), "symbol_combos_per_s": B * combos / (ms * 1e-3),
+                      "candidate_rows_per_s": cand / (ms * 1e-3), "mode": mode},
+           "e2e": {"ms_per_step": e2e_ms, "value": B / (e2e_ms * 1e-3), "h2d_bytes_per_step": pin_x.numel() * 4 + B * 8,
+                   "d2h_bytes_per_step": 8, "api": "eager programs.hwf (memoised plans) + loss_nll + autograd.grad, "
+                                                   "inputs H2D + loss.item() per step"},
+           "first_call_s_incl_host_plans": first,
+           "roofline": roofline(alg, by, ms, hbm, src)}
+    if cpu:
+        res["cpu"] = cpu_reference("hwf7", B, steps=1, warmup=0)
+    return res
 
 
-# ------------------------------------------------------------------ config 4: CLUTRR-style
-def clutrr(B, iters, n_entities=5, k=5):
-    sys.path.insert(0, str(ROOT / "tests"))
-    from golden_cases import clutrr_facts
+# ------------------------------------------------------------------ configs[3]: CLUTRR-style
+def clutrr(dev, iters=20, cpu=True, B=4096, n_entities=5, k=5):
+    from paper_2410_03348_b200.kinship import story_facts
 
     rng = np.random.default_rng(2)
-    facts = clutrr_facts(n_entities)
-    x = torch.tensor(rng.uniform(0.05, 0.95, size=(B, len(facts))).astype(np.float32), device=DEV,
-                     requires_grad=True)
-    t0 = time.perf_counter()
-    ctx = sg.ProgramContext(sg.DtkpAm(k), device=DEV)
+    facts = story_facts(n_entities)
+    x_h = torch.tensor(rng.uniform(0.05, 0.95, size=(B, len(facts))).astype(np.float32))
+    x = x_h.to(dev).requires_grad_(True)
+    ctx = sg.ProgramContext(sg.DtkpAm(k), device=dev)
     out = P.clutrr_closure(ctx, sg.make_distribution(ctx, x, facts))
-    torch.cuda.synchronize(DEV)
-    first = time.perf_counter() - t0
-    targets = torch.tensor(rng.integers(0, len(out), size=B), device=DEV)
     n_derived = len(out)
     del out, ctx
+    tgt_h = torch.tensor(rng.integers(0, n_derived, size=B))
+    targets = tgt_h.to(dev)
 
-    def step():
-        c = sg.ProgramContext(sg.DtkpAm(k), device=DEV)
-        o = P.clutrr_closure(c, sg.make_distribution(c, x, facts))
-        loss = loss_nll(sg.get_probs(o), targets)
-        return torch.autograd.grad(loss, [x])
+    def step_on(xv, t):
+        c = sg.ProgramContext(sg.DtkpAm(k), device=dev)
+        o = P.clutrr_closure(c, sg.make_distribution(c, xv, facts))
+        loss = loss_nll(sg.get_probs(o), t)
+        return loss, torch.autograd.grad(loss, [xv])
 
-    ms, mode = timed(step, iters)
-    emit({"config": f"CLUTRR-style kinship closure, {n_entities} entities x 20 relations, DTKP k={k} "
-                    "(BASELINE configs[3])", "metric": "samples/s (symbolic fwd+bwd)", "value": B / (ms * 1e-3),
-          "ms_per_step": ms, "batch": B, "mode": mode, "derived_facts": n_derived, "input_facts": len(facts),
-          "first_call_s_incl_host_plans": first})
+    flush = Flusher(dev)
+    ms, mode = graph_time(lambda: step_on(x, targets), dev, iters, flush)
+    alg, by = ledger(lambda: step_on(x, targets))
+    pin_x, pin_t = x_h.pin_memory(), tgt_h.pin_memory()
 
+    def host_step():
+        loss, _ = step_on(pin_x.to(dev, non_blocking=True).requires_grad_(True), pin_t.to(dev, non_blocking=True))
+        return loss.item()
 
-# ------------------------------------------------------------------ config 5: sweep
-def sweep(iters):
-    for arity, size in [(2, 10), (2, 100), (2, 1000), (3, 10), (3, 30), (3, 100)]:
-        for B in (1024, 16384, 65536):
-            if arity == 3 and size == 100 and B > 16384:
-                continue
-            rng = np.random.default_rng(size + B)
-            xs = [torch.tensor(rows(rng, B, size), device=DEV, requires_grad=True) for _ in range(arity)]
-            syms = list(range(size))
-            f = (lambda a, b: a + b) if arity == 2 else (lambda a, b, c: a + b + c)
-            n_out = arity * (size - 1) + 1
-            w = torch.tensor(rng.uniform(-1, 1, size=(B, n_out)).astype(np.float32), device=DEV)
-
-            def fwd():
-                c = sg.ProgramContext(sg.Damp(), device=DEV)
-                return sg.get_probs(sg.apply(f, *[sg.make_distribution(c, x, syms) for x in xs]))
-
-            def step():  # d(sum probs * w)/dx: the upstream gradient w goes straight in
-                return torch.autograd.grad(fwd(), xs, grad_outputs=w)
-
-            ms_f, mode = timed(lambda: fwd(), iters)
-            ms, _ = timed(step, iters)
-            C = size ** arity
-            fb = 4 * B * (arity * size + n_out) + 4 * C
-            bb = 4 * B * (n_out + 2 * arity * size) + 4 * C
-            kp = sg.plan.build_plan(f, None, [tuple(syms)] * arity).kernel_plan()
-            emit({"config": f"sweep arity {arity} |S|={size} f=sum B={B} (BASELINE configs[4])",
-                  "path": "toeplitz" if kp.conv else "generic segmented", "batch": B,
-                  "fwd_ms": ms_f, "fwd_bwd_ms": ms, "combos_per_s_fwd": B * C / (ms_f * 1e-3),
-                  "combos_per_s_fwd_bwd": B * C / (ms * 1e-3),
-                  "fwd_algorithmic_gbs": fb / (ms_f * 1e-3) / 1e9, "fwd_hbm_frac": fb / (ms_f * 1e-3) / 1e9 / HBM,
-                  "fwd_bwd_algorithmic_gbs": (fb + bb) / (ms * 1e-3) / 1e9,
-                  "fwd_bwd_hbm_frac": (fb + bb) / (ms * 1e-3) / 1e9 / HBM, "mode": mode})
-            del xs, w
-            torch.cuda.empty_cache()
+    e2e_ms = e2e_time(host_step, dev, iters)
+    hbm, src = hbm_peak()
+    cand = by.get("dtkp_apply", {}).get("units", 0)
+    res = {"config": f"CLUTRR-style kinship closure, {n_entities} entities x 20 relations, DTKP k={k}, B={B} "
+                     "(BASELINE configs[3])", "metric": "samples/s (symbolic fwd+loss+bwd)", "batch": B,
+           "derived_facts": n_derived,
+           "device": {"ms_per_step": ms, "value": B / (ms * 1e-3), "candidate_rows_per_s": cand / (ms * 1e-3),
+                      "mode": mode},
+           "e2e": {"ms_per_step": e2e_ms, "value": B / (e2e_ms * 1e-3), "h2d_bytes_per_step": pin_x.numel() * 4 + B * 8,
+                   "d2h_bytes_per_step": 8, "api": "eager clutrr_closure (fixpoint.closure) + loss_nll + autograd.grad,"
+                                                   " inputs H2D + loss.item() per step"},
+           "roofline": roofline(alg, by, ms, hbm, src)}
+    if cpu:
+        res["cpu"] = cpu_reference("clutrr", B, steps=1, warmup=0)
+    return res
 
 
-# ------------------------------------------------------------------ max-product variant
-def maxsweep(iters):
-    """The max/DAMP variant (sg_maxprod_*) on sweep shapes and the Sum-15 chain."""
-    cases = [(2, 10, 16384), (2, 10, 65536), (2, 100, 16384), (3, 10, 16384)]
-    for arity, size, B in cases:
-        rng = np.random.default_rng(7 * size + B)
-        xs = [torch.tensor(rows(rng, B, size), device=DEV, requires_grad=True) for _ in range(arity)]
-        syms = list(range(size))
-        f = (lambda a, b: a + b) if arity == 2 else (lambda a, b, c: a + b + c)
-        n_out = arity * (size - 1) + 1
-        w = torch.tensor(rng.uniform(-1, 1, size=(B, n_out)).astype(np.float32), device=DEV)
+# ------------------------------------------------------------------ configs[4]: sweep
+SWEEP = [(2, 10, 65536), (2, 10, 16384), (2, 100, 16384), (2, 1000, 16384), (3, 10, 16384), (3, 100, 16384)]
+SWEEP_CPU_BATCH = {(2, 10): 16384, (2, 100): 2048, (2, 1000): 64, (3, 10): 2048, (3, 100): 16}
 
-        def fwd():
-            c = sg.ProgramContext(sg.DampMax(), device=DEV)
-            return sg.get_probs(sg.apply(f, *[sg.make_distribution(c, x, syms) for x in xs]))
 
-        def step():
-            return torch.autograd.grad(fwd(), xs, grad_outputs=w)
+def sweep_point(dev, arity, size, B, iters=20, cpu=True, provenance="damp"):
+    rng = np.random.default_rng(size + B)
+    xs_h = torch.tensor(np.stack([rows(rng, B, size) for _ in range(arity)]))
+    xs = [xs_h[i].to(dev).requires_grad_(True) for i in range(arity)]
+    syms = list(range(size))
+    f = (lambda a, b: a + b) if arity == 2 else (lambda a, b, c: a + b + c)
+    n_out = arity * (size - 1) + 1
+    w_h = torch.tensor(rng.uniform(-1, 1, size=(B, n_out)).astype(np.float32))
+    w = w_h.to(dev)
+    prov = sg.Damp if provenance == "damp" else sg.DampMax
 
-        ms_f, mode = timed(lambda: fwd(), iters)
-        ms, _ = timed(step, iters)
-        C = size ** arity
-        fb = 4 * B * (arity * size + 2 * n_out)           # inputs + probs + argmax
-        bb = 4 * B * (2 * n_out + 2 * arity * size)       # g + argmax + inputs + grads
-        emit({"config": f"max variant: sweep arity {arity} |S|={size} f=sum B={B}", "batch": B,
-              "fwd_ms": ms_f, "fwd_bwd_ms": ms, "combos_per_s_fwd": B * C / (ms_f * 1e-3),
-              "combos_per_s_fwd_bwd": B * C / (ms * 1e-3),
-              "fwd_hbm_frac": fb / (ms_f * 1e-3) / 1e9 / HBM, "fwd_bwd_hbm_frac": (fb + bb) / (ms * 1e-3) / 1e9 / HBM,
-              "mode": mode})
-        del xs, w
-        torch.cuda.empty_cache()
-    B = 16384
-    rng = np.random.default_rng(15)
-    xs = [torch.tensor(rows(rng, B, 10), device=DEV, requires_grad=True) for _ in range(15)]
-    targets = torch.tensor(rng.integers(0, 136, size=B), device=DEV)
+    def step_on(xl, wv):  # d(sum probs * w)/dx: the upstream gradient w goes straight in
+        c = sg.ProgramContext(prov(), device=dev)
+        p = sg.get_probs(sg.apply(f, *[sg.make_distribution(c, x, syms) for x in xl]))
+        return p, torch.autograd.grad(p, xl, grad_outputs=wv)
 
-    def step15():
-        c = sg.ProgramContext(sg.DampMax(), device=DEV)
-        o = P.sum_n(c, [sg.make_distribution(c, x, list(range(10))) for x in xs])
-        return torch.autograd.grad(loss_nll(sg.get_probs(o), targets), xs)
+    def fwd_only():
+        c = sg.ProgramContext(prov(), device=dev)
+        return sg.get_probs(sg.apply(f, *[sg.make_distribution(c, x.detach(), syms) for x in xs]))
 
-    ms, mode = timed(step15, iters)
-    emit({"config": "max variant: Sum-15 chain B=16384 (14 max-product applies) + loss, fwd+bwd",
-          "ms_per_step": ms, "combos_per_s": B * 9590 / (ms * 1e-3), "mode": mode})
+    flush = Flusher(dev)
+    ms_f, mode = graph_time(fwd_only, dev, iters, flush)
+    ms, _ = graph_time(lambda: step_on(xs, w), dev, iters, flush)
+    alg, by = ledger(lambda: step_on(xs, w))
+    alg_f, _ = ledger(fwd_only)
+    pin_x, pin_w = xs_h.pin_memory(), w_h.pin_memory()
+    out_h = torch.empty((B, n_out), dtype=torch.float32).pin_memory()
+
+    def host_step():
+        xd = pin_x.to(dev, non_blocking=True)
+        p, _ = step_on([xd[i].requires_grad_(True) for i in range(arity)], pin_w.to(dev, non_blocking=True))
+        out_h.copy_(p.detach(), non_blocking=True)  # the step's result back to the host
+        torch.cuda.current_stream(dev).synchronize()
+
+    e2e_ms = e2e_time(host_step, dev, iters)
+    C = size ** arity
+    kp = sg.plan.build_plan(f, None, [tuple(syms)] * arity).kernel_plan()
+    hbm, src = hbm_peak()
+    res = {"config": f"sweep arity {arity} |S|={size} f=sum B={B} ({provenance}, BASELINE configs[4])",
+           "metric": "symbol-combos/s (fwd+bwd)", "batch": B, "path": "toeplitz" if kp.conv else "generic segmented",
+           "bound": "hbm" if (arity, size) == (2, 10) else "issue/FMA (SURVEY 8(d): >= 4 combos/byte)",
+           "device": {"ms_per_step": ms, "value": B * C / (ms * 1e-3), "fwd_ms": ms_f,
+                      "fwd_combos_per_s": B * C / (ms_f * 1e-3), "mode": mode,
+                      "fwd_hbm_frac": alg_f / (ms_f * 1e-3) / 1e9 / hbm},
+           "e2e": {"ms_per_step": e2e_ms, "value": B * C / (e2e_ms * 1e-3),
+                   "h2d_bytes_per_step": pin_x.numel() * 4 + pin_w.numel() * 4, "d2h_bytes_per_step": out_h.numel() * 4,
+                   "api": "eager make_distribution/apply/get_probs + autograd.grad(grad_outputs=w), inputs + w H2D, "
+                          "probs D2H per step"},
+           "roofline": roofline(alg, by, ms, hbm, src)}
+    if cpu and provenance == "damp":
+        cb = SWEEP_CPU_BATCH.get((arity, size))
+        if cb:
+            res["cpu"] = cpu_reference("sweep", cb, steps=2, warmup=1, arity=arity, size=size)
+    del xs, w
+    torch.cuda.empty_cache()
+    return res
+
+
+def all_configs(dev, iters=20, cpu=True, only=("sum2", "hwf7", "clutrr", "sweep")):
+    out = {}
+    if "sum2" in only:
+        out["sum2_train"] = sum2_train(dev, iters, cpu)
+    if "hwf7" in only:
+        out["hwf7"] = hwf7(dev, iters, cpu)
+    if "clutrr" in only:
+        out["clutrr"] = clutrr(dev, iters, cpu)
+    if "sweep" in only:
+        for a, s, b in SWEEP:
+            out[f"sweep_a{a}_s{s}_b{b}"] = sweep_point(dev, a, s, b, iters, cpu)
+    if "maxsweep" in only:
+        for a, s, b in [(2, 10, 65536), (2, 100, 16384), (3, 10, 16384)]:
+            out[f"max_sweep_a{a}_s{s}_b{b}"] = sweep_point(dev, a, s, b, iters, False, provenance="max")
+    return out
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="sum2,sum15train,hwf7,clutrr,sweep,maxsweep")
+    ap.add_argument("--only", default="sum2,hwf7,clutrr,sweep")
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
-    torch.cuda.set_device(DEV)
-    only = set(args.only.split(","))
-    if "sum2" in only:
-        train_sum(2, 64, args.iters, "MNIST Sum-2 train, B=64, LeNet + DAMP (BASELINE configs[0])")
-    if "sum15train" in only:
-        train_sum(15, 16384, max(3, args.iters // 4), "MNIST Sum-15 train, B=16384, LeNet + DAMP (BASELINE configs[1])")
-    if "hwf7" in only:
-        hwf7(64, args.iters)
-    if "clutrr" in only:
-        clutrr(4096, args.iters)
-    if "sweep" in only:
-        sweep(args.iters)
-    if "maxsweep" in only:
-        maxsweep(args.iters)
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    res = all_configs(dev, args.iters, not args.no_cpu, tuple(args.only.split(",")))
+    for k, v in res.items():
+        print(json.dumps({"key": k, **v}), flush=True)
 
 
 if __name__ == "__main__":
