@@ -228,6 +228,21 @@ typedef struct sg_dtkp_apply_desc {
   sg_segsum merge2;
   uint64_t* scratch2_member; /* [merge.n_partial][K][W][B] */
   uint8_t* scratch2_present; /* [merge.n_partial][K][B]    */
+  /* Fused conj -> group_disj (arity == 1 only; inner_arity == 0 disables it).  The single
+   * operand of this apply is the output of an arity-2 apply that is never materialised —
+   * HWF's final eval over the 208767 formulas of its last concat step
+   * (programs.py:117-145): operand row r is computed on the fly as that apply's output
+   * segment r, i.e. its records inner_recs[inner_off[r] .. inner_off[r+1]) (inner_rec_words
+   * ints each: the rows of inner_ops[0] and inner_ops[1]) conjoined pairwise with
+   * per-record normalisation and streamed through a top-k (provenance.py:328-341 then
+   * :352-364), exactly the rows sg_dtkp_apply with arity 2 would write.  ops[0] and
+   * op_tail are not read.  Bit-identical to the two launches; the intermediate tag never
+   * touches HBM.                                                                         */
+  int32_t inner_arity;
+  int32_t inner_rec_words;
+  sg_dtkp_operand inner_ops[2];
+  const int32_t* inner_recs;  /* [n_inner_records][inner_rec_words] in output-segment order */
+  const int32_t* inner_off;   /* [ops[0].rows + 1] segment offsets into inner_recs           */
 } sg_dtkp_apply_desc;
 
 int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream);

@@ -84,6 +84,30 @@ __device__ __forceinline__ void cp_async4z(float* dst, const float* src, int src
 __device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+// per-lane L1 prefetch of a contiguous range (lines lane, lane + 32, ...): the backward's
+// next-step state block lands in L1 (free: the chain kernels leave most of it to L1),
+// so the v_{i-1} row loads of a round hit L1 instead of waiting on L2 under load
+__device__ __forceinline__ void prefetch_l1_range(const void* p, unsigned bytes, int lane) {
+  const char* c = reinterpret_cast<const char*>(p);
+  for (unsigned o = (unsigned)lane * 128u; o < bytes; o += 32u * 128u)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(c + o));
+}
+#ifndef SG_CHAIN_L1PF
+#define SG_CHAIN_L1PF 1
+#endif
+#ifndef SG_CHAIN_SATFMA
+#define SG_CHAIN_SATFMA 1
+#endif
+// last tap of a forward output as two scalar fma.rn.sat (round, then clamp to [0, 1];
+// NaN -> +0 like clamp01): bit-identical to ffma2 followed by clamp01x2, 2 instructions
+// instead of 5 (FFMA2 + four FMNMX)
+__device__ __forceinline__ float2 ffma2_sat(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d.x) : "f"(a.x), "f"(b.x), "f"(c.x));
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d.y) : "f"(a.y), "f"(b.y), "f"(c.y));
+  return d;
+}
+
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_ring() { asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 2) : "memory"); }
@@ -165,14 +189,20 @@ __device__ __forceinline__ void stage_filter(float2* F, int slot, const CRows& S
 
 // acc[r] = sum_{j ascending} w[r + KF-1-j] * f[j] (the k_conv_fwd order), computed j
 // outer / r inner so the R accumulators are independent back-to-back FFMA2s.
-template <int KF, int R>
+template <int KF, int R, bool SAT = false>
 __device__ __forceinline__ void conv_tile(float2 (&acc)[R], const float2 (&w)[R + KF - 1], const float2 (&f)[KF]) {
+  if constexpr (SAT && KF == 1) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = ffma2_sat(w[r + KF - 1], f[0], zero2());
+    return;
+  }
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r] = __fmul2_rn(w[r + KF - 1], f[0]);  // == fma(w, f, 0)
 #pragma unroll
   for (int j = 1; j < KF; ++j)
 #pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = ffma2(w[r + KF - 1 - j], f[j], acc[r]);
+    for (int r = 0; r < R; ++r)
+      acc[r] = (SAT && j == KF - 1) ? ffma2_sat(w[r + KF - 1 - j], f[j], acc[r]) : ffma2(w[r + KF - 1 - j], f[j], acc[r]);
 }
 
 __host__ __device__ constexpr int round_up(int a, int r) { return (a + r - 1) / r * r; }
@@ -209,12 +239,12 @@ __device__ __forceinline__ void fwd_round(const float2 (&w)[R + KF - 1], const f
                                           float2* gst, int o0, int nout, bool last, const ChainArgs& a,
                                           const Lane& L, double2& rsum) {
   float2 acc[R];
-  conv_tile<KF, R>(acc, w, f);
+  conv_tile<KF, R, SG_CHAIN_SATFMA != 0>(acc, w, f);  // SAT: acc is already clamp01'ed
   __syncwarp();  // every group's window (this round's and the next's) is loaded before any store
   if (!last) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const float2 v = clamp01x2(acc[r]);
+      const float2 v = SG_CHAIN_SATFMA ? acc[r] : clamp01x2(acc[r]);
       v0[(o0 + r) * kCP] = v;  // padded rows >= nout get clamp01(0) = 0
 #ifndef SG_CHAIN_NOSTORE
       if (o0 + r < nout) gst[(o0 + r) * (kCWS / 2)] = v;
@@ -225,7 +255,7 @@ __device__ __forceinline__ void fwd_round(const float2 (&w)[R + KF - 1], const f
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if (o0 + r < nout) {
-        const float2 v = clamp01x2(acc[r]);
+        const float2 v = SG_CHAIN_SATFMA ? acc[r] : clamp01x2(acc[r]);
         st_rowmajor<VEC>(q, L, v);
         rsum.x += (double)v.x;  // per-sample sum of the output row (the loss' normaliser)
         rsum.y += (double)v.y;
@@ -465,6 +495,9 @@ __global__ void __launch_bounds__(32) k_chain_bwd(const ChainArgs a) {
     load_prev<R, true>(pv, a, sblk, L, a.m, L.g * R);
   if (a.m > 2 && (threadIdx.x & 31) == 0)
     prefetch_l2_bulk(sblk - L.c + (size_t)a.state_off[a.m - 2] * (kCWS / 2), a.n[a.m - 2] * kCWS * 4);
+  if (SG_CHAIN_L1PF && a.m > 1)  // v_{m-1}, read by this first step, -> L1
+    prefetch_l1_range(sblk - L.c + (size_t)a.state_off[a.m - 1] * (kCWS / 2), a.n[a.m - 1] * kCWS * 4,
+                      threadIdx.x & 31);
   cp_wait_all();
   __syncwarp();
   for (int t = 0; t < a.m; ++t) {
@@ -482,6 +515,9 @@ __global__ void __launch_bounds__(32) k_chain_bwd(const ChainArgs a) {
     }
     if (i > 3 && (threadIdx.x & 31) == 0)  // v_{i-3} (read in step i-2) -> L2
       prefetch_l2_bulk(sblk - L.c + (size_t)a.state_off[i - 3] * (kCWS / 2), a.n[i - 3] * kCWS * 4);
+    if (SG_CHAIN_L1PF && i > 2)  // v_{i-2} (read in step i-1) -> L1 one step ahead
+      prefetch_l1_range(sblk - L.c + (size_t)a.state_off[i - 2] * (kCWS / 2), a.n[i - 2] * kCWS * 4,
+                        threadIdx.x & 31);
     if (i > 1)
       bwd_step<KF, R, false>(G + L.c, scratch + L.c, f, pv, i, a, sblk, L);
     else

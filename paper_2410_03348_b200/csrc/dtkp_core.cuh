@@ -17,6 +17,9 @@
 #ifndef SG_DTKP_STREAM_PREFETCH  // streaming (arity-1) kernel loads the next record ahead
 #define SG_DTKP_STREAM_PREFETCH 0
 #endif
+#ifndef SG_DTKP_FUSED_MINB  // resident CTAs/SM asked of the fused conj -> group_disj (K <= 3)
+#define SG_DTKP_FUSED_MINB 4
+#endif
 #ifndef SG_DTKP_UNROLL_K
 #define SG_DTKP_UNROLL_K 4
 #endif
@@ -179,6 +182,11 @@ struct DtkpK {
   uint8_t* out_p;
   uint64_t* scr_m;
   uint8_t* scr_p;
+  // fused conj -> group_disj (AR == 3): operand row r = inner segment r, computed on the fly
+  sg_dtkp_operand inner[2];
+  const int32_t* inner_recs;
+  const int32_t* inner_off;
+  int32_t inner_rec_words;
 };
 
 template <int WT>
@@ -231,10 +239,50 @@ struct TagRows {
 
 __device__ __forceinline__ int rec_row(const DtkpK& a, int c, int i) { return __ldg(a.recs + (size_t)c * a.rec_words + i); }
 
+// T = normalise(conj(A, Bt)): all present row pairs OR-ed in candidate order ra*kb + rb,
+// dedup + top-k (provenance.py:328-341 -> _normalize :366-379).
+template <int K, int WT>
+__device__ __forceinline__ void conj_pairs(TopK<K, WT>& T, const TagRows<K, WT>& A, const TagRows<K, WT>& Bt,
+                                           const PCol& pc) {
+  constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
+  T.clear();
+#pragma unroll (kUnrollK)
+  for (int qa = 0; qa < K; ++qa) {
+    if (!((A.pres >> qa) & 1u)) continue;
+    uint64_t ma[WT];
+    A.row(qa, ma);
+#pragma unroll (kUnrollK)
+    for (int qb = 0; qb < K; ++qb) {
+      if (!((Bt.pres >> qb) & 1u)) continue;
+      uint64_t mm[WT];
+      Bt.row(qb, mm);
+#pragma unroll
+      for (int w = 0; w < WT; ++w) mm[w] |= ma[w];
+      T.insert(mm, proof_key<WT>(mm, pc), 0);
+    }
+  }
+}
+
+// Stream the retained rows of T (rank order) into S: the group_disj of a column of tags
+// (same mask, same p -> same key as a recomputation, so the key is reused).
+template <int K, int WT>
+__device__ __forceinline__ void stream_rows(TopK<K, WT>& S, const TopK<K, WT>& T) {
+  constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
+#pragma unroll (kUnrollK)
+  for (int q = 0; q < K; ++q) {
+    if (q >= T.n) break;
+    uint64_t mm[WT];
+    double kk;
+    T.get(q, mm, kk);
+    S.insert(mm, kk, 0);
+  }
+}
+
 // One work item (an output segment, or a piece of a split one) for one sample: stream its
 // records through the top-k set and write the retained rows.
 // AR: 1 = union / group_disj streaming, 2 = binary conj fold, 0 = conj fold of >= 3
-// operands.  Each is its own kernel, so the streaming kernel does not carry the
+// operands, 3 = group_disj whose operand rows are binary-conj outputs computed on the fly
+// (the fused conj -> group_disj of sg_dtkp_apply_desc.inner_*).  Each is its own kernel, so the streaming kernel does not carry the
 // conj fold's registers (occupancy) or code (instruction cache).
 template <int K, int WT, int AR>
 __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, int64_t b0, bool bval, const PCol& pc) {
@@ -271,6 +319,27 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
           fetch(c + 1, cur);
       }
     }
+  } else if constexpr (AR == 3) {
+    // fused conj -> group_disj: each record is an intermediate symbol s whose tag is the
+    // top-k over its own conj records (what an arity-2 apply writes as row s); its rows
+    // stream into this item's top-k in rank order, as the group_disj of the materialised
+    // tag would read them
+    for (int c = item.y; c < item.z; ++c) {
+      const int s = rec_row(a, c, 0);
+      const int r0 = __ldg(a.inner_off + s), r1 = __ldg(a.inner_off + s + 1);
+      TopK<K, WT> M;
+      M.clear();
+      for (int cc = r0; cc < r1; ++cc) {
+        const int* rr = a.inner_recs + (size_t)cc * a.inner_rec_words;
+        TagRows<K, WT> A, Bt;
+        A.load(a.inner[0], a.B, b, __ldg(rr));
+        Bt.load(a.inner[1], a.B, b, __ldg(rr + 1));
+        TopK<K, WT> T;
+        conj_pairs<K, WT>(T, A, Bt, pc);
+        stream_rows<K, WT>(M, T);
+      }
+      stream_rows<K, WT>(S, M);
+    }
   } else {
     // conj fold, normalised after every step (candidate order ra*kb + rb)
     TagRows<K, WT> A, Bt, An, Bn;
@@ -287,22 +356,7 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
         Bn.load(a.ops[1], a.B, b, rec_row(a, c + 1, 1));
       }
       TopK<K, WT> T;
-      T.clear();
-#pragma unroll (kUnrollK)
-      for (int qa = 0; qa < K; ++qa) {
-        if (!((A.pres >> qa) & 1u)) continue;
-        uint64_t ma[WT];
-        A.row(qa, ma);
-#pragma unroll (kUnrollK)
-        for (int qb = 0; qb < K; ++qb) {
-          if (!((Bt.pres >> qb) & 1u)) continue;
-          uint64_t mm[WT];
-          Bt.row(qb, mm);
-#pragma unroll
-          for (int w = 0; w < WT; ++w) mm[w] |= ma[w];
-          T.insert(mm, proof_key<WT>(mm, pc), 0);
-        }
-      }
+      conj_pairs<K, WT>(T, A, Bt, pc);
 #pragma unroll 1
       for (int i = 2; AR != 2 && i < a.arity; ++i) {
         TagRows<K, WT> Ci;
@@ -327,14 +381,7 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
         }
         T = U;
       }
-#pragma unroll (kUnrollK)
-      for (int q = 0; q < K; ++q) {
-        if (q >= T.n) break;
-        uint64_t mm[WT];
-        double kk;
-        T.get(q, mm, kk);
-        S.insert(mm, kk, 0);  // same mask, same p -> same key as a recomputation
-      }
+      stream_rows<K, WT>(S, T);
       if (more) {
         if constexpr (kPf) {
           A = An;
@@ -372,7 +419,8 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
 __host__ __device__ constexpr int dtkp_min_blocks(int K, int WT, int AR) {
   return SG_DTKP_MINB > 0 ? SG_DTKP_MINB
          : (WT <= 2 && K <= 3) ? (AR == 1 ? (SG_DTKP_STREAM_PREFETCH ? 5 : 6)
-                                  : AR == 2 ? (K > SG_DTKP_CONJ_PREFETCH_MAXK ? 5 : 4) : 1)
+                                  : AR == 2 ? (K > SG_DTKP_CONJ_PREFETCH_MAXK ? 5 : 4)
+                                  : AR == 3 ? SG_DTKP_FUSED_MINB : 1)
          : (WT <= 2 && K <= 5 && AR == 1) ? (SG_DTKP_STREAM_PREFETCH ? 4 : 5)
          : (WT <= 2 && K <= 5 && AR == 2 && K > SG_DTKP_CONJ_PREFETCH_MAXK) ? 3
          : 1;
@@ -454,6 +502,7 @@ static int launch_apply_kwa(const DtkpK& k, int n_blocks, cudaStream_t st) {
 
 template <int K, int WT>
 static int launch_apply_kw(const DtkpK& k, int n_blocks, cudaStream_t st) {
+  if (k.arity == 1 && k.inner_recs != nullptr) return launch_apply_kwa<K, WT, 3>(k, n_blocks, st);
   if (k.arity == 1) return launch_apply_kwa<K, WT, 1>(k, n_blocks, st);
   if (k.arity == 2) return launch_apply_kwa<K, WT, 2>(k, n_blocks, st);
   return launch_apply_kwa<K, WT, 0>(k, n_blocks, st);

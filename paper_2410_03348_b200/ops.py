@@ -489,8 +489,11 @@ def dtkp_sched(device, n: int) -> torch.Tensor:
 
 
 def dtkp_apply(kplan_host, dseg, dmerge, operands, tail, K: int, W: int, I: int, B: int, p: torch.Tensor,
-               arity: int, dmerge2=None):
-    """Run sg_dtkp_apply; operands are (member, present) pairs with full batch B."""
+               arity: int, dmerge2=None, inner=None):
+    """Run sg_dtkp_apply; operands are (member, present) pairs with full batch B.
+    ``inner`` = (inner_plan, [(member, present)] * 2, inner_recs, inner_off, rec_words)
+    runs the fused conj -> group_disj: operand 0 is the never-materialised output of the
+    binary conj described by it (``operands`` is then empty)."""
     dev = p.device
     n_out = dseg.host.n_seg
     out_m = torch.empty((n_out, K, W, B), device=dev, dtype=torch.int64)
@@ -512,6 +515,19 @@ def dtkp_apply(kplan_host, dseg, dmerge, operands, tail, K: int, W: int, I: int,
         d.op_tail.present = pr.data_ptr() if pr.numel() else None
         d.op_tail.rows = m.shape[0]
         d.op_tail.W = m.shape[2]
+    if inner is not None:
+        ikp, iops, irecs, ioff, irw = inner
+        d.inner_arity = 2
+        d.inner_rec_words = irw
+        for i, (m, pr) in enumerate(iops):
+            d.inner_ops[i].member = m.data_ptr() if m.numel() else None
+            d.inner_ops[i].present = pr.data_ptr() if pr.numel() else None
+            d.inner_ops[i].rows = m.shape[0]
+            d.inner_ops[i].W = m.shape[2]
+        d.inner_recs = irecs.data_ptr()
+        d.inner_off = ioff.data_ptr()
+        d.ops[0].rows = ikp.n_out
+        d.ops[0].W = W
     d.p = p.data_ptr() if p.numel() else None
     d.seg = dseg.struct(B)
     d.out_member = out_m.data_ptr() if out_m.numel() else None
@@ -538,6 +554,10 @@ def dtkp_apply(kplan_host, dseg, dmerge, operands, tail, K: int, W: int, I: int,
         partial = dseg.host.n_partial + (dmerge.host.n_partial if dseg.host.n_partial else 0)
         n_rec = kplan_host.n_rec
         cand = n_rec * (K ** arity if arity >= 2 else K)  # candidate rows ranked (upper bound)
+        if inner is not None:  # the inner conj's operands are read, its output never is
+            rows_in = sum(m.shape[0] for m, _ in inner[1])
+            n_rec += inner[0].n_rec * 2
+            cand += inner[0].n_rec * K * K
         _ledger("dtkp_apply", B * (rows_in + n_out + 2 * partial) * row + 4 * B * I + 4 * n_rec * max(arity, 1),
                 B * cand)
     return out_m, out_p

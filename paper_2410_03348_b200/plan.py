@@ -334,21 +334,30 @@ class HostSegsum:
 
     __slots__ = ("n_seg", "rec_words", "recs", "items", "split", "n_partial", "work", "seg_off")
 
-    def __init__(self, seg_off: np.ndarray, recs: np.ndarray, max_item: int):
+    def __init__(self, seg_off: np.ndarray, recs: np.ndarray, max_item: int, weights: np.ndarray | None = None):
+        """Items hold at most ``max_item`` records, or — with per-record ``weights`` (e.g.
+        the inner records behind each record of a fused conj -> group_disj) — close once
+        their weight reaches ``max_item`` (at least one record per item)."""
         n_seg = len(seg_off) - 1
         nrec, nops = recs.shape if recs.ndim == 2 else (recs.shape[0], 1)
         rw = _rec_words(max(nops, 1))
         packed = np.zeros((nrec, rw), dtype=np.int32)
         packed[:, :nops] = recs.reshape(nrec, nops)
         lens = np.diff(seg_off).astype(np.int64)
-        pieces = np.maximum(1, -(-lens // max_item))
-        n_items = int(pieces.sum())
-        seg_of = np.repeat(np.arange(n_seg, dtype=np.int64), pieces)
-        first = np.repeat(np.cumsum(pieces) - pieces, pieces)
-        piece = np.arange(n_items, dtype=np.int64) - first
-        rb = seg_off[seg_of].astype(np.int64) + piece * max_item
-        re = np.minimum(rb + max_item, seg_off[seg_of + 1])
-        re = np.maximum(re, rb)
+        if weights is None:
+            pieces = np.maximum(1, -(-lens // max_item))
+            n_items = int(pieces.sum())
+            seg_of = np.repeat(np.arange(n_seg, dtype=np.int64), pieces)
+            first = np.repeat(np.cumsum(pieces) - pieces, pieces)
+            piece = np.arange(n_items, dtype=np.int64) - first
+            rb = seg_off[seg_of].astype(np.int64) + piece * max_item
+            re = np.minimum(rb + max_item, seg_off[seg_of + 1])
+            re = np.maximum(re, rb)
+        else:
+            seg_of, rb, re = self._weighted_pieces(np.asarray(seg_off, dtype=np.int64),
+                                                   np.asarray(weights, dtype=np.int64), int(max_item))
+            pieces = np.bincount(seg_of, minlength=n_seg)
+            n_items = len(seg_of)
         is_split = pieces[seg_of] > 1
         dest = np.full(n_items, -1, dtype=np.int64)
         n_partial = int(is_split.sum())
@@ -367,8 +376,30 @@ class HostSegsum:
         self.items = items
         self.split = split
         self.n_partial = n_partial
-        self.work = (re - rb) + 2  # records + per-item overhead
+        if weights is None:
+            self.work = (re - rb) + 2  # records + per-item overhead
+        else:
+            cw = np.concatenate([[0], np.cumsum(np.asarray(weights, dtype=np.int64))])
+            self.work = (cw[re] - cw[rb]) + 2
         self.seg_off = seg_off
+
+    @staticmethod
+    def _weighted_pieces(seg_off, w, max_w):
+        seg_of, rb, re = [], [], []
+        for sgi in range(len(seg_off) - 1):
+            a, b = int(seg_off[sgi]), int(seg_off[sgi + 1])
+            start, acc = a, 0
+            for r in range(a, b):
+                if acc > 0 and acc + w[r] > max_w:
+                    seg_of.append(sgi)
+                    rb.append(start)
+                    re.append(r)
+                    start, acc = r, 0
+                acc += w[r]
+            seg_of.append(sgi)
+            rb.append(start)
+            re.append(b)
+        return (np.asarray(seg_of, dtype=np.int64), np.asarray(rb, dtype=np.int64), np.asarray(re, dtype=np.int64))
 
     def blocks(self, n_blocks: int) -> np.ndarray:
         """Item ranges of n_blocks contiguous CTA chunks balanced by work."""
@@ -435,6 +466,7 @@ def csr(keys: np.ndarray, n_seg: int):
 
 DAMP_MAX_ITEM = 128
 DTKP_MAX_ITEM = 48
+DTKP_FUSED_ITEM = 48  # inner conj records (+1 per intermediate symbol) per fused item
 DTKP_MERGE_ITEM = 8  # partial lists per first-level merge item (two-level merge)
 STAGE_BYTES = 200 * 1024
 
@@ -508,6 +540,24 @@ class KernelPlan:
             self._dtkp_host = HostSegsum(off, self.records[order], DTKP_MAX_ITEM)
         return self._dtkp_host
 
+    def dtkp_fused_host(self, inner: "KernelPlan") -> HostSegsum:
+        """Fused conj -> group_disj (this plan arity 1 over ``inner``'s outputs): segments =
+        this plan's outputs, records = inner output ids in ordinal order, items cut by the
+        inner conj records behind them (sg_dtkp_apply_desc.inner_*)."""
+        cache = self.__dict__.setdefault("_fused_hosts", {})
+        hit = cache.get(id(inner))
+        if hit is not None and hit[0] is inner:
+            return hit[1]
+        if self.arity != 1 or inner.arity != 2:
+            raise ValueError("fused DTKP apply needs an arity-1 plan over an arity-2 plan")
+        ioff = np.asarray(inner.dtkp_host().seg_off, dtype=np.int64)
+        order, off = csr(self.out_idx, self.n_out)
+        recs = self.records[order]
+        w = ioff[recs[:, 0] + 1] - ioff[recs[:, 0]] + 1
+        h = HostSegsum(off, recs, DTKP_FUSED_ITEM, weights=w)
+        cache[id(inner)] = (inner, h)
+        return h
+
     def maxprod_host(self) -> "dict[str, np.ndarray]":
         """CSR arrays of the max-product apply (sg_maxprod_plan): records grouped by output
         in first-derivation order, and per input the records using each row."""
@@ -562,27 +612,45 @@ class DevicePlan:
             self._bwd[k] = d
         return d
 
+    def _dtkp_levels(self, host: HostSegsum):
+        """(items, merge, merge2) device work lists of a DTKP segmented problem."""
+        # DTKP items are latency-bound per warp: ask for ~8 resident CTAs per SM
+        seg = DeviceSegsum(host, self.device, True, 16, target_ctas=148 * 8)
+        merge = merge2 = None
+        if len(host.split):
+            # merge of the split segments' partial lists, itself cut into pieces of
+            # DTKP_MERGE_ITEM partials whose lists a second level merges: the serial
+            # chain of a 3868-record segment drops from 48 + 81 to 48 + 8 + 11 records
+            off = np.concatenate([[0], host.split[:, 2]]).astype(np.int64)
+            merge_recs = np.arange(host.n_partial, dtype=np.int32).reshape(-1, 1)
+            mh = HostSegsum(off, merge_recs, DTKP_MERGE_ITEM)
+            # merge items that finish a segment write the original output segment
+            mh.items[:, 0] = host.split[mh.items[:, 0], 0]
+            merge = DeviceSegsum(mh, self.device, True, 16, target_ctas=148 * 8)
+            if len(mh.split):
+                off2 = np.concatenate([[0], mh.split[:, 2]]).astype(np.int64)
+                m2 = HostSegsum(off2, np.arange(mh.n_partial, dtype=np.int32).reshape(-1, 1), 1 << 30)
+                m2.items[:, 0] = host.split[mh.split[m2.items[:, 0], 0], 0]
+                merge2 = DeviceSegsum(m2, self.device, True, 16, target_ctas=148 * 8)
+        return seg, merge, merge2
+
     def dtkp(self):
         if self._dtkp is None:
-            host = self.kp.dtkp_host()
-            # DTKP items are latency-bound per warp: ask for ~8 resident CTAs per SM
-            self._dtkp = DeviceSegsum(host, self.device, True, 16, target_ctas=148 * 8)
-            if len(host.split):
-                # merge of the split segments' partial lists, itself cut into pieces of
-                # DTKP_MERGE_ITEM partials whose lists a second level merges: the serial
-                # chain of a 3868-record segment drops from 48 + 81 to 48 + 8 + 11 records
-                off = np.concatenate([[0], host.split[:, 2]]).astype(np.int64)
-                merge_recs = np.arange(host.n_partial, dtype=np.int32).reshape(-1, 1)
-                mh = HostSegsum(off, merge_recs, DTKP_MERGE_ITEM)
-                # merge items that finish a segment write the original output segment
-                mh.items[:, 0] = host.split[mh.items[:, 0], 0]
-                self._dtkp_merge = DeviceSegsum(mh, self.device, True, 16, target_ctas=148 * 8)
-                if len(mh.split):
-                    off2 = np.concatenate([[0], mh.split[:, 2]]).astype(np.int64)
-                    m2 = HostSegsum(off2, np.arange(mh.n_partial, dtype=np.int32).reshape(-1, 1), 1 << 30)
-                    m2.items[:, 0] = host.split[mh.split[m2.items[:, 0], 0], 0]
-                    self._dtkp_merge2 = DeviceSegsum(m2, self.device, True, 16, target_ctas=148 * 8)
+            self._dtkp, self._dtkp_merge, self._dtkp_merge2 = self._dtkp_levels(self.kp.dtkp_host())
         return self._dtkp, self._dtkp_merge, self._dtkp_merge2
+
+    def dtkp_fused(self, inner: "KernelPlan"):
+        """(items, merge, merge2, inner_recs, inner_off) of the fused conj -> group_disj."""
+        cache = self.__dict__.setdefault("_fused", {})
+        hit = cache.get(id(inner))
+        if hit is None or hit[0] is not inner:
+            ih = inner.dtkp_host()
+            levels = self._dtkp_levels(self.kp.dtkp_fused_host(inner))
+            irecs = torch.from_numpy(np.ascontiguousarray(ih.recs.reshape(-1))).to(self.device)
+            ioff = torch.from_numpy(np.asarray(ih.seg_off, dtype=np.int32)).to(self.device)
+            hit = (inner, (*levels, irecs, ioff, ih.rec_words))
+            cache[id(inner)] = hit
+        return hit[1]
 
     def maxprod_struct(self) -> N.SgMaxprodPlan:
         d = getattr(self, "_maxprod", None)

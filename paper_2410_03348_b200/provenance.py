@@ -473,35 +473,69 @@ class DtkpTags:
     ``present`` uint8 (b, n, k) host arrays — and packs it.
     """
 
-    __slots__ = ("pm", "pp", "registry")
+    __slots__ = ("_pm", "_pp", "registry", "_pending")
 
-    def __init__(self, member, present, registry):
-        if isinstance(member, torch.Tensor) and member.dtype == torch.int64 and member.ndim == 4:
-            self.pm = member
-            self.pp = present
+    def __init__(self, member, present, registry, pending: "_PendingConj | None" = None):
+        self._pending = pending
+        if pending is not None:
+            self._pm = self._pp = None
+        elif isinstance(member, torch.Tensor) and member.dtype == torch.int64 and member.ndim == 4:
+            self._pm = member
+            self._pp = present
         else:
             m = np.asarray(member.cpu() if isinstance(member, torch.Tensor) else member, dtype=np.uint8)
             pr = np.asarray(present.cpu() if isinstance(present, torch.Tensor) else present, dtype=np.uint8)
             dev = registry._dev()
-            self.pm = torch.as_tensor(pack_member(m), device=dev)
-            self.pp = torch.as_tensor(np.ascontiguousarray(pr.transpose(1, 2, 0)), device=dev)
+            self._pm = torch.as_tensor(pack_member(m), device=dev)
+            self._pp = torch.as_tensor(np.ascontiguousarray(pr.transpose(1, 2, 0)), device=dev)
         self.registry = registry
+
+    # A binary-conj apply may be left pending: its consumer, if it is a group_disj-shaped
+    # apply (an arity-1 apply_plan), fuses both into one launch and the intermediate tag
+    # never exists; every other access materialises it with the plain apply kernel.
+    def _materialise(self):
+        pm, pp = self._pending.run()
+        self._pm, self._pp, self._pending = pm, pp, None
+
+    @property
+    def pm(self) -> torch.Tensor:
+        if self._pending is not None:
+            self._materialise()
+        return self._pm
+
+    @pm.setter
+    def pm(self, v):
+        self._pm = v
+
+    @property
+    def pp(self) -> torch.Tensor:
+        if self._pending is not None:
+            self._materialise()
+        return self._pp
+
+    @pp.setter
+    def pp(self, v):
+        self._pp = v
+
+    @property
+    def pending(self) -> "_PendingConj | None":
+        return self._pending
 
     @property
     def batch(self) -> int:
-        return self.pm.shape[3]
+        return self._pending.B if self._pending is not None else self._pm.shape[3]
 
     @property
     def count(self) -> int:
-        return self.pm.shape[0]
+        return self._pending.kp.n_out if self._pending is not None else self._pm.shape[0]
 
     @property
     def k(self) -> int:
-        return self.pm.shape[1]
+        return self._pending.K if self._pending is not None else self._pm.shape[1]
 
     @property
     def W(self) -> int:
-        return self.pm.shape[2]
+        return self._pending.W if self._pending is not None else self._pm.shape[2]
 
     def aligned(self) -> "DtkpTags":
         """Pad the word axis to the registry width (provenance.py:185-192)."""
@@ -543,6 +577,25 @@ class DtkpTags:
                     proofs.add(frozenset(np.flatnonzero(member[m, col, r]).tolist()))
             out.append(proofs)
         return out
+
+
+class _PendingConj:
+    """A deferred binary-conj DTKP apply (plan, operands and registry state captured at
+    call time, so later registrations cannot change what it computes)."""
+
+    __slots__ = ("prov", "registry", "kp", "operands", "B", "K", "W", "I", "p")
+
+    def __init__(self, prov, registry, kp, operands, B, p):
+        self.prov, self.registry, self.kp, self.operands, self.B = prov, registry, kp, operands, B
+        self.K = prov.k
+        self.I = registry.size
+        self.W = _words(self.I)
+        self.p = p
+
+    def run(self):
+        dseg, dmerge, dmerge2 = self.kp.device(self.p.device).dtkp()
+        return ops.dtkp_apply(self.kp, dseg, dmerge, self.operands, None, self.K, self.W, self.I, self.B, self.p, 2,
+                              dmerge2)
 
 
 def _bcast_dtkp(t: DtkpTags, B: int):
@@ -750,11 +803,32 @@ class DtkpAm:
         return DtkpTags(om.cpu().numpy()[:, None], op.cpu().numpy()[:, None], registry)
 
     # ---- fused entry points ---------------------------------------------------------
+    fuse_conj_group = os.environ.get("SG_DTKP_FUSE", "1") != "0"
+
     def apply_plan(self, tags_list, plan: SymbolPlan, batch: int) -> DtkpTags:
-        """K3/K4: gather -> conj fold -> group_disj as one streaming top-k kernel."""
+        """K3/K4: gather -> conj fold -> group_disj as one streaming top-k kernel.
+
+        A binary apply is left pending; an arity-1 apply over a pending binary apply (HWF's
+        eval over its last concat step) runs both as ONE fused kernel (conj ->
+        group_disj), so the intermediate tag (208767 symbols at HWF-7) never reaches HBM."""
         registry = tags_list[0].registry
+        kp = plan.kernel_plan()
+        if self.fuse_conj_group and len(tags_list) == 1:
+            src = tags_list[0]
+            pend = src.pending
+            if pend is not None and pend.registry is registry and pend.B == batch and pend.K == self.k:
+                return self._run_fused(kp, pend, batch)
         ops_ = [_bcast_dtkp(t, batch) for t in tags_list]
-        return self._run(registry, plan.kernel_plan(), ops_, None, len(tags_list), batch)
+        if self.fuse_conj_group and len(tags_list) == 2:
+            p = self._p(registry, batch)
+            return DtkpTags(None, None, registry, pending=_PendingConj(self, registry, kp, ops_, batch, p))
+        return self._run(registry, kp, ops_, None, len(tags_list), batch)
+
+    def _run_fused(self, kp: KernelPlan, pend: "_PendingConj", B: int) -> DtkpTags:
+        dseg, dmerge, dmerge2, irecs, ioff, irw = kp.device(pend.p.device).dtkp_fused(pend.kp)
+        pm, pp = ops.dtkp_apply(kp, dseg, dmerge, [], None, self.k, pend.W, pend.I, B, pend.p, 1, dmerge2,
+                                inner=(pend.kp, pend.operands, irecs, ioff, irw))
+        return DtkpTags(pm, pp, pend.registry)
 
     def union_tags(self, a: DtkpTags, b: DtkpTags, uplan) -> DtkpTags:
         B = max(a.batch, b.batch)

@@ -303,7 +303,11 @@ def clutrr(dev, iters=20, cpu=True, B=4096, n_entities=5, k=5):
 
 # ------------------------------------------------------------------ configs[4]: sweep
 SWEEP = [(2, 10, 65536), (2, 10, 16384), (2, 100, 16384), (2, 1000, 16384), (3, 10, 16384), (3, 100, 16384)]
-SWEEP_CPU_BATCH = {(2, 10): 16384, (2, 100): 2048, (2, 1000): 64, (3, 10): 2048, (3, 100): 16}
+# reference sample batch (and worker processes) per sweep point; the reference's dense
+# group_disj matrix G (provenance.py:248-251) is C x N_out fp64 per apply: 2.4 GB at arity
+# 3 |S|=100 (few processes), 16 GB at arity 2 |S|=1000 (infeasible)
+SWEEP_CPU_BATCH = {(2, 10): (16384, 0), (2, 100): (2048, 0), (3, 10): (2048, 0), (3, 100): (16, 4)}
+SWEEP_CPU_INFEASIBLE = {(2, 1000): "reference dense G = 1e6 x 1999 fp64 = 16 GB per apply (provenance.py:248-251)"}
 
 
 def sweep_point(dev, arity, size, B, iters=20, cpu=True, provenance="damp"):
@@ -358,7 +362,9 @@ def sweep_point(dev, arity, size, B, iters=20, cpu=True, provenance="damp"):
     if cpu and provenance == "damp":
         cb = SWEEP_CPU_BATCH.get((arity, size))
         if cb:
-            res["cpu"] = cpu_reference("sweep", cb, steps=2, warmup=1, arity=arity, size=size)
+            res["cpu"] = cpu_reference("sweep", cb[0], steps=2, warmup=1, procs=cb[1], arity=arity, size=size)
+        elif (arity, size) in SWEEP_CPU_INFEASIBLE:
+            res["cpu"] = {"value": None, "infeasible": SWEEP_CPU_INFEASIBLE[(arity, size)]}
     del xs, w
     torch.cuda.empty_cache()
     return res
