@@ -229,20 +229,19 @@ typedef struct sg_dtkp_apply_desc {
   uint64_t* scratch2_member; /* [merge.n_partial][K][W][B] */
   uint8_t* scratch2_present; /* [merge.n_partial][K][B]    */
   /* Fused conj -> group_disj (arity == 1 only; inner_arity == 0 disables it).  The single
-   * operand of this apply is the output of an arity-2 apply that is never materialised —
-   * HWF's final eval over the 208767 formulas of its last concat step
-   * (programs.py:117-145): operand row r is computed on the fly as that apply's output
-   * segment r, i.e. its records inner_recs[inner_off[r] .. inner_off[r+1]) (inner_rec_words
-   * ints each: the rows of inner_ops[0] and inner_ops[1]) conjoined pairwise with
-   * per-record normalisation and streamed through a top-k (provenance.py:328-341 then
-   * :352-364), exactly the rows sg_dtkp_apply with arity 2 would write.  ops[0] and
-   * op_tail are not read.  Bit-identical to the two launches; the intermediate tag never
-   * touches HBM.                                                                         */
+   * operand of this apply is the output of a binary (arity-2) apply that is never
+   * materialised — HWF's final eval over the 208767 formulas of its last concat step
+   * (programs.py:117-145).  seg.recs then holds the BINARY apply's records (rec_words >= 2:
+   * row of inner_ops[0], row of inner_ops[1]) in this apply's segment order: for every
+   * record of this apply (an intermediate symbol) the conj records of that symbol in their
+   * ordinal order, the last one marked by bit 31 of its second word.  Each symbol's tag is
+   * built exactly as the binary apply builds its output row (per-record normalised conj,
+   * provenance.py:328-341, streamed through a top-k, :352-364) and its rows stream into this
+   * apply's top-k in rank order — bit-identical to the two launches, while the intermediate
+   * tag never touches HBM.  ops[0] and op_tail are not read.                            */
   int32_t inner_arity;
-  int32_t inner_rec_words;
+  int32_t inner_pad_;
   sg_dtkp_operand inner_ops[2];
-  const int32_t* inner_recs;  /* [n_inner_records][inner_rec_words] in output-segment order */
-  const int32_t* inner_off;   /* [ops[0].rows + 1] segment offsets into inner_recs           */
 } sg_dtkp_apply_desc;
 
 int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream);

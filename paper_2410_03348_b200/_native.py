@@ -102,10 +102,8 @@ class SgDtkpApplyDesc(Structure):
         ("scratch2_member", c_void_p),
         ("scratch2_present", c_void_p),
         ("inner_arity", c_int32),
-        ("inner_rec_words", c_int32),
+        ("inner_pad_", c_int32),
         ("inner_ops", SgDtkpOperand * 2),
-        ("inner_recs", c_void_p),
-        ("inner_off", c_void_p),
     ]
 
 

@@ -255,19 +255,13 @@ int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream) {
   k.scr_p = d->scratch_present;
   k.sched = d->sched;
   k.n_items = d->seg.n_items;
-  k.inner_recs = nullptr;
-  k.inner_off = nullptr;
-  k.inner_rec_words = 0;
+  k.fused = 0;
   if (d->inner_arity != 0) {
     // fused conj -> group_disj: only an arity-1 apply over a binary conj
-    SG_RETURN_IF(d->arity != 1 || d->inner_arity != 2 || d->inner_recs == nullptr || d->inner_off == nullptr ||
-                     d->inner_rec_words < 2,
-                 cudaErrorInvalidValue);
+    SG_RETURN_IF(d->arity != 1 || d->inner_arity != 2 || d->seg.rec_words < 2, cudaErrorInvalidValue);
     k.inner[0] = d->inner_ops[0];
     k.inner[1] = d->inner_ops[1];
-    k.inner_recs = d->inner_recs;
-    k.inner_off = d->inner_off;
-    k.inner_rec_words = d->inner_rec_words;
+    k.fused = 1;
   }
   if (d->seg.n_items > 0) {
     int rc = launch_apply(k, d->seg.n_blocks, st);
@@ -276,8 +270,7 @@ int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream) {
   if (d->seg.n_split > 0) {
     DtkpK m = k;
     m.arity = 1;
-    m.inner_recs = nullptr;  // merges read the materialised partial lists
-    m.inner_off = nullptr;
+    m.fused = 0;  // merges read the materialised partial lists
     m.ops[0].member = d->scratch_member;
     m.ops[0].present = d->scratch_present;
     m.ops[0].rows = d->seg.n_partial;

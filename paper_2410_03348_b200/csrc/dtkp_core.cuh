@@ -20,6 +20,9 @@
 #ifndef SG_DTKP_FUSED_MINB  // resident CTAs/SM asked of the fused conj -> group_disj (K <= 3)
 #define SG_DTKP_FUSED_MINB 4
 #endif
+#ifndef SG_DTKP_L1PF  // L1-prefetch the next record's tag rows (one line per lane)
+#define SG_DTKP_L1PF 1
+#endif
 #ifndef SG_DTKP_UNROLL_K
 #define SG_DTKP_UNROLL_K 4
 #endif
@@ -182,11 +185,9 @@ struct DtkpK {
   uint8_t* out_p;
   uint64_t* scr_m;
   uint8_t* scr_p;
-  // fused conj -> group_disj (AR == 3): operand row r = inner segment r, computed on the fly
+  // fused conj -> group_disj (AR == 3): the binary conj's operands (records in recs)
   sg_dtkp_operand inner[2];
-  const int32_t* inner_recs;
-  const int32_t* inner_off;
-  int32_t inner_rec_words;
+  int32_t fused;
 };
 
 template <int WT>
@@ -278,33 +279,67 @@ __device__ __forceinline__ void stream_rows(TopK<K, WT>& S, const TopK<K, WT>& T
   }
 }
 
+// L1 prefetch of one tag's rows for the warp's 32-sample column (row r of op): K*W member
+// words as 2 x 128-byte lines each and K present lines.  The apply's per-record chain is
+// record -> tag rows -> rank; prefetching the NEXT record's rows (one line per lane, no
+// registers held) while the current record is ranked turns its row loads into L1 hits.
+__device__ __forceinline__ void pf_tag_line(const sg_dtkp_operand& op, int K, int64_t B, int64_t col0, int r, int id,
+                                            bool two_lines) {
+  const int nm = K * op.W * 2;
+  const char* addr;
+  if (id < nm) {
+    if ((id & 1) && !two_lines) return;
+    addr = reinterpret_cast<const char*>(op.member + ((size_t)r * K * op.W + (id >> 1)) * B + col0) + (id & 1) * 128;
+  } else {
+    addr = reinterpret_cast<const char*>(op.present + ((size_t)r * K + (id - nm)) * B + col0);
+  }
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(addr));
+}
+
+__device__ __forceinline__ void pf_tags(const sg_dtkp_operand& o0, int r0, const sg_dtkp_operand* o1, int r1, int K,
+                                        int64_t B, int64_t col0, int lane) {
+  if (!SG_DTKP_L1PF) return;
+  const bool two = B - col0 > 16;  // samples col0 + 16 .. col0 + 31 exist
+  const int n0 = K * (2 * o0.W + 1);
+  const int n1 = o1 != nullptr ? K * (2 * o1->W + 1) : 0;
+  for (int id = lane; id < n0 + n1; id += 32) {
+    if (id < n0)
+      pf_tag_line(o0, K, B, col0, r0, id, two);
+    else
+      pf_tag_line(*o1, K, B, col0, r1, id - n0, two);
+  }
+}
+
 // One work item (an output segment, or a piece of a split one) for one sample: stream its
 // records through the top-k set and write the retained rows.
 // AR: 1 = union / group_disj streaming, 2 = binary conj fold, 0 = conj fold of >= 3
-// operands, 3 = group_disj whose operand rows are binary-conj outputs computed on the fly
-// (the fused conj -> group_disj of sg_dtkp_apply_desc.inner_*).  Each is its own kernel, so the streaming kernel does not carry the
-// conj fold's registers (occupancy) or code (instruction cache).
+// operands, 3 = the fused conj -> group_disj (sg_dtkp_apply_desc.inner_arity): records are
+// binary-conj records (rows of inner[0], inner[1]) grouped by intermediate symbol, the last
+// record of each intermediate flagged by bit 31 of its second word.  Each is its own kernel,
+// so the streaming kernel does not carry the conj fold's registers (occupancy) or code.
 template <int K, int WT, int AR>
 __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, int64_t b0, bool bval, const PCol& pc) {
   constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
   const int4 item = __ldg(reinterpret_cast<const int4*>(a.items) + it);
+  const int lane = threadIdx.x & 31;
+  const int64_t col0 = (int64_t)blockIdx.x * kWarp;
   TopK<K, WT> S;
   S.clear();
   if constexpr (AR == 1) {
-    // group_disj / union / merge: stream the stored rows of every record, in order;
-    // the next record's rows are loaded before the current one is ranked.
-    TagRows<K, WT> cur, nxt;
-    auto fetch = [&](int c, TagRows<K, WT>& t) {
-      int r = rec_row(a, c, 0);
-      if (r >= a.ops[0].rows)
-        t.load(a.tail, a.B, b, r - a.ops[0].rows);
-      else
-        t.load(a.ops[0], a.B, b, r);
-    };
-    if (item.y < item.z) fetch(item.y, cur);
+    // group_disj / union / merge: stream the stored rows of every record, in order
+    auto op_of = [&](int r) -> const sg_dtkp_operand& { return r >= a.ops[0].rows ? a.tail : a.ops[0]; };
+    auto row_of = [&](int r) { return r >= a.ops[0].rows ? r - a.ops[0].rows : r; };
+    TagRows<K, WT> cur;
+    int rn = item.y + 1 < item.z ? rec_row(a, item.y + 1, 0) : 0;
+    if (item.y < item.z) {
+      const int r = rec_row(a, item.y, 0);
+      cur.load(op_of(r), a.B, b, row_of(r));
+    }
     for (int c = item.y; c < item.z; ++c) {
       const bool more = c + 1 < item.z;
-      if (SG_DTKP_STREAM_PREFETCH && more) fetch(c + 1, nxt);
+      const int rnext = rn;
+      if (more) pf_tags(op_of(rnext), row_of(rnext), nullptr, 0, K, a.B, col0, lane);
+      if (c + 2 < item.z) rn = rec_row(a, c + 2, 0);
 #pragma unroll (kUnrollK)
       for (int q = 0; q < K; ++q) {
         if (!((cur.pres >> q) & 1u)) continue;
@@ -312,48 +347,78 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
         cur.row(q, mm);
         S.insert(mm, proof_key<WT>(mm, pc), 0);
       }
-      if (more) {
-        if (SG_DTKP_STREAM_PREFETCH)
-          cur = nxt;
-        else
-          fetch(c + 1, cur);
-      }
+      if (more) cur.load(op_of(rnext), a.B, b, row_of(rnext));
     }
   } else if constexpr (AR == 3) {
-    // fused conj -> group_disj: each record is an intermediate symbol s whose tag is the
-    // top-k over its own conj records (what an arity-2 apply writes as row s); its rows
-    // stream into this item's top-k in rank order, as the group_disj of the materialised
-    // tag would read them
+    // fused conj -> group_disj: M collects an intermediate symbol's tag (the top-k over its
+    // conj records, what an arity-2 apply writes as its row); at the symbol's last record
+    // M's rows stream into S in rank order, as the group_disj of the materialised tag reads
+    const sg_dtkp_operand& o0 = a.inner[0];
+    const sg_dtkp_operand& o1 = a.inner[1];
+    TagRows<K, WT> A, Bt;
+    int ra = 0, rbf = 0, ran = 0, rbn = 0;
+    if (item.y < item.z) {
+      ra = rec_row(a, item.y, 0);
+      rbf = rec_row(a, item.y, 1);
+      A.load(o0, a.B, b, ra);
+      Bt.load(o1, a.B, b, rbf & 0x7fffffff);
+    }
+    if (item.y + 1 < item.z) {
+      ran = rec_row(a, item.y + 1, 0);
+      rbn = rec_row(a, item.y + 1, 1);
+    }
+    TopK<K, WT> M;
+    M.clear();
     for (int c = item.y; c < item.z; ++c) {
-      const int s = rec_row(a, c, 0);
-      const int r0 = __ldg(a.inner_off + s), r1 = __ldg(a.inner_off + s + 1);
-      TopK<K, WT> M;
-      M.clear();
-      for (int cc = r0; cc < r1; ++cc) {
-        const int* rr = a.inner_recs + (size_t)cc * a.inner_rec_words;
-        TagRows<K, WT> A, Bt;
-        A.load(a.inner[0], a.B, b, __ldg(rr));
-        Bt.load(a.inner[1], a.B, b, __ldg(rr + 1));
-        TopK<K, WT> T;
-        conj_pairs<K, WT>(T, A, Bt, pc);
-        stream_rows<K, WT>(M, T);
+      const bool more = c + 1 < item.z;
+      const int rna = ran, rnb = rbn;
+      if (more) pf_tags(o0, rna, &o1, rnb & 0x7fffffff, K, a.B, col0, lane);
+      if (c + 2 < item.z) {
+        ran = rec_row(a, c + 2, 0);
+        rbn = rec_row(a, c + 2, 1);
       }
-      stream_rows<K, WT>(S, M);
+      TopK<K, WT> T;
+      conj_pairs<K, WT>(T, A, Bt, pc);
+      stream_rows<K, WT>(M, T);
+      if (rbf < 0) {  // last conj record of this intermediate symbol
+        stream_rows<K, WT>(S, M);
+        M.clear();
+      }
+      if (more) {
+        rbf = rnb;
+        A.load(o0, a.B, b, rna);
+        Bt.load(o1, a.B, b, rnb & 0x7fffffff);
+      }
     }
   } else {
     // conj fold, normalised after every step (candidate order ra*kb + rb)
     TagRows<K, WT> A, Bt, An, Bn;
+    int ran = 0, rbn = 0;
     if (item.y < item.z) {
       A.load(a.ops[0], a.B, b, rec_row(a, item.y, 0));
       Bt.load(a.ops[1], a.B, b, rec_row(a, item.y, 1));
     }
-    // next record's rows prefetched unless K is large (their registers cost occupancy)
+    if (item.y + 1 < item.z) {
+      ran = rec_row(a, item.y + 1, 0);
+      rbn = rec_row(a, item.y + 1, 1);
+    }
+    // next record's rows held in registers only while K is small (their registers cost
+    // occupancy); otherwise L1-prefetched and loaded after the current record
     constexpr bool kPf = K <= SG_DTKP_CONJ_PREFETCH_MAXK;
     for (int c = item.y; c < item.z; ++c) {
       const bool more = c + 1 < item.z;
-      if (kPf && more) {
-        An.load(a.ops[0], a.B, b, rec_row(a, c + 1, 0));
-        Bn.load(a.ops[1], a.B, b, rec_row(a, c + 1, 1));
+      const int rna = ran, rnb = rbn;
+      if (more) {
+        if (kPf) {
+          An.load(a.ops[0], a.B, b, rna);
+          Bn.load(a.ops[1], a.B, b, rnb);
+        } else if (AR == 2) {
+          pf_tags(a.ops[0], rna, &a.ops[1], rnb, K, a.B, col0, lane);
+        }
+      }
+      if (c + 2 < item.z) {
+        ran = rec_row(a, c + 2, 0);
+        rbn = rec_row(a, c + 2, 1);
       }
       TopK<K, WT> T;
       conj_pairs<K, WT>(T, A, Bt, pc);
@@ -387,8 +452,8 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
           A = An;
           Bt = Bn;
         } else {
-          A.load(a.ops[0], a.B, b, rec_row(a, c + 1, 0));
-          Bt.load(a.ops[1], a.B, b, rec_row(a, c + 1, 1));
+          A.load(a.ops[0], a.B, b, rna);
+          Bt.load(a.ops[1], a.B, b, rnb);
         }
       }
     }
@@ -502,7 +567,7 @@ static int launch_apply_kwa(const DtkpK& k, int n_blocks, cudaStream_t st) {
 
 template <int K, int WT>
 static int launch_apply_kw(const DtkpK& k, int n_blocks, cudaStream_t st) {
-  if (k.arity == 1 && k.inner_recs != nullptr) return launch_apply_kwa<K, WT, 3>(k, n_blocks, st);
+  if (k.arity == 1 && k.fused) return launch_apply_kwa<K, WT, 3>(k, n_blocks, st);
   if (k.arity == 1) return launch_apply_kwa<K, WT, 1>(k, n_blocks, st);
   if (k.arity == 2) return launch_apply_kwa<K, WT, 2>(k, n_blocks, st);
   return launch_apply_kwa<K, WT, 0>(k, n_blocks, st);

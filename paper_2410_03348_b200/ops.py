@@ -491,9 +491,9 @@ def dtkp_sched(device, n: int) -> torch.Tensor:
 def dtkp_apply(kplan_host, dseg, dmerge, operands, tail, K: int, W: int, I: int, B: int, p: torch.Tensor,
                arity: int, dmerge2=None, inner=None):
     """Run sg_dtkp_apply; operands are (member, present) pairs with full batch B.
-    ``inner`` = (inner_plan, [(member, present)] * 2, inner_recs, inner_off, rec_words)
-    runs the fused conj -> group_disj: operand 0 is the never-materialised output of the
-    binary conj described by it (``operands`` is then empty)."""
+    ``inner`` = (inner_plan, [(member, present)] * 2) runs the fused conj -> group_disj
+    (``dseg`` from DevicePlan.dtkp_fused): operand 0 is the never-materialised output of
+    the binary apply ``inner_plan`` over those operands (``operands`` is then empty)."""
     dev = p.device
     n_out = dseg.host.n_seg
     out_m = torch.empty((n_out, K, W, B), device=dev, dtype=torch.int64)
@@ -516,16 +516,13 @@ def dtkp_apply(kplan_host, dseg, dmerge, operands, tail, K: int, W: int, I: int,
         d.op_tail.rows = m.shape[0]
         d.op_tail.W = m.shape[2]
     if inner is not None:
-        ikp, iops, irecs, ioff, irw = inner
+        ikp, iops = inner
         d.inner_arity = 2
-        d.inner_rec_words = irw
         for i, (m, pr) in enumerate(iops):
             d.inner_ops[i].member = m.data_ptr() if m.numel() else None
             d.inner_ops[i].present = pr.data_ptr() if pr.numel() else None
             d.inner_ops[i].rows = m.shape[0]
             d.inner_ops[i].W = m.shape[2]
-        d.inner_recs = irecs.data_ptr()
-        d.inner_off = ioff.data_ptr()
         d.ops[0].rows = ikp.n_out
         d.ops[0].W = W
     d.p = p.data_ptr() if p.numel() else None

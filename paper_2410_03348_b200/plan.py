@@ -334,28 +334,34 @@ class HostSegsum:
 
     __slots__ = ("n_seg", "rec_words", "recs", "items", "split", "n_partial", "work", "seg_off")
 
-    def __init__(self, seg_off: np.ndarray, recs: np.ndarray, max_item: int, weights: np.ndarray | None = None):
-        """Items hold at most ``max_item`` records, or — with per-record ``weights`` (e.g.
-        the inner records behind each record of a fused conj -> group_disj) — close once
-        their weight reaches ``max_item`` (at least one record per item)."""
+    def __init__(self, seg_off: np.ndarray, recs: np.ndarray, max_item: int, cut_points: np.ndarray | None = None,
+                 cut_seg: np.ndarray | None = None):
+        """Items hold at most ``max_item`` records.  With ``cut_points`` (record offsets of
+        groups that must stay whole — one intermediate symbol's conj records in a fused
+        conj -> group_disj — and ``cut_seg``, the segment of each group) items are made of
+        whole groups and close before they would exceed ``max_item`` records (at least one
+        group each)."""
+        seg_off = np.asarray(seg_off, dtype=np.int64)
         n_seg = len(seg_off) - 1
         nrec, nops = recs.shape if recs.ndim == 2 else (recs.shape[0], 1)
         rw = _rec_words(max(nops, 1))
         packed = np.zeros((nrec, rw), dtype=np.int32)
         packed[:, :nops] = recs.reshape(nrec, nops)
-        lens = np.diff(seg_off).astype(np.int64)
-        if weights is None:
+        lens = np.diff(seg_off)
+        if cut_points is None:
             pieces = np.maximum(1, -(-lens // max_item))
             n_items = int(pieces.sum())
             seg_of = np.repeat(np.arange(n_seg, dtype=np.int64), pieces)
             first = np.repeat(np.cumsum(pieces) - pieces, pieces)
             piece = np.arange(n_items, dtype=np.int64) - first
-            rb = seg_off[seg_of].astype(np.int64) + piece * max_item
+            rb = seg_off[seg_of] + piece * max_item
             re = np.minimum(rb + max_item, seg_off[seg_of + 1])
             re = np.maximum(re, rb)
         else:
-            seg_of, rb, re = self._weighted_pieces(np.asarray(seg_off, dtype=np.int64),
-                                                   np.asarray(weights, dtype=np.int64), int(max_item))
+            cp = np.asarray(cut_points, dtype=np.int64)
+            gseg_off = np.searchsorted(np.asarray(cut_seg, dtype=np.int64), np.arange(n_seg + 1), side="left")
+            seg_of, gb, ge = self._group_pieces(gseg_off, np.diff(cp), int(max_item))
+            rb, re = cp[gb], cp[ge]
             pieces = np.bincount(seg_of, minlength=n_seg)
             n_items = len(seg_of)
         is_split = pieces[seg_of] > 1
@@ -376,30 +382,28 @@ class HostSegsum:
         self.items = items
         self.split = split
         self.n_partial = n_partial
-        if weights is None:
-            self.work = (re - rb) + 2  # records + per-item overhead
-        else:
-            cw = np.concatenate([[0], np.cumsum(np.asarray(weights, dtype=np.int64))])
-            self.work = (cw[re] - cw[rb]) + 2
+        self.work = (re - rb) + 2  # records + per-item overhead
         self.seg_off = seg_off
 
     @staticmethod
-    def _weighted_pieces(seg_off, w, max_w):
-        seg_of, rb, re = [], [], []
-        for sgi in range(len(seg_off) - 1):
-            a, b = int(seg_off[sgi]), int(seg_off[sgi + 1])
+    def _group_pieces(gseg_off, gsize, max_w):
+        """Per segment, runs of whole groups of at most max_w records (>= 1 group each);
+        an empty segment still gets one (empty) item -> (segment, first group, end group)."""
+        seg_of, gb, ge = [], [], []
+        for sgi in range(len(gseg_off) - 1):
+            a, b = int(gseg_off[sgi]), int(gseg_off[sgi + 1])
             start, acc = a, 0
-            for r in range(a, b):
-                if acc > 0 and acc + w[r] > max_w:
+            for g in range(a, b):
+                if acc > 0 and acc + gsize[g] > max_w:
                     seg_of.append(sgi)
-                    rb.append(start)
-                    re.append(r)
-                    start, acc = r, 0
-                acc += w[r]
+                    gb.append(start)
+                    ge.append(g)
+                    start, acc = g, 0
+                acc += int(gsize[g])
             seg_of.append(sgi)
-            rb.append(start)
-            re.append(b)
-        return (np.asarray(seg_of, dtype=np.int64), np.asarray(rb, dtype=np.int64), np.asarray(re, dtype=np.int64))
+            gb.append(start)
+            ge.append(b)
+        return (np.asarray(seg_of, dtype=np.int64), np.asarray(gb, dtype=np.int64), np.asarray(ge, dtype=np.int64))
 
     def blocks(self, n_blocks: int) -> np.ndarray:
         """Item ranges of n_blocks contiguous CTA chunks balanced by work."""
@@ -541,20 +545,35 @@ class KernelPlan:
         return self._dtkp_host
 
     def dtkp_fused_host(self, inner: "KernelPlan") -> HostSegsum:
-        """Fused conj -> group_disj (this plan arity 1 over ``inner``'s outputs): segments =
-        this plan's outputs, records = inner output ids in ordinal order, items cut by the
-        inner conj records behind them (sg_dtkp_apply_desc.inner_*)."""
+        """Fused conj -> group_disj (this plan arity 1 over ``inner``'s outputs, inner arity
+        2): segments = this plan's outputs; records = for each of its records (an inner
+        output s, ordinal order) the inner conj records of s in their ordinal order, the
+        last one flagged by bit 31 of its second word (sg_dtkp_apply_desc.inner_arity).
+        Items hold whole intermediate symbols, ~DTKP_FUSED_ITEM conj records each."""
         cache = self.__dict__.setdefault("_fused_hosts", {})
         hit = cache.get(id(inner))
         if hit is not None and hit[0] is inner:
             return hit[1]
         if self.arity != 1 or inner.arity != 2:
             raise ValueError("fused DTKP apply needs an arity-1 plan over an arity-2 plan")
-        ioff = np.asarray(inner.dtkp_host().seg_off, dtype=np.int64)
+        ih = inner.dtkp_host()
+        ioff = np.asarray(ih.seg_off, dtype=np.int64)
+        irecs = ih.recs[:, :2].astype(np.int64)
         order, off = csr(self.out_idx, self.n_out)
-        recs = self.records[order]
-        w = ioff[recs[:, 0] + 1] - ioff[recs[:, 0]] + 1
-        h = HostSegsum(off, recs, DTKP_FUSED_ITEM, weights=w)
+        mids = self.records[order, 0].astype(np.int64)
+        lens = ioff[mids + 1] - ioff[mids]
+        # flat conj records of every intermediate, in this plan's segment order
+        starts = np.repeat(ioff[mids], lens)
+        within = np.arange(int(lens.sum()), dtype=np.int64) - np.repeat(np.cumsum(lens) - lens, lens)
+        flat = irecs[starts + within].copy()
+        last = np.cumsum(lens) - 1
+        flat[last, 1] |= np.int64(1) << 31
+        flat = flat.astype(np.uint32).view(np.int32).reshape(-1, 2)
+        # segment offsets and item cuts in flat-record units, at intermediate boundaries
+        mid_off = np.concatenate([[0], np.cumsum(lens)])
+        seg_off = mid_off[off]
+        seg_of_mid = np.repeat(np.arange(self.n_out), np.diff(off))
+        h = HostSegsum(seg_off, flat, DTKP_FUSED_ITEM, cut_points=mid_off, cut_seg=seg_of_mid)
         cache[id(inner)] = (inner, h)
         return h
 
@@ -640,15 +659,11 @@ class DevicePlan:
         return self._dtkp, self._dtkp_merge, self._dtkp_merge2
 
     def dtkp_fused(self, inner: "KernelPlan"):
-        """(items, merge, merge2, inner_recs, inner_off) of the fused conj -> group_disj."""
+        """(items, merge, merge2) of the fused conj -> group_disj over ``inner``."""
         cache = self.__dict__.setdefault("_fused", {})
         hit = cache.get(id(inner))
         if hit is None or hit[0] is not inner:
-            ih = inner.dtkp_host()
-            levels = self._dtkp_levels(self.kp.dtkp_fused_host(inner))
-            irecs = torch.from_numpy(np.ascontiguousarray(ih.recs.reshape(-1))).to(self.device)
-            ioff = torch.from_numpy(np.asarray(ih.seg_off, dtype=np.int32)).to(self.device)
-            hit = (inner, (*levels, irecs, ioff, ih.rec_words))
+            hit = (inner, self._dtkp_levels(self.kp.dtkp_fused_host(inner)))
             cache[id(inner)] = hit
         return hit[1]
 

@@ -825,9 +825,9 @@ class DtkpAm:
         return self._run(registry, kp, ops_, None, len(tags_list), batch)
 
     def _run_fused(self, kp: KernelPlan, pend: "_PendingConj", B: int) -> DtkpTags:
-        dseg, dmerge, dmerge2, irecs, ioff, irw = kp.device(pend.p.device).dtkp_fused(pend.kp)
+        dseg, dmerge, dmerge2 = kp.device(pend.p.device).dtkp_fused(pend.kp)
         pm, pp = ops.dtkp_apply(kp, dseg, dmerge, [], None, self.k, pend.W, pend.I, B, pend.p, 1, dmerge2,
-                                inner=(pend.kp, pend.operands, irecs, ioff, irw))
+                                inner=(pend.kp, pend.operands))
         return DtkpTags(pm, pp, pend.registry)
 
     def union_tags(self, a: DtkpTags, b: DtkpTags, uplan) -> DtkpTags:

@@ -190,3 +190,41 @@ def test_native_planner_errors():
     assert ei.value.symbols == (1,)
     with pytest.raises(TypeError):  # an unhashable result fails in the bucket dict, unwrapped
         P._map_shuffle(lambda x: [x], None, [tuple(range(2))])
+
+
+def test_fused_dtkp_host_plan_keeps_intermediates_whole():
+    """The fused conj -> group_disj work list (sg_dtkp_apply_desc.inner_arity): per output
+    segment, the conj records of its intermediate symbols in (segment ordinal, conj
+    ordinal) order, bit 31 on each intermediate's last record, items of whole
+    intermediates, split segments listed for the merge pass."""
+    import numpy as np
+
+    from paper_2410_03348_b200 import programs as P
+    from paper_2410_03348_b200.plan import build_plan
+
+    d = tuple(P.DIGIT_TOKENS)
+    o = tuple(P.OPERATOR_TOKENS)
+    s1 = build_plan(P._singleton, None, [d])
+    s2 = build_plan(P._concat_symbol, None, [s1.out_symbols, o])
+    s3 = build_plan(P._concat_symbol, None, [s2.out_symbols, d])  # the binary apply (inner)
+    ev = build_plan(P._eval_chain, None, [s3.out_symbols])          # the arity-1 apply (outer)
+    inner, outer = s3.kernel_plan(), ev.kernel_plan()
+    h = outer.dtkp_fused_host(inner)
+    ih = inner.dtkp_host()
+    flat = h.recs[:, :2].view(np.uint32).astype(np.int64)
+    last = (flat[:, 1] >> 31) == 1
+    rows = np.stack([flat[:, 0], flat[:, 1] & 0x7FFFFFFF], axis=1)
+    # expected sequence, straight from the two plans
+    exp, exp_last = [], []
+    for seg in range(outer.n_out):
+        for mid in outer.records[outer.out_idx == seg, 0]:
+            a, b = ih.seg_off[mid], ih.seg_off[mid + 1]
+            exp.extend(ih.recs[a:b, :2].tolist())
+            exp_last.extend([False] * (b - a - 1) + [True])
+    np.testing.assert_array_equal(rows, np.asarray(exp))
+    np.testing.assert_array_equal(last, np.asarray(exp_last))
+    for seg, rb, re, dest in h.items:
+        assert rb == re or last[re - 1]               # items end on an intermediate boundary
+        assert rb == h.seg_off[seg] or last[rb - 1]  # ... and start on one
+    split = np.bincount(h.items[:, 0], minlength=h.n_seg) > 1
+    assert h.n_partial == int(split[h.items[:, 0]].sum()) == int((h.items[:, 3] >= 0).sum())
