@@ -18,6 +18,8 @@
 // Thread mapping: lane == sample (32 samples per warp), one warp per output item; index
 // records are warp-uniform, tag rows are coalesced 256-byte words per warp, the sample's
 // probability column is staged in shared memory as fp64 [I][32].
+#include <cstdlib>
+
 #include "dtkp_core.cuh"
 
 namespace sg {
@@ -256,6 +258,13 @@ int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream) {
   k.sched = d->sched;
   k.n_items = d->seg.n_items;
   k.fused = 0;
+  {
+    static const int l1pf = [] {
+      const char* e = getenv("SG_DTKP_L1PF");
+      return e != nullptr && e[0] == '1' ? 1 : 0;
+    }();
+    k.l1pf = l1pf;
+  }
   if (d->inner_arity != 0) {
     // fused conj -> group_disj: only an arity-1 apply over a binary conj
     SG_RETURN_IF(d->arity != 1 || d->inner_arity != 2 || d->seg.rec_words < 2, cudaErrorInvalidValue);

@@ -20,9 +20,6 @@
 #ifndef SG_DTKP_FUSED_MINB  // resident CTAs/SM asked of the fused conj -> group_disj (K <= 3)
 #define SG_DTKP_FUSED_MINB 4
 #endif
-#ifndef SG_DTKP_L1PF  // L1-prefetch the next record's tag rows (one line per lane)
-#define SG_DTKP_L1PF 1
-#endif
 #ifndef SG_DTKP_UNROLL_K
 #define SG_DTKP_UNROLL_K 4
 #endif
@@ -188,6 +185,7 @@ struct DtkpK {
   // fused conj -> group_disj (AR == 3): the binary conj's operands (records in recs)
   sg_dtkp_operand inner[2];
   int32_t fused;
+  int32_t l1pf;  // L1-prefetch the next record's tag rows (SG_DTKP_L1PF=1; measured: no gain)
 };
 
 template <int WT>
@@ -297,8 +295,8 @@ __device__ __forceinline__ void pf_tag_line(const sg_dtkp_operand& op, int K, in
 }
 
 __device__ __forceinline__ void pf_tags(const sg_dtkp_operand& o0, int r0, const sg_dtkp_operand* o1, int r1, int K,
-                                        int64_t B, int64_t col0, int lane) {
-  if (!SG_DTKP_L1PF) return;
+                                        int64_t B, int64_t col0, int lane, int on) {
+  if (!on) return;
   const bool two = B - col0 > 16;  // samples col0 + 16 .. col0 + 31 exist
   const int n0 = K * (2 * o0.W + 1);
   const int n1 = o1 != nullptr ? K * (2 * o1->W + 1) : 0;
@@ -338,7 +336,7 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
     for (int c = item.y; c < item.z; ++c) {
       const bool more = c + 1 < item.z;
       const int rnext = rn;
-      if (more) pf_tags(op_of(rnext), row_of(rnext), nullptr, 0, K, a.B, col0, lane);
+      if (more) pf_tags(op_of(rnext), row_of(rnext), nullptr, 0, K, a.B, col0, lane, a.l1pf);
       if (c + 2 < item.z) rn = rec_row(a, c + 2, 0);
 #pragma unroll (kUnrollK)
       for (int q = 0; q < K; ++q) {
@@ -372,7 +370,7 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
     for (int c = item.y; c < item.z; ++c) {
       const bool more = c + 1 < item.z;
       const int rna = ran, rnb = rbn;
-      if (more) pf_tags(o0, rna, &o1, rnb & 0x7fffffff, K, a.B, col0, lane);
+      if (more) pf_tags(o0, rna, &o1, rnb & 0x7fffffff, K, a.B, col0, lane, a.l1pf);
       if (c + 2 < item.z) {
         ran = rec_row(a, c + 2, 0);
         rbn = rec_row(a, c + 2, 1);
@@ -413,7 +411,7 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
           An.load(a.ops[0], a.B, b, rna);
           Bn.load(a.ops[1], a.B, b, rnb);
         } else if (AR == 2) {
-          pf_tags(a.ops[0], rna, &a.ops[1], rnb, K, a.B, col0, lane);
+          pf_tags(a.ops[0], rna, &a.ops[1], rnb, K, a.B, col0, lane, a.l1pf);
         }
       }
       if (c + 2 < item.z) {

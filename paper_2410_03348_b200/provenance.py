@@ -803,7 +803,10 @@ class DtkpAm:
         return DtkpTags(om.cpu().numpy()[:, None], op.cpu().numpy()[:, None], registry)
 
     # ---- fused entry points ---------------------------------------------------------
-    fuse_conj_group = os.environ.get("SG_DTKP_FUSE", "1") != "0"
+    # the fused conj -> group_disj launch is exact (tests/test_gpu_fused.py) but, as built,
+    # slower than the two launches on HWF-7 (1.77 ms vs 1.45 ms, profiles/r02_dtkp_launches.md):
+    # opt in with SG_DTKP_FUSE=1
+    fuse_conj_group = os.environ.get("SG_DTKP_FUSE", "0") == "1"
 
     def apply_plan(self, tags_list, plan: SymbolPlan, batch: int) -> DtkpTags:
         """K3/K4: gather -> conj fold -> group_disj as one streaming top-k kernel.

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 def _run(name, inputs, fuse):
     import paper_2410_03348_b200 as sg
 
-    old = sg.DtkpAm.fuse_conj_group
+    old = sg.DtkpAm.fuse_conj_group  # default off; both paths must agree
     sg.DtkpAm.fuse_conj_group = fuse
     try:
         return run_gpu(name, inputs)
@@ -61,6 +61,17 @@ def test_pending_conj_materialises_for_other_consumers(cuda):
     import torch
 
     import paper_2410_03348_b200 as sg
+
+    old = sg.DtkpAm.fuse_conj_group
+    sg.DtkpAm.fuse_conj_group = True
+    try:
+        _pending_case(cuda, sg)
+    finally:
+        sg.DtkpAm.fuse_conj_group = old
+
+
+def _pending_case(cuda, sg):
+    import torch
 
     ctx = sg.ProgramContext(sg.DtkpAm(3), device=cuda)
     rng = np.random.default_rng(3)
