@@ -22,6 +22,7 @@
  *   sg_damp_rows_add    provenance.py:239-240 Damp.disj; distribution.py:279-297 union
  *   sg_chain_fwd/bwd    a left fold of Toeplitz applies (programs.py:42-49 sum_n) as one
  *                       launch each way; per step the same as sg_damp_apply_fwd/bwd
+ *   sg_maxchain_fwd/bwd the same fold under the max/DAMP variant (per step sg_maxprod_*)
  *   sg_nll_fwd/bwd      learn.py:92-119 loss_nll (the caller right after get_probs)
  *   sg_rows_gather      provenance.py:233-234 / :320-326 gather (filter, distribution.py:158-169)
  *   sg_to_symbol_major  provenance.py:223-225 Damp.input_tags (layout + fp32 cast of the block)
@@ -170,6 +171,19 @@ int32_t sg_chain_max_rows(int32_t kf);
 int sg_chain_fwd(const sg_chain* chain, float* out, double* rowsum, sg_stream_t stream);
 int sg_chain_bwd(const sg_chain* chain, const float* grad_out, sg_rows grad_base,
                  const sg_rows* grad_filters, sg_stream_t stream);
+
+/* ---- fused max-product Toeplitz chain (the north star's max/DAMP variant) ------------
+ * The same left fold as sg_chain_* under DampMax (long operand first, kf-row filters):
+ * v_i = clamp01(max_s v_{i-1}[s] * S_i[o - s]), first maximal record (s ascending) kept;
+ * per step bit-identical to sg_maxprod_fwd/bwd.  states: sg_maxchain_states_elems floats
+ * ([rows][B]), argmax: sg_maxchain_argmax_bytes bytes (the argmax tap per step, output,
+ * sample); both written by fwd and read by bwd.  rowsum as for sg_chain_fwd. */
+int64_t sg_maxchain_states_elems(int32_t n0, int32_t kf, int32_t m, int64_t B);
+int64_t sg_maxchain_argmax_bytes(int32_t n0, int32_t kf, int32_t m, int64_t B);
+int32_t sg_maxchain_max_rows(int32_t kf);
+int sg_maxchain_fwd(const sg_chain* chain, float* out, double* rowsum, uint8_t* argmax, sg_stream_t stream);
+int sg_maxchain_bwd(const sg_chain* chain, const uint8_t* argmax, const float* grad_out, sg_rows grad_base,
+                    const sg_rows* grad_filters, sg_stream_t stream);
 
 /* ---- fused get_probs -> loss_nll (learn.py:92-119, pass-through clamps) ---------------
  * loss = -(1/B) sum_b log(max(max(p[t_b][b] / (sum_n p[n][b] + 1e-8), 1e-12), 1e-12)),

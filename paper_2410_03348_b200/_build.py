@@ -40,6 +40,7 @@ def _units():
         ("chain.o", CSRC / "chain.cu", []),
         ("dtkp.o", CSRC / "dtkp.cu", []),
         ("maxprod.o", CSRC / "maxprod.cu", []),
+        ("maxchain.o", CSRC / "maxchain.cu", []),
     ]
     for k in range(1, 9):
         units.append((f"dtkp_apply_k{k}.o", CSRC / "dtkp_apply_k.cu", [f"-DSG_DTKP_K={k}"]))

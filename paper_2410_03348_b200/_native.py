@@ -145,6 +145,11 @@ EXPORTS = {
     "sg_chain_max_rows": (c_int32, [c_int32]),
     "sg_chain_fwd": (c_int32, [POINTER(SgChain), c_void_p, c_void_p, c_void_p]),
     "sg_chain_bwd": (c_int32, [POINTER(SgChain), c_void_p, SgRows, POINTER(SgRows), c_void_p]),
+    "sg_maxchain_states_elems": (c_int64, [c_int32, c_int32, c_int32, c_int64]),
+    "sg_maxchain_argmax_bytes": (c_int64, [c_int32, c_int32, c_int32, c_int64]),
+    "sg_maxchain_max_rows": (c_int32, [c_int32]),
+    "sg_maxchain_fwd": (c_int32, [POINTER(SgChain), c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sg_maxchain_bwd": (c_int32, [POINTER(SgChain), c_void_p, c_void_p, SgRows, POINTER(SgRows), c_void_p]),
     "sg_nll_scratch_bytes": (c_int64, [c_int64, c_int64]),
     "sg_nll_fwd": (c_int32, [SgRows, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "sg_nll_bwd": (c_int32, [SgRows, c_int64, c_int64, c_void_p, c_void_p, c_void_p, SgRows, c_void_p]),

@@ -1,0 +1,303 @@
+// Fused max-product Toeplitz chains (the north star's max/DAMP variant) for sm_100a.
+//
+// A left fold of max-product applies v_i = clamp01(max-prod(v_{i-1}, S_i)), where every
+// step is apply(f, res, d_i) with T[s][j] = s + j and the long operand first (every
+// sum_n fold step, programs.py:42-49, under DampMax), runs as ONE forward and ONE
+// backward launch instead of m generic sg_maxprod launches each way.  Per step the
+// arithmetic is exactly sg_maxprod_fwd/bwd's (maxprod.cu): the records of output o are
+// (s, o - s) in enumeration order (s ascending), value = max of the fp32 products with the
+// FIRST maximal record kept (tensor.py:319-325), clamp01 after; the backward sends g[o] to
+// that record only, and every gradient row is the fmaf sum of its contributions in record
+// order (input row s: o ascending; filter row j: s ascending) — bit-identical to the
+// per-apply kernels.
+//
+// Mapping.  Lane = sample: a sample's whole chain lives in its own shared-memory column,
+// so no two lanes ever touch the same word and the kernels need no barrier at all.  The
+// forward updates the state in place (outputs descending, four at a time from one
+// 13-row window), streams the clamped intermediate states and the argmax tap j* (one
+// byte) per (step, output, sample) to HBM row-major over the batch (coalesced).  The
+// backward walks the steps down, loads v_{i-1} into its column, and scatters each
+// output's upstream gradient to its argmax record: G_{i-1}[s*] += g[o] * S[j*] (shared
+// column) and dS[j*] += g[o] * v_{i-1}[s*] (registers, select-updated), o ascending.
+#include "common.cuh"
+
+namespace sg {
+
+constexpr int kMcMaxSteps = 32;
+
+__device__ __forceinline__ void mc_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+struct MCRows {
+  const float* p;
+  int64_t sr, sb;
+  __device__ __forceinline__ float ld(int64_t r, int64_t b) const { return __ldg(p + r * sr + b * sb); }
+};
+
+struct MaxChainArgs {
+  MCRows base;
+  MCRows filt[kMcMaxSteps];
+  float* dfilt_p[kMcMaxSteps];
+  int64_t dfilt_sr[kMcMaxSteps], dfilt_sb[kMcMaxSteps];
+  int n[kMcMaxSteps + 1];
+  int state_off[kMcMaxSteps + 1];  // row offset of v_i (i = 1..m-1) in `states`
+  int arg_off[kMcMaxSteps + 1];    // row offset of step i's argmax bytes (i = 1..m)
+  int m, n_max;
+  int64_t B;
+  float* states;         // [state rows][B]
+  uint8_t* argmax;       // [arg rows][B]: j* of output o of step i
+  float* out;            // [n_m][B]
+  double* rowsum;        // optional [B]
+  const float* g_out;    // [n_m][B]
+  float* dbase_p;
+  int64_t dbase_sr, dbase_sb;
+};
+
+template <int KF>
+__device__ __forceinline__ void maxrec(float& best, int& arg, float v, int j, bool valid) {
+  // records arrive s ascending (j descending): the first valid one seeds, later ones replace
+  // only when strictly greater — the first maximal record wins (maxprod.cu)
+  if (valid && (arg < 0 || v > best)) {
+    best = v;
+    arg = j;
+  }
+}
+
+// Forward: column V (stride 32 floats) holds KF-1 zero rows, then the state; in place.
+template <int KF>
+__global__ void __launch_bounds__(32) k_maxchain_fwd(const MaxChainArgs a) {
+  extern __shared__ float mcs[];
+  const int lane = threadIdx.x;
+  const int64_t b0 = (int64_t)blockIdx.x * 32 + lane;
+  const bool bval = b0 < a.B;
+  const int64_t b = bval ? b0 : a.B - 1;
+  constexpr int PAD = KF - 1;
+  float* V = mcs + lane;  // row r at V[(PAD + r) * 32]
+  mc_pdl_wait();
+#pragma unroll
+  for (int r = 0; r < PAD; ++r) V[r * 32] = 0.f;
+  for (int r = 0; r < a.n[0]; ++r) V[(PAD + r) * 32] = a.base.ld(r, b);
+  double rs = 0.0;
+  for (int i = 1; i <= a.m; ++i) {
+    float f[KF];
+#pragma unroll
+    for (int j = 0; j < KF; ++j) f[j] = a.filt[i - 1].ld(j, b);
+    const int nin = a.n[i - 1], nout = a.n[i];
+    const bool last = i == a.m;
+    float* gst = last ? a.out : a.states + (size_t)a.state_off[i] * a.B;
+    uint8_t* gam = a.argmax + (size_t)a.arg_off[i] * a.B;
+    // outputs descending in groups of 4 (o3 = o0 - 3 .. o0): one window of KF + 3 rows
+    for (int o0 = nout - 1; o0 >= 0; o0 -= 4) {
+      float w[KF + 3];
+#pragma unroll
+      for (int u = 0; u < KF + 3; ++u) {
+        const int s = o0 - 3 - PAD + u;  // s >= -PAD - 3; rows < -PAD read as 0 (masked below)
+        w[u] = s >= -PAD ? V[(PAD + s) * 32] : 0.f;
+      }
+      float best[4];
+      int arg[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        best[q] = 0.f;
+        arg[q] = -1;
+      }
+#pragma unroll
+      for (int j = KF - 1; j >= 0; --j) {  // s = o - j ascending
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int o = o0 - q;
+          const int s = o - j;
+          maxrec<KF>(best[q], arg[q], w[3 - q + PAD - j] * f[j], j, o >= 0 && s >= 0 && s < nin);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int o = o0 - q;
+        if (o < 0) break;
+        const float v = clamp01(best[q]);  // every output of a Toeplitz step has a record
+        V[(PAD + o) * 32] = v;
+        if (bval) {
+          gst[(size_t)o * a.B + b0] = v;
+          gam[(size_t)o * a.B + b0] = (uint8_t)arg[q];
+        }
+        if (last) rs += (double)v;
+      }
+    }
+  }
+  if (a.rowsum != nullptr && bval) a.rowsum[b0] = rs;
+}
+
+// Backward.  Columns: G (current upstream gradient, n_max rows), H (the next one),
+// Vp (v_{i-1}).
+template <int KF>
+__global__ void __launch_bounds__(32) k_maxchain_bwd(const MaxChainArgs a) {
+  extern __shared__ float mcs[];
+  const int lane = threadIdx.x;
+  const int64_t b0 = (int64_t)blockIdx.x * 32 + lane;
+  const bool bval = b0 < a.B;
+  const int64_t b = bval ? b0 : a.B - 1;
+  float* G = mcs + lane;
+  float* H = G + (size_t)a.n_max * 32;
+  float* Vp = H + (size_t)a.n_max * 32;
+  mc_pdl_wait();
+  for (int o = 0; o < a.n[a.m]; ++o) G[o * 32] = __ldg(a.g_out + (size_t)o * a.B + b);
+  for (int i = a.m; i >= 1; --i) {
+    const int nin = a.n[i - 1], nout = a.n[i];
+    float f[KF], dS[KF];
+#pragma unroll
+    for (int j = 0; j < KF; ++j) {
+      f[j] = a.filt[i - 1].ld(j, b);
+      dS[j] = 0.f;
+    }
+    if (i > 1) {
+      const float* st = a.states + (size_t)a.state_off[i - 1] * a.B;
+      for (int s = 0; s < nin; ++s) Vp[s * 32] = __ldg(st + (size_t)s * a.B + b);
+    } else {
+      for (int s = 0; s < nin; ++s) Vp[s * 32] = a.base.ld(s, b);
+    }
+    for (int s = 0; s < nin; ++s) H[s * 32] = 0.f;
+    const uint8_t* am = a.argmax + (size_t)a.arg_off[i] * a.B + b;
+    for (int o = 0; o < nout; ++o) {
+      const int j = __ldg(am + (size_t)o * a.B);
+      const int s = o - j;
+      const float g = G[o * 32];
+      float fj = f[0];
+#pragma unroll
+      for (int jj = 1; jj < KF; ++jj) fj = jj == j ? f[jj] : fj;
+      H[s * 32] = fmaf(g, fj, H[s * 32]);
+      const float vs = Vp[s * 32];
+#pragma unroll
+      for (int jj = 0; jj < KF; ++jj) dS[jj] = jj == j ? fmaf(g, vs, dS[jj]) : dS[jj];
+    }
+    if (bval) {
+#pragma unroll
+      for (int j = 0; j < KF; ++j) a.dfilt_p[i - 1][j * a.dfilt_sr[i - 1] + b0 * a.dfilt_sb[i - 1]] = dS[j];
+    }
+    float* t = G;
+    G = H;
+    H = t;
+  }
+  if (bval)
+    for (int s = 0; s < a.n[0]; ++s) a.dbase_p[s * a.dbase_sr + b0 * a.dbase_sb] = G[s * 32];
+}
+
+static int mc_fill(MaxChainArgs& a, const sg_chain* c) {
+  if (c->m < 1 || c->m > kMcMaxSteps || c->kf < 1 || c->kf > 16 || c->n0 < 1) return (int)cudaErrorInvalidValue;
+  a.base = MCRows{c->base.ptr, c->base.stride_row, c->base.stride_b};
+  a.m = c->m;
+  a.B = c->B;
+  a.n[0] = c->n0;
+  int soff = 0, aoff = 0, nmax = c->n0;
+  for (int i = 1; i <= c->m; ++i) {
+    a.n[i] = a.n[i - 1] + c->kf - 1;
+    a.filt[i - 1] = MCRows{c->filters[i - 1].ptr, c->filters[i - 1].stride_row, c->filters[i - 1].stride_b};
+    a.state_off[i] = soff;
+    if (i < c->m) soff += a.n[i];
+    a.arg_off[i] = aoff;
+    aoff += a.n[i];
+    if (a.n[i] > nmax) nmax = a.n[i];
+  }
+  a.state_off[0] = a.arg_off[0] = 0;
+  a.n_max = nmax;
+  a.states = c->states;
+  return 0;
+}
+
+template <typename... KArgs>
+static cudaError_t mc_launch(void (*kernel)(KArgs...), const MaxChainArgs& a, size_t smem, cudaStream_t st) {
+  cudaError_t e = ensure_smem((const void*)kernel, smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)ceil_div(a.B, 32));
+  cfg.blockDim = dim3(32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  count_launch();
+  return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
+#define SG_MC_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
+
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" {
+
+int64_t sg_maxchain_states_elems(int32_t n0, int32_t kf, int32_t m, int64_t B) {
+  int64_t rows = 0, n = n0;
+  for (int i = 1; i < m; ++i) {
+    n += kf - 1;
+    rows += n;
+  }
+  return rows * B;
+}
+
+int64_t sg_maxchain_argmax_bytes(int32_t n0, int32_t kf, int32_t m, int64_t B) {
+  int64_t rows = 0, n = n0;
+  for (int i = 1; i <= m; ++i) {
+    n += kf - 1;
+    rows += n;
+  }
+  return rows * B;
+}
+
+int32_t sg_maxchain_max_rows(int32_t kf) {
+  if (kf < 1 || kf > 16) return 0;
+  // backward: three columns of n_max rows x 32 lanes x 4 B within 227 KB
+  return (int32_t)(227 * 1024 / (3 * 32 * 4));
+}
+
+int sg_maxchain_fwd(const sg_chain* c, float* out, double* rowsum, uint8_t* argmax, sg_stream_t stream) {
+  MaxChainArgs a{};
+  int rc = mc_fill(a, c);
+  if (rc) return rc;
+  if (c->B <= 0) return 0;
+  SG_RETURN_IF(a.n_max > sg_maxchain_max_rows(c->kf), cudaErrorNotSupported);
+  a.out = out;
+  a.rowsum = rowsum;
+  a.argmax = argmax;
+  const size_t smem = (size_t)(c->kf - 1 + a.n_max) * 32 * sizeof(float);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (c->kf) {
+#define X(K) \
+  case K: return (int)mc_launch(k_maxchain_fwd<K>, a, smem, st);
+    SG_MC_CASES(X)
+#undef X
+    default: return (int)cudaErrorInvalidValue;
+  }
+}
+
+int sg_maxchain_bwd(const sg_chain* c, const uint8_t* argmax, const float* grad_out, sg_rows grad_base,
+                    const sg_rows* grad_filters, sg_stream_t stream) {
+  MaxChainArgs a{};
+  int rc = mc_fill(a, c);
+  if (rc) return rc;
+  if (c->B <= 0) return 0;
+  SG_RETURN_IF(a.n_max > sg_maxchain_max_rows(c->kf), cudaErrorNotSupported);
+  a.argmax = const_cast<uint8_t*>(argmax);
+  a.g_out = grad_out;
+  a.dbase_p = grad_base.ptr;
+  a.dbase_sr = grad_base.stride_row;
+  a.dbase_sb = grad_base.stride_b;
+  for (int i = 0; i < c->m; ++i) {
+    a.dfilt_p[i] = grad_filters[i].ptr;
+    a.dfilt_sr[i] = grad_filters[i].stride_row;
+    a.dfilt_sb[i] = grad_filters[i].stride_b;
+  }
+  const size_t smem = (size_t)3 * a.n_max * 32 * sizeof(float);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (c->kf) {
+#define X(K) \
+  case K: return (int)mc_launch(k_maxchain_bwd<K>, a, smem, st);
+    SG_MC_CASES(X)
+#undef X
+    default: return (int)cudaErrorInvalidValue;
+  }
+}
+
+}  // extern "C"

@@ -289,6 +289,61 @@ class ConvChainFn(torch.autograd.Function):
         return (None, None, None, gbase, *gfilt)
 
 
+@functools.lru_cache(maxsize=None)
+def maxchain_max_rows(kf: int) -> int:
+    return int(_lib().sg_maxchain_max_rows(kf))
+
+
+class MaxChainFn(torch.autograd.Function):
+    """The max/DAMP variant of ConvChainFn: a left fold of max-product Toeplitz applies in
+    one forward and one backward launch (csrc/maxchain.cu), per step bit-identical to
+    MaxProdApply (first-argmax gradient, pass-through clamp)."""
+
+    @staticmethod
+    def forward(ctx, n0: int, kf: int, B: int, base, *filters):
+        m = len(filters)
+        dev = base.device
+        _check_operand(base, "max chain base")
+        for f in filters:
+            _check_operand(f, "max chain filter")
+        states = torch.empty((max(int(_lib().sg_maxchain_states_elems(n0, kf, m, B)), 1),), device=dev, dtype=F32)
+        argmax = torch.empty((max(int(_lib().sg_maxchain_argmax_bytes(n0, kf, m, B)), 1),), device=dev,
+                             dtype=torch.uint8)
+        out = torch.empty((n0 + m * (kf - 1), B), device=dev, dtype=F32)
+        rowsum = torch.empty((B,), device=dev, dtype=torch.float64)
+        c = _chain_struct(n0, kf, B, base, filters, states)
+        with launch_timer("maxchain_fwd"):
+            rc = _lib().sg_maxchain_fwd(ctypes.byref(c), out.data_ptr(), rowsum.data_ptr(), argmax.data_ptr(),
+                                        N.stream_ptr(dev))
+        N.check(rc, "sg_maxchain_fwd")
+        _ledger("maxchain_fwd", 4 * B * (n0 + m * kf + states.numel() // max(B, 1) + out.shape[0]) + argmax.numel()
+                + 8 * B, B * sum((n0 + i * (kf - 1)) * kf for i in range(m)))
+        out._sg_rowsum = (rowsum, out._version)
+        ctx.meta = (n0, kf, B)
+        ctx.save_for_backward(base, states, argmax, *filters)
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        base, states, argmax, *filters = ctx.saved_tensors
+        n0, kf, B = ctx.meta
+        g = g.contiguous()
+        gbase = torch.empty_like(base)
+        gfilt = [torch.empty_like(f) for f in filters]
+        c = _chain_struct(n0, kf, B, base, filters, states)
+        arr = (N.SgRows * N.CHAIN_MAX_STEPS)()
+        for i, t in enumerate(gfilt):
+            arr[i] = N.rows(t)
+        with launch_timer("maxchain_bwd"):
+            rc = _lib().sg_maxchain_bwd(ctypes.byref(c), argmax.data_ptr(), g.data_ptr(), N.rows(gbase), arr,
+                                        N.stream_ptr(g.device))
+        N.check(rc, "sg_maxchain_bwd")
+        m = len(filters)
+        _ledger("maxchain_bwd", 4 * B * (g.shape[0] + 2 * m * kf + states.numel() // max(B, 1) + 2 * n0)
+                + argmax.numel(), B * sum((n0 + i * (kf - 1)) * kf for i in range(m)))
+        return (None, None, None, gbase, *gfilt)
+
+
 def _chain_struct(n0, kf, B, base, filters, states) -> N.SgChain:
     c = N.SgChain()
     c.base = N.rows(base)

@@ -140,31 +140,35 @@ class _ConvChain:
     materialises it with ONE fused forward launch, and autograd runs ONE fused backward
     (ops.ConvChainFn).  Results equal the per-apply kernels step for step."""
 
-    __slots__ = ("base", "filters", "kf", "B", "n_out", "first_plan")
+    __slots__ = ("base", "filters", "kf", "B", "n_out", "first_plan", "kind")
     MAX_STEPS = 32
 
     @staticmethod
-    def max_rows(kf: int) -> int:
+    def max_rows(kf: int, kind: str = "sum") -> int:
         """Longest state (rows) whose fwd/bwd shared-memory working set fits one CTA."""
-        return ops.chain_max_rows(kf)
+        return ops.chain_max_rows(kf) if kind == "sum" else ops.maxchain_max_rows(kf)
 
-    def __init__(self, base, filters, kf, B, n_out, first_plan):
+    def __init__(self, base, filters, kf, B, n_out, first_plan, kind="sum"):
         self.base, self.filters, self.kf, self.B, self.n_out = base, filters, kf, B, n_out
         self.first_plan = first_plan
+        self.kind = kind
 
-    def can_extend(self, kf: int, B: int, n_out: int) -> bool:
-        return (kf == self.kf and B == self.B and len(self.filters) < self.MAX_STEPS
-                and n_out <= self.max_rows(kf) and n_out == self.n_out + kf - 1)
+    def can_extend(self, kf: int, B: int, n_out: int, kind: str = "sum") -> bool:
+        return (kind == self.kind and kf == self.kf and B == self.B and len(self.filters) < self.MAX_STEPS
+                and n_out <= self.max_rows(kf, kind) and n_out == self.n_out + kf - 1)
 
     def extend(self, short_sm: torch.Tensor, n_out: int) -> "_ConvChain":
-        return _ConvChain(self.base, self.filters + [short_sm], self.kf, self.B, n_out, self.first_plan)
+        return _ConvChain(self.base, self.filters + [short_sm], self.kf, self.B, n_out, self.first_plan, self.kind)
 
     def materialize(self) -> torch.Tensor:
-        if len(self.filters) == 1:  # a single apply: the per-apply Toeplitz kernel
-            return ops.damp_apply(self.first_plan, _conv_operands(self.first_plan, self.base, self.filters[0]),
-                                  self.B)
-        return ops.ConvChainFn.apply(self.base.shape[0], self.kf, self.B, ops.expand_batch(self.base, self.B),
-                                     *[ops.expand_batch(f, self.B) for f in self.filters])
+        if len(self.filters) == 1:  # a single apply: the per-apply kernel
+            ops_ = _conv_operands(self.first_plan, self.base, self.filters[0])
+            if self.kind == "max":
+                return ops.maxprod_apply(self.first_plan, ops_, self.B)
+            return ops.damp_apply(self.first_plan, ops_, self.B)
+        fn = ops.ConvChainFn if self.kind == "sum" else ops.MaxChainFn
+        return fn.apply(self.base.shape[0], self.kf, self.B, ops.expand_batch(self.base, self.B),
+                        *[ops.expand_batch(f, self.B) for f in self.filters])
 
 
 def _conv_operands(kp, long_sm, short_sm):
@@ -354,8 +358,20 @@ class DampMax(Damp):
                                        tags.batch))
 
     def apply_plan(self, tags_list, plan: SymbolPlan, batch: int) -> DampTags:
-        """gather -> product fold -> max bucket (+clamp) in one sg_maxprod_fwd launch."""
-        return _damp(ops.maxprod_apply(plan.kernel_plan(), [t.sm for t in tags_list], batch))
+        """gather -> product fold -> max bucket (+clamp) in one sg_maxprod_fwd launch;
+        Toeplitz applies whose long operand (input 0, so records are ordered by it) is the
+        previous apply's output fold into one fused max chain (sg_maxchain_*)."""
+        kp = plan.kernel_plan()
+        if self.fuse_chains and kp.conv == 1 and kp.conv_short == 1 and len(tags_list) == 2:
+            long_t, short_t = tags_list[0], tags_list[1]
+            kf = kp.sizes[1]
+            if short_t.batch in (1, batch) and long_t.batch in (1, batch) and \
+                    kp.n_out <= _ConvChain.max_rows(kf, "max"):
+                ch = long_t._chain
+                if ch is not None and ch.can_extend(kf, batch, kp.n_out, "max"):
+                    return DampTags(chain=ch.extend(short_t.sm, kp.n_out))
+                return DampTags(chain=_ConvChain(long_t.sm, [short_t.sm], kf, batch, kp.n_out, kp, "max"))
+        return _damp(ops.maxprod_apply(kp, [t.sm for t in tags_list], batch))
 
     def union_tags(self, a: DampTags, b: DampTags, uplan) -> DampTags:
         return self._pairwise_max(a, b, uplan.ia, uplan.ib)

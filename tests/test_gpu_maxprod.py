@@ -88,3 +88,60 @@ def test_max_decomposed_operators(cuda):
     ref = np.stack([a_np[:, g].max(axis=1) if g else np.zeros(B) for g in groups], axis=1)
     _close(got, ref, "group_disj")
     _close(prov.gather(a, [6, 0, 6]).value.cpu().numpy(), a_np[:, [6, 0, 6]], "gather")
+
+
+def _max_sum_chain(xs, fuse, targets=None, w=None):
+    import paper_2410_03348_b200 as sg
+    from paper_2410_03348_b200 import programs as P
+    from paper_2410_03348_b200.learn import loss_nll
+
+    old = sg.DampMax.fuse_chains
+    sg.DampMax.fuse_chains = fuse
+    try:
+        ctx = sg.ProgramContext(sg.DampMax(), device="cuda")
+        leaves = [torch.tensor(x, device="cuda", dtype=torch.float32, requires_grad=True) for x in xs]
+        out = P.sum_n(ctx, [sg.make_distribution(ctx, lf, list(range(x.shape[1]))) for lf, x in zip(leaves, xs)])
+        probs = sg.get_probs(out)
+        if targets is not None:
+            loss = loss_nll(probs, torch.as_tensor(targets, device="cuda"))
+        else:
+            loss = (probs.double() * torch.as_tensor(w, device="cuda")).sum()
+        loss.backward()
+        return out, probs.detach().double().cpu().numpy(), [lf.grad.double().cpu().numpy() for lf in leaves]
+    finally:
+        sg.DampMax.fuse_chains = old
+
+
+@pytest.mark.parametrize("n,B", [(15, 1000), (4, 33), (9, 257), (15, 16384)])
+def test_max_chain_bit_identical_to_per_apply_kernels(cuda, n, B):
+    """The fused max chain (sg_maxchain_*) equals the per-apply sg_maxprod path bit for bit
+    (same products, first-argmax routing, fmaf order), loss included."""
+    rng = np.random.default_rng(n * 7 + B)
+    xs = [_rows(rng, B, 10) for _ in range(n)]
+    t = rng.integers(0, 9 * n + 1, size=B)
+    out_f, p_f, g_f = _max_sum_chain(xs, True, targets=t)
+    out_u, p_u, g_u = _max_sum_chain(xs, False, targets=t)
+    assert out_f.symbols == out_u.symbols
+    np.testing.assert_array_equal(p_f, p_u)
+    for a, b in zip(g_f, g_u):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("uniform", [False, True])
+def test_max_chain_vs_oracle(cuda, uniform):
+    """Sum-6 under the max variant vs the oracle; uniform inputs make every record of an
+    output tie, so every gradient must follow the first-argmax rule exactly."""
+    from oracle import programs as OP
+    from paper_2410_03348_b200.plan import UNDEFINED
+
+    rng = np.random.default_rng(11)
+    B, n = 37, 6
+    xs = [np.full((B, 10), 0.1) if uniform else _rows(rng, B, 10) for _ in range(n)]
+    xs = [x.astype(np.float32).astype(np.float64) for x in xs]
+    w = rng.uniform(-1, 1, size=(B, 9 * n + 1))
+    _, probs, grads = _max_sum_chain(xs, True, w=w)
+    ctx = OP.OContext("max", None, undefined=UNDEFINED)
+    out = OP.sum_n([OP.make_distribution(ctx, x, list(range(10))) for x in xs])
+    _close(probs, OP.get_probs(out), "max chain probs")
+    for g, r in zip(grads, OP.grad_inputs(out, w)):
+        _close(g, r, "max chain grads", floor=1e-6)

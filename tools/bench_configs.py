@@ -370,7 +370,44 @@ def sweep_point(dev, arity, size, B, iters=20, cpu=True, provenance="damp"):
     return res
 
 
-def all_configs(dev, iters=20, cpu=True, only=("sum2", "hwf7", "clutrr", "sweep")):
+# ------------------------------------------------------------------ max/DAMP variant, Sum-15
+def max_sum15(dev, iters=20, B=16384):
+    """The north star's max/DAMP variant on the headline shape: Sum-15 chain under DampMax
+    (fused sg_maxchain_fwd/bwd) + loss_nll, fwd + bwd, B=16384."""
+    rng = np.random.default_rng(15)
+    xs_h = torch.tensor(np.stack([rows(rng, B, 10) for _ in range(15)]))
+    xs = [xs_h[i].to(dev).requires_grad_(True) for i in range(15)]
+    tgt_h = torch.tensor(rng.integers(0, 136, size=B))
+    targets = tgt_h.to(dev)
+
+    def step_on(xl, t):
+        c = sg.ProgramContext(sg.DampMax(), device=dev)
+        o = P.sum_n(c, [sg.make_distribution(c, x, list(range(10))) for x in xl])
+        loss = loss_nll(sg.get_probs(o), t)
+        return loss, torch.autograd.grad(loss, xl)
+
+    flush = Flusher(dev)
+    ms, mode = graph_time(lambda: step_on(xs, targets), dev, iters, flush)
+    alg, by = ledger(lambda: step_on(xs, targets))
+    pin_x, pin_t = xs_h.pin_memory(), tgt_h.pin_memory()
+
+    def host_step():
+        xd = pin_x.to(dev, non_blocking=True)
+        loss, _ = step_on([xd[i].requires_grad_(True) for i in range(15)], pin_t.to(dev, non_blocking=True))
+        return loss.item()
+
+    e2e_ms = e2e_time(host_step, dev, iters)
+    hbm, src = hbm_peak()
+    return {"config": "max/DAMP variant: Sum-15 chain (14 max-product applies) + loss_nll, fwd+bwd, B=16384",
+            "metric": "symbol-combos/s", "batch": B,
+            "device": {"ms_per_step": ms, "value": B * 9590 / (ms * 1e-3), "mode": mode},
+            "e2e": {"ms_per_step": e2e_ms, "value": B * 9590 / (e2e_ms * 1e-3),
+                    "h2d_bytes_per_step": pin_x.numel() * 4 + B * 8, "d2h_bytes_per_step": 8,
+                    "api": "eager sum_n under DampMax + loss_nll + autograd.grad, inputs H2D + loss.item()"},
+            "roofline": roofline(alg, by, ms, hbm, src)}
+
+
+def all_configs(dev, iters=20, cpu=True, only=("sum2", "hwf7", "clutrr", "sweep", "max15")):
     out = {}
     if "sum2" in only:
         out["sum2_train"] = sum2_train(dev, iters, cpu)
@@ -381,6 +418,8 @@ def all_configs(dev, iters=20, cpu=True, only=("sum2", "hwf7", "clutrr", "sweep"
     if "sweep" in only:
         for a, s, b in SWEEP:
             out[f"sweep_a{a}_s{s}_b{b}"] = sweep_point(dev, a, s, b, iters, cpu)
+    if "max15" in only:
+        out["max_sum15"] = max_sum15(dev, iters)
     if "maxsweep" in only:
         for a, s, b in [(2, 10, 65536), (2, 100, 16384), (3, 10, 16384)]:
             out[f"max_sweep_a{a}_s{s}_b{b}"] = sweep_point(dev, a, s, b, iters, False, provenance="max")
@@ -389,7 +428,7 @@ def all_configs(dev, iters=20, cpu=True, only=("sum2", "hwf7", "clutrr", "sweep"
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="sum2,hwf7,clutrr,sweep")
+    ap.add_argument("--only", default="sum2,hwf7,clutrr,sweep,max15")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
