@@ -172,6 +172,10 @@ int sg_chain_fwd(const sg_chain* chain, float* out, double* rowsum, sg_stream_t 
 int sg_chain_bwd(const sg_chain* chain, const float* grad_out, sg_rows grad_base,
                  const sg_rows* grad_filters, sg_stream_t stream);
 
+/* 1 when sg_damp_apply_bwd of a short-filter Toeplitz plan (conv == 1) reads its upstream
+ * gradient in any layout (the staged kernels); 0: it must be contiguous [n_out][B]. */
+int32_t sg_damp_conv_staged(int32_t kf, int32_t n_long, int32_t n_out);
+
 /* ---- fused max-product Toeplitz chain (the north star's max/DAMP variant) ------------
  * The same left fold as sg_chain_* under DampMax (long operand first, kf-row filters):
  * v_i = clamp01(max_s v_{i-1}[s] * S_i[o - s]), first maximal record (s ascending) kept;

@@ -645,6 +645,170 @@ static int conv_bwd_t(const float* g, int n_out, const Rows& L, int nL, const Ro
 
 #define SG_CONV_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
 
+// ------------------------------- staged short-filter Toeplitz ------------------------
+// The same applies as k_conv_fwd / k_conv_bwd (identical forward FMA order), for CTAs of
+// 32 samples x 4 warps that first stage every operand row of their samples in shared
+// memory ([rows][33]): a user (B, n) block read in place is one CONTIGUOUS span per 32
+// samples (32 n floats), so it is loaded with linear, fully coalesced accesses and
+// transposed on the way in — instead of every warp-wide row load touching n lines (the
+// strided in-place read that made the unstaged kernels L1-wavefront bound).  Gradients are
+// staged the same way on the way out, and the upstream gradient is read in place in either
+// layout (no transpose copy before the backward).  Lane = sample; warps split the output
+// rows (tiles of 8 rows from one register window) and the filter-gradient rows.
+constexpr int kCsRows = 8;     // rows per warp tile
+constexpr int kCsPitch = 33;   // shared row pitch (floats): conflict-free transposed stores
+__device__ __forceinline__ int cs_div(int a, int b) { return (a + b - 1) / b; }
+
+// rows [0, n) of X for samples b0 .. b0 + 31 -> sm[r * kCsPitch + s] (0 past B)
+__device__ __forceinline__ void cs_stage(float* sm, const Rows& X, int n, int64_t B, int64_t b0) {
+  const int tid = threadIdx.x;
+  const int nt = blockDim.x;
+  const int ns = (int)(B - b0 < kWarp ? B - b0 : kWarp);
+  if (X.sr == 1 && X.sb != 0) {  // sample-major (user block): sample s's row is contiguous
+    for (int i = tid; i < kWarp * n; i += nt) {
+      const int sidx = i / n, r = i - sidx * n;
+      sm[r * kCsPitch + sidx] = sidx < ns ? __ldg(X.p + (b0 + sidx) * X.sb + r) : 0.f;
+    }
+  } else {  // symbol-major rows (or a batch broadcast): row r over the samples
+    for (int i = tid; i < kWarp * n; i += nt) {
+      const int r = i >> 5, sidx = i & 31;
+      sm[r * kCsPitch + sidx] = sidx < ns ? __ldg(X.p + (int64_t)r * X.sr + (b0 + sidx) * X.sb) : 0.f;
+    }
+  }
+}
+
+// sm[r * kCsPitch + s] -> rows [0, n) of Y for samples b0 .. b0 + 31 (coalesced either way)
+__device__ __forceinline__ void cs_unstage(const float* sm, const WRows& Y, int n, int64_t B, int64_t b0) {
+  const int tid = threadIdx.x;
+  const int nt = blockDim.x;
+  const int ns = (int)(B - b0 < kWarp ? B - b0 : kWarp);
+  if (Y.sr == 1) {
+    for (int i = tid; i < kWarp * n; i += nt) {
+      const int sidx = i / n, r = i - sidx * n;
+      if (sidx < ns) Y.p[(b0 + sidx) * Y.sb + r] = sm[r * kCsPitch + sidx];
+    }
+  } else {
+    for (int i = tid; i < kWarp * n; i += nt) {
+      const int r = i >> 5, sidx = i & 31;
+      if (sidx < ns) Y.p[(int64_t)r * Y.sr + (b0 + sidx) * Y.sb] = sm[r * kCsPitch + sidx];
+    }
+  }
+}
+
+template <int KF>
+__global__ void __launch_bounds__(128) k_convs_fwd(const Rows L, int nL, const Rows S, float* __restrict__ out,
+                                                   int n_out, int64_t B) {
+  extern __shared__ float csm[];
+  float* sS = csm;                          // [KF][33]
+  float* sL = csm + KF * kCsPitch;          // [(KF - 1) zero rows + nL (+ tile slack)][33]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t b0 = (int64_t)blockIdx.x * kWarp;
+  const int64_t b = b0 + lane;
+  pdl_wait();
+  cs_stage(sS, S, KF, B, b0);
+  cs_stage(sL + (KF - 1) * kCsPitch, L, nL, B, b0);
+  const int lrows = KF - 1 + nL;
+  const int lcap = KF - 1 + cs_div(n_out, kCsRows) * kCsRows;
+  for (int i = threadIdx.x; i < (KF - 1) * kCsPitch; i += blockDim.x) sL[i] = 0.f;
+  for (int i = lrows * kCsPitch + threadIdx.x; i < lcap * kCsPitch; i += blockDim.x) sL[i] = 0.f;
+  __syncthreads();
+  pdl_trigger();
+  float f[KF];
+#pragma unroll
+  for (int j = 0; j < KF; ++j) f[j] = sS[j * kCsPitch + lane];
+  const int n_tiles = cs_div(n_out, kCsRows);
+  for (int t = warp; t < n_tiles; t += 4) {
+    const int o0 = t * kCsRows;
+    float w[kCsRows + KF - 1];  // L rows o0 - (KF - 1) .. o0 + kCsRows - 1 (zero-padded)
+#pragma unroll
+    for (int u = 0; u < kCsRows + KF - 1; ++u) w[u] = sL[(o0 + u) * kCsPitch + lane];
+#pragma unroll
+    for (int r = 0; r < kCsRows; ++r) {
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < KF; ++j) acc = fmaf(w[r + KF - 1 - j], f[j], acc);  // k_conv_fwd's order
+      const int o = o0 + r;
+      if (o < n_out && b < B) out[(size_t)o * B + b] = clamp01(acc);
+    }
+  }
+}
+
+// dL[s] = sum_j g[s + j] S[j] (j ascending);  dS[j] = sum_s g[s + j] L[s] (s ascending)
+template <int KF>
+__global__ void __launch_bounds__(128) k_convs_bwd(const Rows g, int n_out, const Rows L, int nL, const Rows S,
+                                                   WRows dL, WRows dS, int64_t B) {
+  extern __shared__ float csm[];
+  const int gcap = cs_div(nL, kCsRows) * kCsRows + KF;  // g rows + zero slack for the windows
+  float* sS = csm;                           // [KF][33]
+  float* sG = sS + KF * kCsPitch;            // [gcap][33]
+  float* sL = sG + gcap * kCsPitch;          // [nL][33]
+  float* sdL = sL + nL * kCsPitch;           // [nL][33]
+  float* sdS = sdL + nL * kCsPitch;          // [KF][33]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t b0 = (int64_t)blockIdx.x * kWarp;
+  pdl_wait();
+  cs_stage(sS, S, KF, B, b0);
+  cs_stage(sG, g, n_out, B, b0);
+  cs_stage(sL, L, nL, B, b0);
+  for (int i = n_out * kCsPitch + threadIdx.x; i < gcap * kCsPitch; i += blockDim.x) sG[i] = 0.f;
+  __syncthreads();
+  pdl_trigger();
+  {
+    float f[KF];
+#pragma unroll
+    for (int j = 0; j < KF; ++j) f[j] = sS[j * kCsPitch + lane];
+    const int n_tiles = cs_div(nL, kCsRows);
+    for (int t = warp; t < n_tiles; t += 4) {
+      const int s0 = t * kCsRows;
+      float gw[kCsRows + KF - 1];
+#pragma unroll
+      for (int u = 0; u < kCsRows + KF - 1; ++u) gw[u] = sG[(s0 + u) * kCsPitch + lane];
+#pragma unroll
+      for (int r = 0; r < kCsRows; ++r) {
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 0; j < KF; ++j) acc = fmaf(gw[r + j], f[j], acc);
+        if (s0 + r < nL) sdL[(s0 + r) * kCsPitch + lane] = acc;
+      }
+    }
+  }
+  for (int j = warp; j < KF; j += 4) {
+    float acc = 0.f;
+    for (int s0 = 0; s0 < nL; ++s0) acc = fmaf(sG[(s0 + j) * kCsPitch + lane], sL[s0 * kCsPitch + lane], acc);
+    sdS[j * kCsPitch + lane] = acc;
+  }
+  __syncthreads();
+  cs_unstage(sdL, dL, nL, B, b0);
+  cs_unstage(sdS, dS, KF, B, b0);
+}
+
+static size_t convs_fwd_smem(int kf, int n_out) {
+  return (size_t)(kf + kf - 1 + ceil_div(n_out, kCsRows) * kCsRows + kCsRows) * kCsPitch * sizeof(float);
+}
+static size_t convs_bwd_smem(int kf, int nL) {
+  return (size_t)(kf + ceil_div(nL, kCsRows) * kCsRows + kf + 2 * nL + kf) * kCsPitch * sizeof(float);
+}
+static bool convs_fits(int kf, int nL, int n_out) {
+  return convs_fwd_smem(kf, n_out) <= 96 * 1024 && convs_bwd_smem(kf, nL) <= 96 * 1024;
+}
+
+template <int KF>
+static int convs_fwd_t(const Rows& L, int nL, const Rows& S, float* out, int n_out, int64_t B, cudaStream_t st) {
+  const size_t smem = convs_fwd_smem(KF, n_out);
+  cudaError_t e = ensure_smem((const void*)k_convs_fwd<KF>, smem);
+  if (e != cudaSuccess) return (int)e;
+  return (int)launch(k_convs_fwd<KF>, dim3(ceil_div(B, kWarp)), dim3(128), smem, st, L, nL, S, out, n_out, B);
+}
+
+template <int KF>
+static int convs_bwd_t(const Rows& g, int n_out, const Rows& L, int nL, const Rows& S, const WRows& dL,
+                       const WRows& dS, int64_t B, cudaStream_t st) {
+  const size_t smem = convs_bwd_smem(KF, nL);
+  cudaError_t e = ensure_smem((const void*)k_convs_bwd<KF>, smem);
+  if (e != cudaSuccess) return (int)e;
+  return (int)launch(k_convs_bwd<KF>, dim3(ceil_div(B, kWarp)), dim3(128), smem, st, g, n_out, L, nL, S, dL, dS, B);
+}
+
 // ------------------------------- long Toeplitz (both operands long) ------------------
 // f = sum over two long symbol lists (sweep |S| = 100, 1000): every output is a full 1-D
 // convolution per sample, O(|S|) multiply-adds per output, so this is FMA-bound, not
@@ -723,21 +887,44 @@ static int lconv(const Rows& X, int nx, const Rows& H, int nh, int t0, const WRo
 
 static Rows reversed(const Rows& r, int n) { return Rows{r.p + (int64_t)(n - 1) * r.sr, -r.sr, r.sb}; }
 
+#ifndef SG_CONV_STAGED  // 0: always the unstaged k_conv_* kernels (A/B runs)
+#define SG_CONV_STAGED 1
+#endif
+static bool conv_staged(int kf, int nL, int n_out) {
+  static const bool off = [] {
+    const char* e = getenv("SG_CONV_UNSTAGED");
+    return e != nullptr && e[0] == '1';
+  }();
+  return SG_CONV_STAGED && !off && convs_fits(kf, nL, n_out);
+}
+
 static int conv_fwd(int kf, const Rows& L, int nL, const Rows& S, float* out, int n_out, int64_t B, cudaStream_t st) {
+  const bool staged = conv_staged(kf, nL, n_out);
   switch (kf) {
 #define X(K) \
-  case K: return conv_fwd_t<K>(L, nL, S, out, n_out, B, st);
+  case K: return staged ? convs_fwd_t<K>(L, nL, S, out, n_out, B, st) : conv_fwd_t<K>(L, nL, S, out, n_out, B, st);
     SG_CONV_CASES(X)
 #undef X
     default: return (int)cudaErrorInvalidValue;
   }
 }
 
-static int conv_bwd(int kf, const float* g, int n_out, const Rows& L, int nL, const Rows& S, const WRows& dL,
+// g: the staged kernel reads any layout; the unstaged one needs contiguous [n_out][B]
+static int conv_bwd(int kf, const Rows& g, int n_out, const Rows& L, int nL, const Rows& S, const WRows& dL,
                     const WRows& dS, int64_t B, cudaStream_t st) {
+  if (conv_staged(kf, nL, n_out)) {
+    switch (kf) {
+#define X(K) \
+  case K: return convs_bwd_t<K>(g, n_out, L, nL, S, dL, dS, B, st);
+      SG_CONV_CASES(X)
+#undef X
+      default: return (int)cudaErrorInvalidValue;
+    }
+  }
+  SG_RETURN_IF((B > 1 && g.sb != 1) || (n_out > 1 && g.sr != B), cudaErrorInvalidValue);
   switch (kf) {
 #define X(K) \
-  case K: return conv_bwd_t<K>(g, n_out, L, nL, S, dL, dS, B, st);
+  case K: return conv_bwd_t<K>(g.p, n_out, L, nL, S, dL, dS, B, st);
     SG_CONV_CASES(X)
 #undef X
     default: return (int)cudaErrorInvalidValue;
@@ -1123,9 +1310,7 @@ int sg_damp_apply_bwd(const sg_damp_plan* plan, const sg_rows* inputs, sg_rows g
   if (plan->conv) {
     const int sh = plan->conv_short, lo = 1 - sh;
     SG_RETURN_IF(grad_in[0].ptr == nullptr || grad_in[1].ptr == nullptr, cudaErrorInvalidValue);
-    SG_RETURN_IF((B > 1 && grad_rows.stride_b != 1) || (plan->n_out > 1 && grad_rows.stride_row != B),
-                 cudaErrorInvalidValue);
-    return conv_bwd(plan->sizes[sh], grad_rows.ptr, plan->n_out, rows_of(inputs[lo]), plan->sizes[lo], rows_of(inputs[sh]),
+    return conv_bwd(plan->sizes[sh], g, plan->n_out, rows_of(inputs[lo]), plan->sizes[lo], rows_of(inputs[sh]),
                     wrows_of(grad_in[lo]), wrows_of(grad_in[sh]), B, st);
   }
   for (int k = 0; k < n; ++k) {
@@ -1156,6 +1341,10 @@ int sg_damp_rows_add(const sg_rows A, const int32_t* ia, const sg_rows Bm, const
   dim3 grid(gx, n_rows < 65535 ? (unsigned)n_rows : 65535u);
   return (int)launch(k_rows_add, grid, dim3(threads), 0, (cudaStream_t)stream, rows_of(A), ia, rows_of(Bm), ib,
                      n_rows, B, (int)clamp01_, out);
+}
+
+int32_t sg_damp_conv_staged(int32_t kf, int32_t n_long, int32_t n_out) {
+  return conv_staged(kf, n_long, n_out) ? 1 : 0;
 }
 
 int64_t sg_nll_scratch_bytes(int64_t n, int64_t B) {

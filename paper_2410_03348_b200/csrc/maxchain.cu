@@ -75,12 +75,20 @@ __global__ void __launch_bounds__(32) k_maxchain_fwd(const MaxChainArgs a) {
   mc_pdl_wait();
 #pragma unroll
   for (int r = 0; r < PAD; ++r) V[r * 32] = 0.f;
+#pragma unroll 8
   for (int r = 0; r < a.n[0]; ++r) V[(PAD + r) * 32] = a.base.ld(r, b);
   double rs = 0.0;
+  float fn[KF];  // the next step's filter, loaded one step ahead
+#pragma unroll
+  for (int j = 0; j < KF; ++j) fn[j] = a.filt[0].ld(j, b);
   for (int i = 1; i <= a.m; ++i) {
     float f[KF];
 #pragma unroll
-    for (int j = 0; j < KF; ++j) f[j] = a.filt[i - 1].ld(j, b);
+    for (int j = 0; j < KF; ++j) f[j] = fn[j];
+    if (i < a.m) {
+#pragma unroll
+      for (int j = 0; j < KF; ++j) fn[j] = a.filt[i].ld(j, b);
+    }
     const int nin = a.n[i - 1], nout = a.n[i];
     const bool last = i == a.m;
     float* gst = last ? a.out : a.states + (size_t)a.state_off[i] * a.B;
@@ -139,34 +147,55 @@ __global__ void __launch_bounds__(32) k_maxchain_bwd(const MaxChainArgs a) {
   float* H = G + (size_t)a.n_max * 32;
   float* Vp = H + (size_t)a.n_max * 32;
   mc_pdl_wait();
+#pragma unroll 8
   for (int o = 0; o < a.n[a.m]; ++o) G[o * 32] = __ldg(a.g_out + (size_t)o * a.B + b);
+  float fn[KF];  // the next (lower) step's filter, loaded one step ahead
+#pragma unroll
+  for (int j = 0; j < KF; ++j) fn[j] = a.filt[a.m - 1].ld(j, b);
   for (int i = a.m; i >= 1; --i) {
     const int nin = a.n[i - 1], nout = a.n[i];
     float f[KF], dS[KF];
 #pragma unroll
     for (int j = 0; j < KF; ++j) {
-      f[j] = a.filt[i - 1].ld(j, b);
+      f[j] = fn[j];
       dS[j] = 0.f;
     }
     if (i > 1) {
+#pragma unroll
+      for (int j = 0; j < KF; ++j) fn[j] = a.filt[i - 2].ld(j, b);
+    }
+    if (i > 1) {
       const float* st = a.states + (size_t)a.state_off[i - 1] * a.B;
+#pragma unroll 8
       for (int s = 0; s < nin; ++s) Vp[s * 32] = __ldg(st + (size_t)s * a.B + b);
     } else {
+#pragma unroll 8
       for (int s = 0; s < nin; ++s) Vp[s * 32] = a.base.ld(s, b);
     }
     for (int s = 0; s < nin; ++s) H[s * 32] = 0.f;
     const uint8_t* am = a.argmax + (size_t)a.arg_off[i] * a.B + b;
-    for (int o = 0; o < nout; ++o) {
-      const int j = __ldg(am + (size_t)o * a.B);
-      const int s = o - j;
-      const float g = G[o * 32];
-      float fj = f[0];
+    // the argmax taps of 16 outputs are loaded together (independent loads in flight),
+    // then the outputs are scattered in ascending order
+    constexpr int kBatch = 16;
+    for (int o0 = 0; o0 < nout; o0 += kBatch) {
+      int jb[kBatch];
 #pragma unroll
-      for (int jj = 1; jj < KF; ++jj) fj = jj == j ? f[jj] : fj;
-      H[s * 32] = fmaf(g, fj, H[s * 32]);
-      const float vs = Vp[s * 32];
+      for (int q = 0; q < kBatch; ++q) jb[q] = o0 + q < nout ? (int)__ldg(am + (size_t)(o0 + q) * a.B) : 0;
 #pragma unroll
-      for (int jj = 0; jj < KF; ++jj) dS[jj] = jj == j ? fmaf(g, vs, dS[jj]) : dS[jj];
+      for (int q = 0; q < kBatch; ++q) {
+        const int o = o0 + q;
+        if (o >= nout) break;
+        const int j = jb[q];
+        const int s = o - j;
+        const float g = G[o * 32];
+        float fj = f[0];
+#pragma unroll
+        for (int jj = 1; jj < KF; ++jj) fj = jj == j ? f[jj] : fj;
+        H[s * 32] = fmaf(g, fj, H[s * 32]);
+        const float vs = Vp[s * 32];
+#pragma unroll
+        for (int jj = 0; jj < KF; ++jj) dS[jj] = jj == j ? fmaf(g, vs, dS[jj]) : dS[jj];
+      }
     }
     if (bval) {
 #pragma unroll

@@ -127,7 +127,7 @@ class DampApply(torch.autograd.Function):
         inputs = ctx.saved_tensors
         kplan: KernelPlan = ctx.kplan
         B = ctx.B
-        if kplan.conv == 1:  # the short-filter Toeplitz backward reads contiguous rows
+        if kplan.conv == 1 and not conv_staged(kplan):  # the unstaged kernel reads contiguous rows
             g = g.contiguous()
         dev = g.device
         need = [i for i in range(len(inputs)) if ctx.needs_input_grad[2 + i]]
@@ -152,6 +152,17 @@ class DampApply(torch.autograd.Function):
         return (None, None, *grads)
 
 
+def conv_staged(kplan: KernelPlan) -> bool:
+    """Whether the short-filter Toeplitz backward reads the upstream gradient in place."""
+    sh = kplan.conv_short
+    return _conv_staged(kplan.sizes[sh], kplan.sizes[1 - sh], kplan.n_out)
+
+
+@functools.lru_cache(maxsize=4096)
+def _conv_staged(kf: int, n_long: int, n_out: int) -> bool:
+    return bool(_lib().sg_damp_conv_staged(kf, n_long, n_out))
+
+
 class MaxProdApply(torch.autograd.Function):
     """Max-product apply (the north star's max variant): per output the max over its
     records of the product of the inputs, gradient to the first maximal record
@@ -168,6 +179,8 @@ class MaxProdApply(torch.autograd.Function):
         rc = _lib().sg_maxprod_fwd(ctypes.byref(s), N.rows_array(inputs), B, int(kplan.clamp), N.ptr(out),
                                    N.ptr(arg), N.stream_ptr(dev))
         N.check(rc, "sg_maxprod_fwd")
+        _ledger("maxprod_fwd", 4 * B * (sum(kplan.sizes) + 2 * kplan.n_out) + 4 * kplan.n_rec * (kplan.arity + 1),
+                B * kplan.n_rec)
         ctx.kplan = kplan
         ctx.B = B
         ctx.save_for_backward(arg, *inputs)
@@ -185,6 +198,8 @@ class MaxProdApply(torch.autograd.Function):
             rc = _lib().sg_maxprod_bwd(ctypes.byref(s), N.rows_array(inputs), ctx.B, N.ptr(arg), N.rows(g),
                                        N.rows_array(grads), N.stream_ptr(dev))
             N.check(rc, "sg_maxprod_bwd")
+            _ledger("maxprod_bwd", 4 * ctx.B * (2 * kplan.n_out + sum(2 * n for n in kplan.sizes))
+                    + 4 * kplan.n_rec * (kplan.arity + 2), ctx.B * kplan.n_rec)
         return (None, None, *grads)
 
 

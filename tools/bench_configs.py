@@ -146,6 +146,24 @@ def roofline(alg_bytes, by_kernel, ms, hbm, peak_src):
                       "step time with L2 flushed"}
 
 
+def issue_ceiling(prefix):
+    """The DTKP kernels' issue-ceiling fractions from the committed ncu --set full captures
+    (profiles/issue.json, tools/ncu_issue.py): the apply is instruction-issue bound
+    (SURVEY 8(d)), so its roofline is the SM issue rate, 4 warp-instructions/cycle/SM."""
+    try:
+        d = json.loads((ROOT / "profiles" / "issue.json").read_text())
+    except (OSError, ValueError):
+        return None
+    ent = {k: v for k, v in d.items() if k.startswith(prefix)}
+    if not ent:
+        return None
+    top = max(ent.values(), key=lambda v: v["duration_us"])
+    return {"bound": "issue", "kernel": top["kernel"], "frac": top["issue_active_frac"],
+            "ipc_per_sm": top["ipc_per_sm"], "peak_ipc_per_sm": top["ipc_peak"],
+            "fp64_pipe_frac": top["fp64_pipe_frac"], "source": "profiles/issue.json (ncu --set full)",
+            "kernels": ent}
+
+
 def rows(rng, B, n):
     r = rng.uniform(0.05, 1.0, size=(B, n))
     return (r / r.sum(axis=1, keepdims=True)).astype(np.float32)
@@ -248,7 +266,7 @@ def hwf7(dev, iters=20, cpu=True, B=64):
                    "d2h_bytes_per_step": 8, "api": "eager programs.hwf (memoised plans) + loss_nll + autograd.grad, "
                                                    "inputs H2D + loss.item() per step"},
            "first_call_s_incl_host_plans": first,
-           "roofline": roofline(alg, by, ms, hbm, src)}
+           "roofline": roofline(alg, by, ms, hbm, src), "issue_ceiling": issue_ceiling("hwf7_")}
     if cpu:
         res["cpu"] = cpu_reference("hwf7", B, steps=1, warmup=0)
     return res
@@ -295,7 +313,7 @@ def clutrr(dev, iters=20, cpu=True, B=4096, n_entities=5, k=5):
            "e2e": {"ms_per_step": e2e_ms, "value": B / (e2e_ms * 1e-3), "h2d_bytes_per_step": pin_x.numel() * 4 + B * 8,
                    "d2h_bytes_per_step": 8, "api": "eager clutrr_closure (fixpoint.closure) + loss_nll + autograd.grad,"
                                                    " inputs H2D + loss.item() per step"},
-           "roofline": roofline(alg, by, ms, hbm, src)}
+           "roofline": roofline(alg, by, ms, hbm, src), "issue_ceiling": issue_ceiling("clutrr_")}
     if cpu:
         res["cpu"] = cpu_reference("clutrr", B, steps=1, warmup=0)
     return res
