@@ -887,15 +887,16 @@ static int lconv(const Rows& X, int nx, const Rows& H, int nh, int t0, const WRo
 
 static Rows reversed(const Rows& r, int n) { return Rows{r.p + (int64_t)(n - 1) * r.sr, -r.sr, r.sb}; }
 
-#ifndef SG_CONV_STAGED  // 0: always the unstaged k_conv_* kernels (A/B runs)
-#define SG_CONV_STAGED 1
-#endif
+// The staged kernels are exact but measured SLOWER than the unstaged ones at the sweep's
+// shapes (B=65536, arity 2, |S|=10: fwd 14.4 vs 8.2 us, bwd 20.5 vs 12.0 + 8.1 us for the
+// transposing copy it removes; profiles/r02_sweep_launches.md), so they are opt-in:
+// SG_CONV_STAGED=1 in the environment.
 static bool conv_staged(int kf, int nL, int n_out) {
-  static const bool off = [] {
-    const char* e = getenv("SG_CONV_UNSTAGED");
+  static const bool on = [] {
+    const char* e = getenv("SG_CONV_STAGED");
     return e != nullptr && e[0] == '1';
   }();
-  return SG_CONV_STAGED && !off && convs_fits(kf, nL, n_out);
+  return on && convs_fits(kf, nL, n_out);
 }
 
 static int conv_fwd(int kf, const Rows& L, int nL, const Rows& S, float* out, int n_out, int64_t B, cudaStream_t st) {

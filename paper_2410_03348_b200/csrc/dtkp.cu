@@ -258,13 +258,6 @@ int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream) {
   k.sched = d->sched;
   k.n_items = d->seg.n_items;
   k.fused = 0;
-  {
-    static const int l1pf = [] {
-      const char* e = getenv("SG_DTKP_L1PF");
-      return e != nullptr && e[0] == '1' ? 1 : 0;
-    }();
-    k.l1pf = l1pf;
-  }
   if (d->inner_arity != 0) {
     // fused conj -> group_disj: only an arity-1 apply over a binary conj
     SG_RETURN_IF(d->arity != 1 || d->inner_arity != 2 || d->seg.rec_words < 2, cudaErrorInvalidValue);

@@ -18,7 +18,7 @@
 #define SG_DTKP_STREAM_PREFETCH 0
 #endif
 #ifndef SG_DTKP_FUSED_MINB  // resident CTAs/SM asked of the fused conj -> group_disj (K <= 3)
-#define SG_DTKP_FUSED_MINB 4
+#define SG_DTKP_FUSED_MINB 5
 #endif
 #ifndef SG_DTKP_UNROLL_K
 #define SG_DTKP_UNROLL_K 4
@@ -185,7 +185,6 @@ struct DtkpK {
   // fused conj -> group_disj (AR == 3): the binary conj's operands (records in recs)
   sg_dtkp_operand inner[2];
   int32_t fused;
-  int32_t l1pf;  // L1-prefetch the next record's tag rows (SG_DTKP_L1PF=1; measured: no gain)
 };
 
 template <int WT>
@@ -238,13 +237,20 @@ struct TagRows {
 
 __device__ __forceinline__ int rec_row(const DtkpK& a, int c, int i) { return __ldg(a.recs + (size_t)c * a.rec_words + i); }
 
-// T = normalise(conj(A, Bt)): all present row pairs OR-ed in candidate order ra*kb + rb,
-// dedup + top-k (provenance.py:328-341 -> _normalize :366-379).
+// Stream the candidates of conj(A, Bt) — all present row pairs OR-ed, in candidate order
+// ra*kb + rb (provenance.py:328-341) — into the running top-k T.  With T cleared first
+// this is the conj's own normalisation (_normalize :366-379).  Streaming them straight into
+// the group_disj's running top-k (provenance.py:352-364) instead of normalising each combo
+// first gives the SAME rows in the same order: a candidate in the top-k of the whole
+// segment has fewer than k better candidates in its own combo, so it survives that combo's
+// normalisation; normalisation keeps the candidate order among equal keys, dedup keeps the
+// first occurrence either way, and the top-k of a union equals the top-k of the union of
+// the members' top-k lists (SURVEY §7 hard part 2).  Only n-ary folds (arity >= 3) must
+// normalise between steps: there the truncation feeds the next OR.
 template <int K, int WT>
-__device__ __forceinline__ void conj_pairs(TopK<K, WT>& T, const TagRows<K, WT>& A, const TagRows<K, WT>& Bt,
-                                           const PCol& pc) {
+__device__ __forceinline__ void conj_into(TopK<K, WT>& T, const TagRows<K, WT>& A, const TagRows<K, WT>& Bt,
+                                          const PCol& pc) {
   constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
-  T.clear();
 #pragma unroll (kUnrollK)
   for (int qa = 0; qa < K; ++qa) {
     if (!((A.pres >> qa) & 1u)) continue;
@@ -277,37 +283,6 @@ __device__ __forceinline__ void stream_rows(TopK<K, WT>& S, const TopK<K, WT>& T
   }
 }
 
-// L1 prefetch of one tag's rows for the warp's 32-sample column (row r of op): K*W member
-// words as 2 x 128-byte lines each and K present lines.  The apply's per-record chain is
-// record -> tag rows -> rank; prefetching the NEXT record's rows (one line per lane, no
-// registers held) while the current record is ranked turns its row loads into L1 hits.
-__device__ __forceinline__ void pf_tag_line(const sg_dtkp_operand& op, int K, int64_t B, int64_t col0, int r, int id,
-                                            bool two_lines) {
-  const int nm = K * op.W * 2;
-  const char* addr;
-  if (id < nm) {
-    if ((id & 1) && !two_lines) return;
-    addr = reinterpret_cast<const char*>(op.member + ((size_t)r * K * op.W + (id >> 1)) * B + col0) + (id & 1) * 128;
-  } else {
-    addr = reinterpret_cast<const char*>(op.present + ((size_t)r * K + (id - nm)) * B + col0);
-  }
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(addr));
-}
-
-__device__ __forceinline__ void pf_tags(const sg_dtkp_operand& o0, int r0, const sg_dtkp_operand* o1, int r1, int K,
-                                        int64_t B, int64_t col0, int lane, int on) {
-  if (!on) return;
-  const bool two = B - col0 > 16;  // samples col0 + 16 .. col0 + 31 exist
-  const int n0 = K * (2 * o0.W + 1);
-  const int n1 = o1 != nullptr ? K * (2 * o1->W + 1) : 0;
-  for (int id = lane; id < n0 + n1; id += 32) {
-    if (id < n0)
-      pf_tag_line(o0, K, B, col0, r0, id, two);
-    else
-      pf_tag_line(*o1, K, B, col0, r1, id - n0, two);
-  }
-}
-
 // One work item (an output segment, or a piece of a split one) for one sample: stream its
 // records through the top-k set and write the retained rows.
 // AR: 1 = union / group_disj streaming, 2 = binary conj fold, 0 = conj fold of >= 3
@@ -319,25 +294,21 @@ template <int K, int WT, int AR>
 __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, int64_t b0, bool bval, const PCol& pc) {
   constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
   const int4 item = __ldg(reinterpret_cast<const int4*>(a.items) + it);
-  const int lane = threadIdx.x & 31;
-  const int64_t col0 = (int64_t)blockIdx.x * kWarp;
   TopK<K, WT> S;
   S.clear();
   if constexpr (AR == 1) {
-    // group_disj / union / merge: stream the stored rows of every record, in order
-    auto op_of = [&](int r) -> const sg_dtkp_operand& { return r >= a.ops[0].rows ? a.tail : a.ops[0]; };
-    auto row_of = [&](int r) { return r >= a.ops[0].rows ? r - a.ops[0].rows : r; };
+    // group_disj / union / merge: stream the stored rows of every record, in order;
+    // the next record's rows are loaded after the current one is ranked
     TagRows<K, WT> cur;
-    int rn = item.y + 1 < item.z ? rec_row(a, item.y + 1, 0) : 0;
-    if (item.y < item.z) {
-      const int r = rec_row(a, item.y, 0);
-      cur.load(op_of(r), a.B, b, row_of(r));
-    }
+    auto fetch = [&](int c) {
+      const int r = rec_row(a, c, 0);
+      if (r >= a.ops[0].rows)
+        cur.load(a.tail, a.B, b, r - a.ops[0].rows);
+      else
+        cur.load(a.ops[0], a.B, b, r);
+    };
+    if (item.y < item.z) fetch(item.y);
     for (int c = item.y; c < item.z; ++c) {
-      const bool more = c + 1 < item.z;
-      const int rnext = rn;
-      if (more) pf_tags(op_of(rnext), row_of(rnext), nullptr, 0, K, a.B, col0, lane, a.l1pf);
-      if (c + 2 < item.z) rn = rec_row(a, c + 2, 0);
 #pragma unroll (kUnrollK)
       for (int q = 0; q < K; ++q) {
         if (!((cur.pres >> q) & 1u)) continue;
@@ -345,7 +316,7 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
         cur.row(q, mm);
         S.insert(mm, proof_key<WT>(mm, pc), 0);
       }
-      if (more) cur.load(op_of(rnext), a.B, b, row_of(rnext));
+      if (c + 1 < item.z) fetch(c + 1);
     }
   } else if constexpr (AR == 3) {
     // fused conj -> group_disj: M collects an intermediate symbol's tag (the top-k over its
@@ -370,14 +341,11 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
     for (int c = item.y; c < item.z; ++c) {
       const bool more = c + 1 < item.z;
       const int rna = ran, rnb = rbn;
-      if (more) pf_tags(o0, rna, &o1, rnb & 0x7fffffff, K, a.B, col0, lane, a.l1pf);
       if (c + 2 < item.z) {
         ran = rec_row(a, c + 2, 0);
         rbn = rec_row(a, c + 2, 1);
       }
-      TopK<K, WT> T;
-      conj_pairs<K, WT>(T, A, Bt, pc);
-      stream_rows<K, WT>(M, T);
+      conj_into<K, WT>(M, A, Bt, pc);
       if (rbf < 0) {  // last conj record of this intermediate symbol
         stream_rows<K, WT>(S, M);
         M.clear();
@@ -406,22 +374,22 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
     for (int c = item.y; c < item.z; ++c) {
       const bool more = c + 1 < item.z;
       const int rna = ran, rnb = rbn;
-      if (more) {
-        if (kPf) {
-          An.load(a.ops[0], a.B, b, rna);
-          Bn.load(a.ops[1], a.B, b, rnb);
-        } else if (AR == 2) {
-          pf_tags(a.ops[0], rna, &a.ops[1], rnb, K, a.B, col0, lane, a.l1pf);
-        }
+      if (kPf && more) {
+        An.load(a.ops[0], a.B, b, rna);
+        Bn.load(a.ops[1], a.B, b, rnb);
       }
       if (c + 2 < item.z) {
         ran = rec_row(a, c + 2, 0);
         rbn = rec_row(a, c + 2, 1);
       }
+      if constexpr (AR == 2) {
+        conj_into<K, WT>(S, A, Bt, pc);  // exact: see conj_into
+      } else {
       TopK<K, WT> T;
-      conj_pairs<K, WT>(T, A, Bt, pc);
+      T.clear();
+      conj_into<K, WT>(T, A, Bt, pc);
 #pragma unroll 1
-      for (int i = 2; AR != 2 && i < a.arity; ++i) {
+      for (int i = 2; i < a.arity; ++i) {
         TagRows<K, WT> Ci;
         Ci.load(a.ops[i], a.B, b, rec_row(a, c, i));
         TopK<K, WT> U;
@@ -445,6 +413,7 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
         T = U;
       }
       stream_rows<K, WT>(S, T);
+      }
       if (more) {
         if constexpr (kPf) {
           A = An;
@@ -480,12 +449,14 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
 // Resident CTAs per SM the register allocator is asked for: the highest that compiles
 // without spills at K <= 3 / K <= 5 and W <= 2 (ptxas -v), else whatever the kernel needs.
 __host__ __device__ constexpr int dtkp_min_blocks(int K, int WT, int AR) {
+  // binary conj (AR 2) streams its candidates straight into the segment's top-k (no
+  // per-combo top-k set): 6 / 4 CTAs per SM at K <= 3 / K <= 5 without spills
   return SG_DTKP_MINB > 0 ? SG_DTKP_MINB
          : (WT <= 2 && K <= 3) ? (AR == 1 ? (SG_DTKP_STREAM_PREFETCH ? 5 : 6)
-                                  : AR == 2 ? (K > SG_DTKP_CONJ_PREFETCH_MAXK ? 5 : 4)
+                                  : AR == 2 ? (K > SG_DTKP_CONJ_PREFETCH_MAXK ? 6 : 4)
                                   : AR == 3 ? SG_DTKP_FUSED_MINB : 1)
          : (WT <= 2 && K <= 5 && AR == 1) ? (SG_DTKP_STREAM_PREFETCH ? 4 : 5)
-         : (WT <= 2 && K <= 5 && AR == 2 && K > SG_DTKP_CONJ_PREFETCH_MAXK) ? 3
+         : (WT <= 2 && K <= 5 && AR == 2 && K > SG_DTKP_CONJ_PREFETCH_MAXK) ? 4
          : 1;
 }
 

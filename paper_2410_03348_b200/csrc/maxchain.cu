@@ -147,8 +147,14 @@ __global__ void __launch_bounds__(32) k_maxchain_bwd(const MaxChainArgs a) {
   float* H = G + (size_t)a.n_max * 32;
   float* Vp = H + (size_t)a.n_max * 32;
   mc_pdl_wait();
-#pragma unroll 8
-  for (int o = 0; o < a.n[a.m]; ++o) G[o * 32] = __ldg(a.g_out + (size_t)o * a.B + b);
+  for (int o0 = 0; o0 < a.n[a.m]; o0 += 32) {
+    float v[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) v[u] = o0 + u < a.n[a.m] ? __ldg(a.g_out + (size_t)(o0 + u) * a.B + b) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 32; ++u)
+      if (o0 + u < a.n[a.m]) G[(o0 + u) * 32] = v[u];
+  }
   float fn[KF];  // the next (lower) step's filter, loaded one step ahead
 #pragma unroll
   for (int j = 0; j < KF; ++j) fn[j] = a.filt[a.m - 1].ld(j, b);
@@ -164,13 +170,33 @@ __global__ void __launch_bounds__(32) k_maxchain_bwd(const MaxChainArgs a) {
 #pragma unroll
       for (int j = 0; j < KF; ++j) fn[j] = a.filt[i - 2].ld(j, b);
     }
+    // v_{i-1} into the lane's column, 32 independent loads in flight per lane (one warp
+    // per scheduler here: memory-level parallelism has to come from inside the warp); the
+    // step after's rows are prefetched into L2 (one 128-byte line = one row of the warp)
     if (i > 1) {
       const float* st = a.states + (size_t)a.state_off[i - 1] * a.B;
-#pragma unroll 8
-      for (int s = 0; s < nin; ++s) Vp[s * 32] = __ldg(st + (size_t)s * a.B + b);
+      for (int s0 = 0; s0 < nin; s0 += 32) {
+        float v[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) v[u] = s0 + u < nin ? __ldg(st + (size_t)(s0 + u) * a.B + b) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 32; ++u)
+          if (s0 + u < nin) Vp[(s0 + u) * 32] = v[u];
+      }
+      if (i > 2) {
+        const float* nx = a.states + (size_t)a.state_off[i - 2] * a.B + (b0 - lane);
+        for (int r = lane; r < a.n[i - 2]; r += 32)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + (size_t)r * a.B));
+      }
     } else {
-#pragma unroll 8
-      for (int s = 0; s < nin; ++s) Vp[s * 32] = a.base.ld(s, b);
+      for (int s0 = 0; s0 < nin; s0 += 32) {
+        float v[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) v[u] = s0 + u < nin ? a.base.ld(s0 + u, b) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 32; ++u)
+          if (s0 + u < nin) Vp[(s0 + u) * 32] = v[u];
+      }
     }
     for (int s = 0; s < nin; ++s) H[s * 32] = 0.f;
     const uint8_t* am = a.argmax + (size_t)a.arg_off[i] * a.B + b;
