@@ -258,7 +258,10 @@ typedef struct sg_dtkp_apply_desc {
    * apply's top-k in rank order — bit-identical to the two launches, while the intermediate
    * tag never touches HBM.  ops[0] and op_tail are not read.                            */
   int32_t inner_arity;
-  int32_t inner_pad_;
+  /* seg_packed != 0: seg's items (.x = first segment, .w = -1) may hold runs of WHOLE
+   * segments; word 0 of a segment's last record carries bit 31 (rows are < 2^31).  Items
+   * with .w >= 0 are pieces of one split segment, as always.  The merges are never packed. */
+  int32_t seg_packed;
   sg_dtkp_operand inner_ops[2];
 } sg_dtkp_apply_desc;
 

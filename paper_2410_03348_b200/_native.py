@@ -102,7 +102,7 @@ class SgDtkpApplyDesc(Structure):
         ("scratch2_member", c_void_p),
         ("scratch2_present", c_void_p),
         ("inner_arity", c_int32),
-        ("inner_pad_", c_int32),
+        ("seg_packed", c_int32),
         ("inner_ops", SgDtkpOperand * 2),
     ]
 

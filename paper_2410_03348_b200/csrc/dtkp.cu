@@ -258,6 +258,7 @@ int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream) {
   k.sched = d->sched;
   k.n_items = d->seg.n_items;
   k.fused = 0;
+  k.packed = d->seg_packed;
   if (d->inner_arity != 0) {
     // fused conj -> group_disj: only an arity-1 apply over a binary conj
     SG_RETURN_IF(d->arity != 1 || d->inner_arity != 2 || d->seg.rec_words < 2, cudaErrorInvalidValue);
@@ -273,6 +274,7 @@ int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream) {
     DtkpK m = k;
     m.arity = 1;
     m.fused = 0;  // merges read the materialised partial lists
+    m.packed = 0;
     m.ops[0].member = d->scratch_member;
     m.ops[0].present = d->scratch_present;
     m.ops[0].rows = d->seg.n_partial;

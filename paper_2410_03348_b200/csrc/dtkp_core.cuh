@@ -185,6 +185,7 @@ struct DtkpK {
   // fused conj -> group_disj (AR == 3): the binary conj's operands (records in recs)
   sg_dtkp_operand inner[2];
   int32_t fused;
+  int32_t packed;  // items may hold runs of whole segments (record word 0 bit 31 = segment end)
 };
 
 template <int WT>
@@ -283,8 +284,32 @@ __device__ __forceinline__ void stream_rows(TopK<K, WT>& S, const TopK<K, WT>& T
   }
 }
 
-// One work item (an output segment, or a piece of a split one) for one sample: stream its
-// records through the top-k set and write the retained rows.
+// Write the retained rows of S as tag row `row` of (om, opr) for this lane's sample.
+template <int K, int WT>
+__device__ __forceinline__ void emit_rows(const DtkpK& a, const TopK<K, WT>& S, uint64_t* om_base, uint8_t* op_base,
+                                          int row, int64_t b0) {
+  uint64_t* om = om_base + (size_t)row * K * a.W * a.B;
+  uint8_t* opr = op_base + (size_t)row * K * a.B;
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    const bool live = q < S.n;
+    opr[(size_t)q * a.B + b0] = live ? 1 : 0;
+#pragma unroll
+    for (int w = 0; w < WT; ++w)
+      if (w < a.W) om[((size_t)q * a.W + w) * a.B + b0] = live ? S.m[q][w] : 0ull;
+  }
+}
+
+constexpr int kRowMask = 0x7fffffff;  // record word 0 bit 31: last record of a segment (packed items)
+
+// One work item for one sample: stream its records through the top-k set and write the
+// retained rows.  An item is a piece of one (long, split) segment written to scratch
+// (item.w >= 0), one whole segment (item.w < 0), or — in a packed problem (a.packed) —
+// a run of WHOLE short segments starting at segment item.x: each record whose word 0
+// carries bit 31 closes the current segment (its rows are written, the set is cleared and
+// the next segment begins).  Packing turns e.g. HWF-7 step 7 (208,767 segments of ~1.5
+// records) into items of ~48 records, so the per-item chain (work counter atomic ->
+// item -> records) is paid once per 30 segments instead of once per segment.
 // AR: 1 = union / group_disj streaming, 2 = binary conj fold, 0 = conj fold of >= 3
 // operands, 3 = the fused conj -> group_disj (sg_dtkp_apply_desc.inner_arity): records are
 // binary-conj records (rows of inner[0], inner[1]) grouped by intermediate symbol, the last
@@ -294,21 +319,32 @@ template <int K, int WT, int AR>
 __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, int64_t b0, bool bval, const PCol& pc) {
   constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
   const int4 item = __ldg(reinterpret_cast<const int4*>(a.items) + it);
+  const bool multi = a.packed && item.w < 0;  // segments close at flagged records
+  int seg = item.x;
   TopK<K, WT> S;
   S.clear();
+  auto close_seg = [&](int word0) {
+    if (multi && word0 < 0) {
+      if (bval) emit_rows<K, WT>(a, S, a.out_m, a.out_p, seg, b0);
+      S.clear();
+      ++seg;
+    }
+  };
   if constexpr (AR == 1) {
     // group_disj / union / merge: stream the stored rows of every record, in order;
     // the next record's rows are loaded after the current one is ranked
     TagRows<K, WT> cur;
-    auto fetch = [&](int c) {
-      const int r = rec_row(a, c, 0);
+    auto fetch = [&](int r) {
+      r &= kRowMask;
       if (r >= a.ops[0].rows)
         cur.load(a.tail, a.B, b, r - a.ops[0].rows);
       else
         cur.load(a.ops[0], a.B, b, r);
     };
-    if (item.y < item.z) fetch(item.y);
+    int w0 = item.y < item.z ? rec_row(a, item.y, 0) : 0;
+    if (item.y < item.z) fetch(w0);
     for (int c = item.y; c < item.z; ++c) {
+      const int wn = c + 1 < item.z ? rec_row(a, c + 1, 0) : 0;
 #pragma unroll (kUnrollK)
       for (int q = 0; q < K; ++q) {
         if (!((cur.pres >> q) & 1u)) continue;
@@ -316,7 +352,9 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
         cur.row(q, mm);
         S.insert(mm, proof_key<WT>(mm, pc), 0);
       }
-      if (c + 1 < item.z) fetch(c + 1);
+      close_seg(w0);
+      if (c + 1 < item.z) fetch(wn);
+      w0 = wn;
     }
   } else if constexpr (AR == 3) {
     // fused conj -> group_disj: M collects an intermediate symbol's tag (the top-k over its
@@ -329,8 +367,8 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
     if (item.y < item.z) {
       ra = rec_row(a, item.y, 0);
       rbf = rec_row(a, item.y, 1);
-      A.load(o0, a.B, b, ra);
-      Bt.load(o1, a.B, b, rbf & 0x7fffffff);
+      A.load(o0, a.B, b, ra & kRowMask);
+      Bt.load(o1, a.B, b, rbf & kRowMask);
     }
     if (item.y + 1 < item.z) {
       ran = rec_row(a, item.y + 1, 0);
@@ -350,18 +388,21 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
         stream_rows<K, WT>(S, M);
         M.clear();
       }
+      close_seg(ra);
       if (more) {
+        ra = rna;
         rbf = rnb;
-        A.load(o0, a.B, b, rna);
-        Bt.load(o1, a.B, b, rnb & 0x7fffffff);
+        A.load(o0, a.B, b, rna & kRowMask);
+        Bt.load(o1, a.B, b, rnb & kRowMask);
       }
     }
   } else {
     // conj fold, normalised after every step (candidate order ra*kb + rb)
     TagRows<K, WT> A, Bt, An, Bn;
-    int ran = 0, rbn = 0;
+    int wa = 0, ran = 0, rbn = 0;
     if (item.y < item.z) {
-      A.load(a.ops[0], a.B, b, rec_row(a, item.y, 0));
+      wa = rec_row(a, item.y, 0);
+      A.load(a.ops[0], a.B, b, wa & kRowMask);
       Bt.load(a.ops[1], a.B, b, rec_row(a, item.y, 1));
     }
     if (item.y + 1 < item.z) {
@@ -369,13 +410,13 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
       rbn = rec_row(a, item.y + 1, 1);
     }
     // next record's rows held in registers only while K is small (their registers cost
-    // occupancy); otherwise L1-prefetched and loaded after the current record
+    // occupancy); otherwise loaded after the current record
     constexpr bool kPf = K <= SG_DTKP_CONJ_PREFETCH_MAXK;
     for (int c = item.y; c < item.z; ++c) {
       const bool more = c + 1 < item.z;
       const int rna = ran, rnb = rbn;
       if (kPf && more) {
-        An.load(a.ops[0], a.B, b, rna);
+        An.load(a.ops[0], a.B, b, rna & kRowMask);
         Bn.load(a.ops[1], a.B, b, rnb);
       }
       if (c + 2 < item.z) {
@@ -385,64 +426,53 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
       if constexpr (AR == 2) {
         conj_into<K, WT>(S, A, Bt, pc);  // exact: see conj_into
       } else {
-      TopK<K, WT> T;
-      T.clear();
-      conj_into<K, WT>(T, A, Bt, pc);
+        TopK<K, WT> T;
+        T.clear();
+        conj_into<K, WT>(T, A, Bt, pc);
 #pragma unroll 1
-      for (int i = 2; i < a.arity; ++i) {
-        TagRows<K, WT> Ci;
-        Ci.load(a.ops[i], a.B, b, rec_row(a, c, i));
-        TopK<K, WT> U;
-        U.clear();
+        for (int i = 2; i < a.arity; ++i) {
+          TagRows<K, WT> Ci;
+          Ci.load(a.ops[i], a.B, b, rec_row(a, c, i));
+          TopK<K, WT> U;
+          U.clear();
 #pragma unroll (kUnrollK)
-        for (int qa = 0; qa < K; ++qa) {
-          if (qa >= T.n) break;
-          uint64_t ma[WT];
-          double ka;
-          T.get(qa, ma, ka);
+          for (int qa = 0; qa < K; ++qa) {
+            if (qa >= T.n) break;
+            uint64_t ma[WT];
+            double ka;
+            T.get(qa, ma, ka);
 #pragma unroll (kUnrollK)
-          for (int qb = 0; qb < K; ++qb) {
-            if (!((Ci.pres >> qb) & 1u)) continue;
-            uint64_t mm[WT];
-            Ci.row(qb, mm);
+            for (int qb = 0; qb < K; ++qb) {
+              if (!((Ci.pres >> qb) & 1u)) continue;
+              uint64_t mm[WT];
+              Ci.row(qb, mm);
 #pragma unroll
-            for (int w = 0; w < WT; ++w) mm[w] |= ma[w];
-            U.insert(mm, proof_key<WT>(mm, pc), 0);
+              for (int w = 0; w < WT; ++w) mm[w] |= ma[w];
+              U.insert(mm, proof_key<WT>(mm, pc), 0);
+            }
           }
+          T = U;
         }
-        T = U;
+        stream_rows<K, WT>(S, T);
       }
-      stream_rows<K, WT>(S, T);
-      }
+      close_seg(wa);
       if (more) {
+        wa = rna;
         if constexpr (kPf) {
           A = An;
           Bt = Bn;
         } else {
-          A.load(a.ops[0], a.B, b, rna);
+          A.load(a.ops[0], a.B, b, rna & kRowMask);
           Bt.load(a.ops[1], a.B, b, rnb);
         }
       }
     }
   }
-  if (bval) {
-    uint64_t* om;
-    uint8_t* opr;
-    if (item.w < 0) {
-      om = a.out_m + (size_t)item.x * K * a.W * a.B;
-      opr = a.out_p + (size_t)item.x * K * a.B;
-    } else {
-      om = a.scr_m + (size_t)item.w * K * a.W * a.B;
-      opr = a.scr_p + (size_t)item.w * K * a.B;
-    }
-#pragma unroll
-    for (int q = 0; q < K; ++q) {
-      const bool live = q < S.n;
-      opr[(size_t)q * a.B + b0] = live ? 1 : 0;
-#pragma unroll
-      for (int w = 0; w < WT; ++w)
-        if (w < a.W) om[((size_t)q * a.W + w) * a.B + b0] = live ? S.m[q][w] : 0ull;
-    }
+  if (bval && (!multi || item.y == item.z)) {  // (a packed item without records = one empty segment)
+    if (item.w < 0)
+      emit_rows<K, WT>(a, S, a.out_m, a.out_p, item.x, b0);
+    else
+      emit_rows<K, WT>(a, S, a.scr_m, a.scr_p, item.w, b0);
   }
 }
 

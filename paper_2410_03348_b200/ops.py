@@ -597,6 +597,7 @@ def dtkp_apply(kplan_host, dseg, dmerge, operands, tail, K: int, W: int, I: int,
         d.ops[0].W = W
     d.p = p.data_ptr() if p.numel() else None
     d.seg = dseg.struct(B)
+    d.seg_packed = 1 if getattr(dseg.host, "packed", False) else 0
     d.out_member = out_m.data_ptr() if out_m.numel() else None
     d.out_present = out_p.data_ptr() if out_p.numel() else None
     scr_m = scr_p = None

@@ -17,6 +17,8 @@ with T[s0][s1] == s0 + s1.
 
 from __future__ import annotations
 
+import os
+
 import itertools
 from collections import OrderedDict
 
@@ -332,10 +334,10 @@ def _rec_words(n_ops: int) -> int:
 class HostSegsum:
     """One segmented problem: records grouped into segments, cut into bounded items."""
 
-    __slots__ = ("n_seg", "rec_words", "recs", "items", "split", "n_partial", "work", "seg_off")
+    __slots__ = ("n_seg", "rec_words", "recs", "items", "split", "n_partial", "work", "seg_off", "packed")
 
     def __init__(self, seg_off: np.ndarray, recs: np.ndarray, max_item: int, cut_points: np.ndarray | None = None,
-                 cut_seg: np.ndarray | None = None):
+                 cut_seg: np.ndarray | None = None, pack: bool = False):
         """Items hold at most ``max_item`` records.  With ``cut_points`` (record offsets of
         groups that must stay whole — one intermediate symbol's conj records in a fused
         conj -> group_disj — and ``cut_seg``, the segment of each group) items are made of
@@ -348,7 +350,15 @@ class HostSegsum:
         packed = np.zeros((nrec, rw), dtype=np.int32)
         packed[:, :nops] = recs.reshape(nrec, nops)
         lens = np.diff(seg_off)
-        if cut_points is None:
+        self.packed = bool(pack)
+        if pack:
+            # runs of whole short segments per item; word 0 of every segment's last record
+            # carries bit 31 (sg_dtkp_apply_desc.seg_packed); long segments are split as usual
+            seg_of, rb, re, pieces = self._pack(seg_off, lens, int(max_item))
+            n_items = len(seg_of)
+            nz = np.nonzero(lens > 0)[0]
+            packed[seg_off[nz + 1] - 1, 0] |= np.int32(-2**31)
+        elif cut_points is None:
             pieces = np.maximum(1, -(-lens // max_item))
             n_items = int(pieces.sum())
             seg_of = np.repeat(np.arange(n_seg, dtype=np.int64), pieces)
@@ -384,6 +394,38 @@ class HostSegsum:
         self.n_partial = n_partial
         self.work = (re - rb) + 2  # records + per-item overhead
         self.seg_off = seg_off
+
+    @staticmethod
+    def _pack(seg_off, lens, max_item):
+        """(first segment, begin, end, pieces-per-segment) of packed items: whole segments
+        of at most max_item records gathered while they fit, longer ones split."""
+        seg_of, rb, re = [], [], []
+        pieces = np.ones(len(lens), dtype=np.int64)
+        cur_s, cur_b, cur_n = -1, 0, 0
+        for sgi, ln in enumerate(lens.tolist()):
+            a = int(seg_off[sgi])
+            if ln > max_item or ln == 0:
+                if cur_s >= 0:
+                    seg_of.append(cur_s), rb.append(cur_b), re.append(cur_b + cur_n)
+                    cur_s = -1
+                if ln == 0:
+                    seg_of.append(sgi), rb.append(a), re.append(a)
+                    continue
+                k = -(-ln // max_item)
+                pieces[sgi] = k
+                for p in range(k):
+                    seg_of.append(sgi), rb.append(a + p * max_item), re.append(min(a + (p + 1) * max_item, a + ln))
+                continue
+            if cur_s >= 0 and cur_n + ln > max_item:
+                seg_of.append(cur_s), rb.append(cur_b), re.append(cur_b + cur_n)
+                cur_s = -1
+            if cur_s < 0:
+                cur_s, cur_b, cur_n = sgi, a, 0
+            cur_n += ln
+        if cur_s >= 0:
+            seg_of.append(cur_s), rb.append(cur_b), re.append(cur_b + cur_n)
+        return (np.asarray(seg_of, dtype=np.int64), np.asarray(rb, dtype=np.int64), np.asarray(re, dtype=np.int64),
+                pieces)
 
     @staticmethod
     def _group_pieces(gseg_off, gsize, max_w):
@@ -470,6 +512,7 @@ def csr(keys: np.ndarray, n_seg: int):
 
 DAMP_MAX_ITEM = 128
 DTKP_MAX_ITEM = 48
+DTKP_PACK = os.environ.get("SG_DTKP_PACK", "1") != "0"  # runs of short segments per item
 DTKP_FUSED_ITEM = 48  # inner conj records (+1 per intermediate symbol) per fused item
 DTKP_MERGE_ITEM = 8  # partial lists per first-level merge item (two-level merge)
 STAGE_BYTES = 200 * 1024
@@ -541,7 +584,7 @@ class KernelPlan:
     def dtkp_host(self) -> HostSegsum:
         if self._dtkp_host is None:
             order, off = csr(self.out_idx, self.n_out)
-            self._dtkp_host = HostSegsum(off, self.records[order], DTKP_MAX_ITEM)
+            self._dtkp_host = HostSegsum(off, self.records[order], DTKP_MAX_ITEM, pack=DTKP_PACK)
         return self._dtkp_host
 
     def dtkp_fused_host(self, inner: "KernelPlan") -> HostSegsum:
@@ -558,7 +601,7 @@ class KernelPlan:
             raise ValueError("fused DTKP apply needs an arity-1 plan over an arity-2 plan")
         ih = inner.dtkp_host()
         ioff = np.asarray(ih.seg_off, dtype=np.int64)
-        irecs = ih.recs[:, :2].astype(np.int64)
+        irecs = ih.recs[:, :2].astype(np.int64) & 0x7FFFFFFF  # (segment-end flags of a packed inner)
         order, off = csr(self.out_idx, self.n_out)
         mids = self.records[order, 0].astype(np.int64)
         lens = ioff[mids + 1] - ioff[mids]

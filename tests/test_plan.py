@@ -219,7 +219,7 @@ def test_fused_dtkp_host_plan_keeps_intermediates_whole():
     for seg in range(outer.n_out):
         for mid in outer.records[outer.out_idx == seg, 0]:
             a, b = ih.seg_off[mid], ih.seg_off[mid + 1]
-            exp.extend(ih.recs[a:b, :2].tolist())
+            exp.extend((ih.recs[a:b, :2].astype(np.int64) & 0x7FFFFFFF).tolist())
             exp_last.extend([False] * (b - a - 1) + [True])
     np.testing.assert_array_equal(rows, np.asarray(exp))
     np.testing.assert_array_equal(last, np.asarray(exp_last))
@@ -228,3 +228,40 @@ def test_fused_dtkp_host_plan_keeps_intermediates_whole():
         assert rb == h.seg_off[seg] or last[rb - 1]  # ... and start on one
     split = np.bincount(h.items[:, 0], minlength=h.n_seg) > 1
     assert h.n_partial == int(split[h.items[:, 0]].sum()) == int((h.items[:, 3] >= 0).sum())
+
+
+def test_packed_dtkp_items_cover_every_segment_once():
+    """Packed DTKP work lists (sg_dtkp_apply_desc.seg_packed): items are runs of whole
+    short segments (bit 31 on each segment's last record) or pieces of split long ones;
+    every record is covered once, every segment is closed exactly once."""
+    import numpy as np
+
+    from paper_2410_03348_b200.plan import HostSegsum
+
+    rng = np.random.default_rng(0)
+    lens = rng.choice([0, 1, 1, 2, 3, 5, 47, 48, 49, 130], size=400)
+    off = np.concatenate([[0], np.cumsum(lens)])
+    recs = rng.integers(0, 1000, size=(int(off[-1]), 2)).astype(np.int32)
+    h = HostSegsum(off, recs, 48, pack=True)
+    assert h.packed
+    flags = h.recs[:, 0] < 0
+    np.testing.assert_array_equal(h.recs[:, 0] & 0x7FFFFFFF, recs[:, 0])
+    np.testing.assert_array_equal(np.nonzero(flags)[0], off[1:][lens > 0] - 1)
+    covered = np.zeros(len(recs), dtype=int)
+    closed = np.zeros(len(lens), dtype=int)
+    for seg, rb, re, dest in h.items:
+        covered[rb:re] += 1
+        assert re - rb <= 48
+        if dest < 0:
+            assert rb == off[seg]
+            if rb == re:
+                closed[seg] += 1
+            else:
+                closed[seg: seg + int(flags[rb:re].sum())] += 1
+                assert flags[re - 1]
+        else:
+            assert lens[seg] > 48
+    for sp_seg, pb, pe in h.split:
+        closed[sp_seg] += 1
+        assert pe - pb == -(-lens[sp_seg] // 48)
+    assert (covered == 1).all() and (closed == 1).all()
