@@ -337,7 +337,7 @@ class HostSegsum:
     __slots__ = ("n_seg", "rec_words", "recs", "items", "split", "n_partial", "work", "seg_off", "packed")
 
     def __init__(self, seg_off: np.ndarray, recs: np.ndarray, max_item: int, cut_points: np.ndarray | None = None,
-                 cut_seg: np.ndarray | None = None, pack: bool = False):
+                 cut_seg: np.ndarray | None = None, pack: int = 0):
         """Items hold at most ``max_item`` records.  With ``cut_points`` (record offsets of
         groups that must stay whole — one intermediate symbol's conj records in a fused
         conj -> group_disj — and ``cut_seg``, the segment of each group) items are made of
@@ -350,11 +350,12 @@ class HostSegsum:
         packed = np.zeros((nrec, rw), dtype=np.int32)
         packed[:, :nops] = recs.reshape(nrec, nops)
         lens = np.diff(seg_off)
-        self.packed = bool(pack)
-        if pack:
-            # runs of whole short segments per item; word 0 of every segment's last record
-            # carries bit 31 (sg_dtkp_apply_desc.seg_packed); long segments are split as usual
-            seg_of, rb, re, pieces = self._pack(seg_off, lens, int(max_item))
+        self.packed = pack > 1
+        if self.packed:
+            # runs of whole short segments (<= pack records) per item; word 0 of every
+            # segment's last record carries bit 31 (sg_dtkp_apply_desc.seg_packed); long
+            # segments are split at max_item as usual
+            seg_of, rb, re, pieces = self._pack(seg_off, lens, int(max_item), int(pack))
             n_items = len(seg_of)
             nz = np.nonzero(lens > 0)[0]
             packed[seg_off[nz + 1] - 1, 0] |= np.int32(-2**31)
@@ -396,27 +397,31 @@ class HostSegsum:
         self.seg_off = seg_off
 
     @staticmethod
-    def _pack(seg_off, lens, max_item):
+    def _pack(seg_off, lens, max_item, pack):
         """(first segment, begin, end, pieces-per-segment) of packed items: whole segments
-        of at most max_item records gathered while they fit, longer ones split."""
+        gathered while the item holds at most `pack` records, segments longer than
+        max_item split."""
         seg_of, rb, re = [], [], []
         pieces = np.ones(len(lens), dtype=np.int64)
         cur_s, cur_b, cur_n = -1, 0, 0
         for sgi, ln in enumerate(lens.tolist()):
             a = int(seg_off[sgi])
-            if ln > max_item or ln == 0:
+            if ln > max_item or ln == 0 or ln > pack:
                 if cur_s >= 0:
                     seg_of.append(cur_s), rb.append(cur_b), re.append(cur_b + cur_n)
                     cur_s = -1
                 if ln == 0:
                     seg_of.append(sgi), rb.append(a), re.append(a)
                     continue
+                if ln <= max_item:  # a whole segment too long to pack: its own item
+                    seg_of.append(sgi), rb.append(a), re.append(a + ln)
+                    continue
                 k = -(-ln // max_item)
                 pieces[sgi] = k
                 for p in range(k):
                     seg_of.append(sgi), rb.append(a + p * max_item), re.append(min(a + (p + 1) * max_item, a + ln))
                 continue
-            if cur_s >= 0 and cur_n + ln > max_item:
+            if cur_s >= 0 and cur_n + ln > pack:
                 seg_of.append(cur_s), rb.append(cur_b), re.append(cur_b + cur_n)
                 cur_s = -1
             if cur_s < 0:
@@ -513,6 +518,20 @@ def csr(keys: np.ndarray, n_seg: int):
 DAMP_MAX_ITEM = 128
 DTKP_MAX_ITEM = 48
 DTKP_PACK = os.environ.get("SG_DTKP_PACK", "1") != "0"  # runs of short segments per item
+DTKP_RESIDENT_WARPS = 148 * 6 * 4  # one resident wave of 4-warp apply CTAs at 6 per SM
+
+
+def dtkp_pack_size(n_rec: int, B: int) -> int:
+    """Records per packed item: as many short segments per item as keeps ~4 items per
+    resident warp of each 32-sample column (HWF-7 step 7 at B=64: 43; the CLUTRR closure
+    at B=4096: its segments stay ~whole), so packing removes per-item overhead without
+    starving the grid."""
+    if not DTKP_PACK:
+        return 0
+    gx = max(1, -(-B // 32))
+    target = max(1, 4 * DTKP_RESIDENT_WARPS // gx)
+    p = min(DTKP_MAX_ITEM, n_rec // target)
+    return p if p > 1 else 0
 DTKP_FUSED_ITEM = 48  # inner conj records (+1 per intermediate symbol) per fused item
 DTKP_MERGE_ITEM = 8  # partial lists per first-level merge item (two-level merge)
 STAGE_BYTES = 200 * 1024
@@ -581,11 +600,17 @@ class KernelPlan:
             self._bwd_host[k] = h
         return h
 
-    def dtkp_host(self) -> HostSegsum:
+    def dtkp_host(self, pack: int = 0) -> HostSegsum:
+        """DTKP work list; pack > 1 gathers runs of whole short segments of up to `pack`
+        records per item (sg_dtkp_apply_desc.seg_packed)."""
         if self._dtkp_host is None:
+            self._dtkp_host = {}
+        h = self._dtkp_host.get(pack)
+        if h is None:
             order, off = csr(self.out_idx, self.n_out)
-            self._dtkp_host = HostSegsum(off, self.records[order], DTKP_MAX_ITEM, pack=DTKP_PACK)
-        return self._dtkp_host
+            h = HostSegsum(off, self.records[order], DTKP_MAX_ITEM, pack=pack)
+            self._dtkp_host[pack] = h
+        return h
 
     def dtkp_fused_host(self, inner: "KernelPlan") -> HostSegsum:
         """Fused conj -> group_disj (this plan arity 1 over ``inner``'s outputs, inner arity
@@ -696,10 +721,16 @@ class DevicePlan:
                 merge2 = DeviceSegsum(m2, self.device, True, 16, target_ctas=148 * 8)
         return seg, merge, merge2
 
-    def dtkp(self):
+    def dtkp(self, B: int = 0):
+        """(items, merge, merge2) for batch B (the packing granularity depends on B)."""
+        pack = dtkp_pack_size(self.kp.n_rec, B) if B else 0
         if self._dtkp is None:
-            self._dtkp, self._dtkp_merge, self._dtkp_merge2 = self._dtkp_levels(self.kp.dtkp_host())
-        return self._dtkp, self._dtkp_merge, self._dtkp_merge2
+            self._dtkp = {}
+        hit = self._dtkp.get(pack)
+        if hit is None:
+            hit = self._dtkp_levels(self.kp.dtkp_host(pack))
+            self._dtkp[pack] = hit
+        return hit
 
     def dtkp_fused(self, inner: "KernelPlan"):
         """(items, merge, merge2) of the fused conj -> group_disj over ``inner``."""

@@ -609,7 +609,7 @@ class _PendingConj:
         self.p = p
 
     def run(self):
-        dseg, dmerge, dmerge2 = self.kp.device(self.p.device).dtkp()
+        dseg, dmerge, dmerge2 = self.kp.device(self.p.device).dtkp(self.B)
         return ops.dtkp_apply(self.kp, dseg, dmerge, self.operands, None, self.K, self.W, self.I, self.B, self.p, 2,
                               dmerge2)
 
@@ -725,7 +725,7 @@ class DtkpAm:
     def _run(self, registry, kp: KernelPlan, operands, tail, arity: int, B: int) -> DtkpTags:
         W = _words(registry.size)
         p = self._p(registry, B)
-        dseg, dmerge, dmerge2 = kp.device(p.device).dtkp()
+        dseg, dmerge, dmerge2 = kp.device(p.device).dtkp(B)
         pm, pp = ops.dtkp_apply(kp, dseg, dmerge, operands, tail, self.k, W, registry.size, B, p, arity, dmerge2)
         return DtkpTags(pm, pp, registry)
 

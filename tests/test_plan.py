@@ -242,16 +242,20 @@ def test_packed_dtkp_items_cover_every_segment_once():
     lens = rng.choice([0, 1, 1, 2, 3, 5, 47, 48, 49, 130], size=400)
     off = np.concatenate([[0], np.cumsum(lens)])
     recs = rng.integers(0, 1000, size=(int(off[-1]), 2)).astype(np.int32)
-    h = HostSegsum(off, recs, 48, pack=True)
+    h = HostSegsum(off, recs, 48, pack=40)
     assert h.packed
     flags = h.recs[:, 0] < 0
     np.testing.assert_array_equal(h.recs[:, 0] & 0x7FFFFFFF, recs[:, 0])
     np.testing.assert_array_equal(np.nonzero(flags)[0], off[1:][lens > 0] - 1)
+    from paper_2410_03348_b200.plan import dtkp_pack_size
+
+    assert dtkp_pack_size(307120, 64) == 43 and dtkp_pack_size(2000, 4096) == 18 and dtkp_pack_size(100, 4096) == 0
     covered = np.zeros(len(recs), dtype=int)
     closed = np.zeros(len(lens), dtype=int)
     for seg, rb, re, dest in h.items:
         covered[rb:re] += 1
         assert re - rb <= 48
+        assert re - rb <= 40 or (dest < 0 and lens[seg] == re - rb)  # a packed run, or one whole segment
         if dest < 0:
             assert rb == off[seg]
             if rb == re:
