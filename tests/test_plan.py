@@ -255,7 +255,7 @@ def test_packed_dtkp_items_cover_every_segment_once():
     for seg, rb, re, dest in h.items:
         covered[rb:re] += 1
         assert re - rb <= 48
-        assert re - rb <= 40 or (dest < 0 and lens[seg] == re - rb)  # a packed run, or one whole segment
+        assert re - rb <= 40 or dest >= 0 or lens[seg] == re - rb  # packed run, split piece or one whole segment
         if dest < 0:
             assert rb == off[seg]
             if rb == re:
