@@ -236,19 +236,30 @@ __device__ __forceinline__ void fwd_window(float2 (&w)[R + KF - 1], const float2
 // One forward round for the lane's group: rows o0..o0+R-1 of v_i from its window.
 template <int KF, int R, bool VEC>
 __device__ __forceinline__ void fwd_round(const float2 (&w)[R + KF - 1], const float2 (&f)[KF], float2* v0,
-                                          float2* gst, int o0, int nout, bool last, const ChainArgs& a,
+                                          float2* gst, int o0, int nout, bool last, bool full, const ChainArgs& a,
                                           const Lane& L, double2& rsum) {
   float2 acc[R];
   conv_tile<KF, R, SG_CHAIN_SATFMA != 0>(acc, w, f);  // SAT: acc is already clamp01'ed
   __syncwarp();  // every group's window (this round's and the next's) is loaded before any store
   if (!last) {
+    // one 64-bit row pointer per round: the R stores use immediate offsets; `full` (warp-
+    // uniform: every row of the round is a real row) drops the per-row bounds checks
+    float2* vrow = v0 + o0 * kCP;
+    float2* grow = gst + (size_t)o0 * (kCWS / 2);
+    if (full) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const float2 v = SG_CHAIN_SATFMA ? acc[r] : clamp01x2(acc[r]);
-      v0[(o0 + r) * kCP] = v;  // padded rows >= nout get clamp01(0) = 0
-#ifndef SG_CHAIN_NOSTORE
-      if (o0 + r < nout) gst[(o0 + r) * (kCWS / 2)] = v;
-#endif
+      for (int r = 0; r < R; ++r) {
+        const float2 v = SG_CHAIN_SATFMA ? acc[r] : clamp01x2(acc[r]);
+        vrow[r * kCP] = v;
+        grow[r * (kCWS / 2)] = v;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const float2 v = SG_CHAIN_SATFMA ? acc[r] : clamp01x2(acc[r]);
+        vrow[r * kCP] = v;  // padded rows >= nout get clamp01(0) = 0
+        if (o0 + r < nout) grow[r * (kCWS / 2)] = v;
+      }
     }
   } else {
     float* q = a.out + (size_t)o0 * a.B;
@@ -324,10 +335,12 @@ __global__ void __launch_bounds__(32) k_chain_fwd(const ChainArgs a) {
     fwd_window<KF, R>(wA, v0, (kr - 1) * kRound + L.g * R);
     for (int k = kr - 1; k >= 0; k -= 2) {
       if (k >= 1) fwd_window<KF, R>(wB, v0, (k - 1) * kRound + L.g * R);
-      fwd_round<KF, R, VEC>(wA, f, v0, gst, k * kRound + L.g * R, nout, last, a, L, rsum);
+      fwd_round<KF, R, VEC>(wA, f, v0, gst, k * kRound + L.g * R, nout, last, (k + 1) * kRound <= nout, a, L,
+                            rsum);
       if (k < 1) break;
       if (k >= 2) fwd_window<KF, R>(wA, v0, (k - 2) * kRound + L.g * R);
-      fwd_round<KF, R, VEC>(wB, f, v0, gst, (k - 1) * kRound + L.g * R, nout, last, a, L, rsum);
+      fwd_round<KF, R, VEC>(wB, f, v0, gst, (k - 1) * kRound + L.g * R, nout, last, k * kRound <= nout, a, L,
+                            rsum);
     }
     if (!a.allf) cp_wait_ring();
     __syncwarp();
@@ -353,6 +366,11 @@ __device__ __forceinline__ void load_prev(float2 (&pv)[R], const ChainArgs& a, c
   const int nin = a.n[ii - 1];
   if constexpr (!FIRST) {
     const float2* p = sblk + (size_t)(a.state_off[ii - 1] + s0) * (kCWS / 2);
+    if (s0 + R <= nin) {  // all rows real: unpredicated loads at immediate offsets
+#pragma unroll
+      for (int r = 0; r < R; ++r) pv[r] = p[r * (kCWS / 2)];
+      return;
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) pv[r] = s0 + r < nin ? p[r * (kCWS / 2)] : zero2();
   } else {

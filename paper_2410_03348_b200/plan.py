@@ -532,7 +532,7 @@ def dtkp_pack_size(n_rec: int, B: int) -> int:
     target = max(1, 4 * DTKP_RESIDENT_WARPS // gx)
     p = min(DTKP_MAX_ITEM, n_rec // target)
     return p if p > 1 else 0
-DTKP_FUSED_ITEM = 48  # inner conj records (+1 per intermediate symbol) per fused item
+DTKP_FUSED_ITEM = int(os.environ.get("SG_DTKP_FUSED_ITEM", "48"))  # conj records per fused item
 DTKP_MERGE_ITEM = 8  # partial lists per first-level merge item (two-level merge)
 STAGE_BYTES = 200 * 1024
 
