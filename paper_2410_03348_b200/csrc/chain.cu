@@ -388,12 +388,19 @@ __device__ __forceinline__ void load_prev(float2 (&pv)[R], const ChainArgs& a, c
 // current tile computes; pvA holds the first tile on entry and the next step's first tile
 // on exit.  The four groups' dS partials are summed through shared scratch in fixed order
 // (deterministic, no atomics).
-template <int KF, int R, bool FIRST>
-__device__ __forceinline__ void bwd_round(float2* G, const float2 (&f)[KF], const float2 (&pv)[R], float2 (&d2)[KF],
-                                          int s0, int nin, bool full, const ChainArgs& a, const Lane& L) {
-  float2 gw[R + KF - 1];
+template <int KF, int R>
+__device__ __forceinline__ void bwd_window(float2 (&gw)[R + KF - 1], const float2* G, int s0) {
+  const float2* p = G + s0 * kCP;
 #pragma unroll
-  for (int u = 0; u < R + KF - 1; ++u) gw[u] = G[(s0 + u) * kCP];
+  for (int u = 0; u < R + KF - 1; ++u) gw[u] = p[u * kCP];
+}
+
+// gw: this round's G window, loaded by the caller one round ahead (the next round's
+// windows never overlap this round's stores: rounds ascend by kRound rows)
+template <int KF, int R, bool FIRST>
+__device__ __forceinline__ void bwd_round(float2* G, const float2 (&f)[KF], const float2 (&gw)[R + KF - 1],
+                                          const float2 (&pv)[R], float2 (&d2)[KF], int s0, int nin, bool full,
+                                          const ChainArgs& a, const Lane& L) {
   float2 acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r] = __fmul2_rn(gw[r], f[0]);  // == fma(gw, f, 0)
@@ -431,14 +438,22 @@ __device__ __forceinline__ void bwd_step(float2* G, float2* scratch, const float
 #pragma unroll
   for (int j = 0; j < KF; ++j) d2[j] = zero2();
   float2 pvB[R];
+  float2 gA[R + KF - 1], gB[R + KF - 1];
   const int s0g = L.g * R;
+  bwd_window<KF, R>(gA, G, s0g);
   for (int k = 0; k < kr; k += 2) {
     const int s0 = k * STEP + s0g;
-    if (k + 1 < kr) load_prev<R, FIRST>(pvB, a, sblk, L, i, s0 + STEP);
-    bwd_round<KF, R, FIRST>(G, f, pvA, d2, s0, nin, (k + 1) * STEP <= nin, a, L);
+    if (k + 1 < kr) {
+      load_prev<R, FIRST>(pvB, a, sblk, L, i, s0 + STEP);
+      bwd_window<KF, R>(gB, G, s0 + STEP);
+    }
+    bwd_round<KF, R, FIRST>(G, f, gA, pvA, d2, s0, nin, (k + 1) * STEP <= nin, a, L);
     if (k + 1 >= kr) break;
-    if (k + 2 < kr) load_prev<R, FIRST>(pvA, a, sblk, L, i, s0 + 2 * STEP);
-    bwd_round<KF, R, FIRST>(G, f, pvB, d2, s0 + STEP, nin, (k + 2) * STEP <= nin, a, L);
+    if (k + 2 < kr) {
+      load_prev<R, FIRST>(pvA, a, sblk, L, i, s0 + 2 * STEP);
+      bwd_window<KF, R>(gA, G, s0 + 2 * STEP);
+    }
+    bwd_round<KF, R, FIRST>(G, f, gB, pvB, d2, s0 + STEP, nin, (k + 2) * STEP <= nin, a, L);
   }
   if constexpr (!FIRST) {
     // rows [kr*STEP, kr*STEP + KF - 1) may still hold G_i; the next step's windows reach them
