@@ -349,12 +349,17 @@ def measure_train(torch, sg, device, B, steps, warmup, world, backend, flush):
     torch.cuda.synchronize(device)
     graph, mode = None, "eager"
     if backend == "nccl" or world == 1:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            step()
-        graph.replay()
-        torch.cuda.synchronize(device)
-        mode = "cuda_graph (all_reduce captured)" if world > 1 else "cuda_graph"
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, capture_error_mode="thread_local"):
+                step()
+            graph.replay()
+            torch.cuda.synchronize(device)
+            mode = "cuda_graph (all_reduce captured)" if world > 1 else "cuda_graph"
+        except Exception as exc:  # noqa: BLE001 - e.g. a collective that cannot be captured here
+            graph = None
+            mode = f"eager (capture failed: {type(exc).__name__}: {str(exc)[:120]})"
+            torch.cuda.synchronize(device)
     if world > 1:
         dist_barrier(torch, world)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
