@@ -263,6 +263,13 @@ typedef struct sg_dtkp_apply_desc {
    * with .w >= 0 are pieces of one split segment, as always.  The merges are never packed. */
   int32_t seg_packed;
   sg_dtkp_operand inner_ops[2];
+  /* rows_ranked != 0: every operand tag holds its present rows first in non-increasing key
+   * order (true for every normalised tag: kernel outputs, input tags, row gathers).  A
+   * streaming (arity-1) apply then stops reading a tag at its first row that cannot enter
+   * the full top-k — its later rows rank no higher, and a tie loses to the earlier row.
+   * 0 (e.g. hand-built tags): every row is ranked.                                      */
+  int32_t rows_ranked;
+  int32_t rows_ranked_pad_;
 } sg_dtkp_apply_desc;
 
 int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream);

@@ -104,6 +104,8 @@ class SgDtkpApplyDesc(Structure):
         ("inner_arity", c_int32),
         ("seg_packed", c_int32),
         ("inner_ops", SgDtkpOperand * 2),
+        ("rows_ranked", c_int32),
+        ("rows_ranked_pad_", c_int32),
     ]
 
 

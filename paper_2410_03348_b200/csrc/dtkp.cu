@@ -259,6 +259,7 @@ int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream) {
   k.n_items = d->seg.n_items;
   k.fused = 0;
   k.packed = d->seg_packed;
+  k.ranked = d->rows_ranked;
   if (d->inner_arity != 0) {
     // fused conj -> group_disj: only an arity-1 apply over a binary conj
     SG_RETURN_IF(d->arity != 1 || d->inner_arity != 2 || d->seg.rec_words < 2, cudaErrorInvalidValue);
@@ -275,6 +276,7 @@ int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream) {
     m.arity = 1;
     m.fused = 0;  // merges read the materialised partial lists
     m.packed = 0;
+    m.ranked = 1;  // partial lists are written in rank order
     m.ops[0].member = d->scratch_member;
     m.ops[0].present = d->scratch_present;
     m.ops[0].rows = d->seg.n_partial;

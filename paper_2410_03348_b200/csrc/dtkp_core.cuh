@@ -186,6 +186,7 @@ struct DtkpK {
   sg_dtkp_operand inner[2];
   int32_t fused;
   int32_t packed;  // items may hold runs of whole segments (record word 0 bit 31 = segment end)
+  int32_t ranked;  // operand rows are in non-increasing key order (streaming may stop early)
 };
 
 template <int WT>
@@ -280,6 +281,8 @@ __device__ __forceinline__ void stream_rows(TopK<K, WT>& S, const TopK<K, WT>& T
     uint64_t mm[WT];
     double kk;
     T.get(q, mm, kk);
+    // T is ranked: once a row cannot enter a full S, none of the later ones can
+    if (S.n == K && !(kk > S.key[K - 1])) break;
     S.insert(mm, kk, 0);
   }
 }
@@ -350,7 +353,10 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
         if (!((cur.pres >> q) & 1u)) continue;
         uint64_t mm[WT];
         cur.row(q, mm);
-        S.insert(mm, proof_key<WT>(mm, pc), 0);
+        const double kk = proof_key<WT>(mm, pc);
+        // a ranked tag's later rows cannot enter a full top-k this row cannot enter
+        if (a.ranked && S.n == K && !(kk > S.key[K - 1])) break;
+        S.insert(mm, kk, 0);
       }
       close_seg(w0);
       if (c + 1 < item.z) fetch(wn);
@@ -485,7 +491,7 @@ __host__ __device__ constexpr int dtkp_min_blocks(int K, int WT, int AR) {
          : (WT <= 2 && K <= 3) ? (AR == 1 ? (SG_DTKP_STREAM_PREFETCH ? 5 : 6)
                                   : AR == 2 ? (K > SG_DTKP_CONJ_PREFETCH_MAXK ? 6 : 4)
                                   : AR == 3 ? SG_DTKP_FUSED_MINB : 1)
-         : (WT <= 2 && K <= 5 && AR == 1) ? (SG_DTKP_STREAM_PREFETCH ? 4 : 5)
+         : (WT <= 2 && K <= 5 && AR == 1) ? 4
          : (WT <= 2 && K <= 5 && AR == 2 && K > SG_DTKP_CONJ_PREFETCH_MAXK) ? 4
          : 1;
 }

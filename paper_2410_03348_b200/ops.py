@@ -541,6 +541,7 @@ def index_tensor(indices, device) -> torch.Tensor:
 _SCHED: "dict[tuple, torch.Tensor]" = {}
 _SCHED_RETIRED: "list[torch.Tensor]" = []  # outgrown buffers a captured graph may still use
 DTKP_DYNAMIC = True  # False: the static block partition (sched = NULL), kept for tests
+DTKP_RANKED = True   # False: never use the ranked-rows early exit (A/B tests)
 
 
 def dtkp_sched(device, n: int) -> torch.Tensor:
@@ -559,7 +560,7 @@ def dtkp_sched(device, n: int) -> torch.Tensor:
 
 
 def dtkp_apply(kplan_host, dseg, dmerge, operands, tail, K: int, W: int, I: int, B: int, p: torch.Tensor,
-               arity: int, dmerge2=None, inner=None):
+               arity: int, dmerge2=None, inner=None, ranked: bool = True):
     """Run sg_dtkp_apply; operands are (member, present) pairs with full batch B.
     ``inner`` = (inner_plan, [(member, present)] * 2) runs the fused conj -> group_disj
     (``dseg`` from DevicePlan.dtkp_fused): operand 0 is the never-materialised output of
@@ -598,6 +599,7 @@ def dtkp_apply(kplan_host, dseg, dmerge, operands, tail, K: int, W: int, I: int,
     d.p = p.data_ptr() if p.numel() else None
     d.seg = dseg.struct(B)
     d.seg_packed = 1 if getattr(dseg.host, "packed", False) else 0
+    d.rows_ranked = 1 if ranked else 0
     d.out_member = out_m.data_ptr() if out_m.numel() else None
     d.out_present = out_p.data_ptr() if out_p.numel() else None
     scr_m = scr_p = None

@@ -489,16 +489,22 @@ class DtkpTags:
     ``present`` uint8 (b, n, k) host arrays — and packs it.
     """
 
-    __slots__ = ("_pm", "_pp", "registry", "_pending")
+    __slots__ = ("_pm", "_pp", "registry", "_pending", "ranked")
 
-    def __init__(self, member, present, registry, pending: "_PendingConj | None" = None):
+    def __init__(self, member, present, registry, pending: "_PendingConj | None" = None, ranked: bool | None = None):
+        # ranked: every (symbol, sample) holds its present rows first, in non-increasing key
+        # order — true for every tag the kernels, input_tags / zero / one and the row
+        # gathers produce; hand-built reference-layout tags are not assumed ranked
         self._pending = pending
         if pending is not None:
             self._pm = self._pp = None
+            self.ranked = True
         elif isinstance(member, torch.Tensor) and member.dtype == torch.int64 and member.ndim == 4:
             self._pm = member
             self._pp = present
+            self.ranked = True if ranked is None else bool(ranked)
         else:
+            self.ranked = False if ranked is None else bool(ranked)
             m = np.asarray(member.cpu() if isinstance(member, torch.Tensor) else member, dtype=np.uint8)
             pr = np.asarray(present.cpu() if isinstance(present, torch.Tensor) else present, dtype=np.uint8)
             dev = registry._dev()
@@ -722,42 +728,45 @@ class DtkpAm:
             return p.expand(p.shape[0], B).contiguous()
         raise ProvenanceError(f"registry batch {p.shape[1]} does not match tag batch {B}")
 
-    def _run(self, registry, kp: KernelPlan, operands, tail, arity: int, B: int) -> DtkpTags:
+    def _run(self, registry, kp: KernelPlan, operands, tail, arity: int, B: int, ranked: bool = True) -> DtkpTags:
         W = _words(registry.size)
         p = self._p(registry, B)
         dseg, dmerge, dmerge2 = kp.device(p.device).dtkp(B)
-        pm, pp = ops.dtkp_apply(kp, dseg, dmerge, operands, tail, self.k, W, registry.size, B, p, arity, dmerge2)
+        pm, pp = ops.dtkp_apply(kp, dseg, dmerge, operands, tail, self.k, W, registry.size, B, p, arity, dmerge2,
+                                ranked=ranked and ops.DTKP_RANKED)
         return DtkpTags(pm, pp, registry)
 
     # ---- protocol ----------------------------------------------------------------------
     def gather(self, tags: DtkpTags, indices) -> DtkpTags:
         rng = _as_range(indices)
         if rng is not None:  # contiguous symbol rows: a zero-copy view of both tensors
-            return DtkpTags(tags.pm[rng[0]:rng[1]], tags.pp[rng[0]:rng[1]], tags.registry)
+            return DtkpTags(tags.pm[rng[0]:rng[1]], tags.pp[rng[0]:rng[1]], tags.registry, ranked=tags.ranked)
         idx = ops.index_map(indices, tags.count, tags.pm.device).idx
         n = int(idx.numel())
         pm = torch.empty((n, *tags.pm.shape[1:]), device=tags.pm.device, dtype=torch.int64)
         pp = torch.empty((n, *tags.pp.shape[1:]), device=tags.pp.device, dtype=torch.uint8)
         ops.rows_gather(tags.pm, idx, pm)
         ops.rows_gather(tags.pp, idx, pp)
-        return DtkpTags(pm, pp, tags.registry)
+        return DtkpTags(pm, pp, tags.registry, ranked=tags.ranked)
 
     def conj(self, a: DtkpTags, b: DtkpTags) -> DtkpTags:
         """All row pairs OR-ed, dedup + top-k (provenance.py:328-341)."""
         self._check_registry(a, b)
         B = max(a.batch, b.batch)
-        return self._run(a.registry, _IDPLANS.conj_plan(a.count), [_bcast_dtkp(a, B), _bcast_dtkp(b, B)], None, 2, B)
+        return self._run(a.registry, _IDPLANS.conj_plan(a.count), [_bcast_dtkp(a, B), _bcast_dtkp(b, B)], None, 2, B,
+                         a.ranked and b.ranked)
 
     def disj(self, a: DtkpTags, b: DtkpTags) -> DtkpTags:
         """Rows of a then rows of b, dedup + top-k (provenance.py:343-350)."""
         self._check_registry(a, b)
         B = max(a.batch, b.batch)
-        return self._run(a.registry, _IDPLANS.disj_plan(a.count), [_bcast_dtkp(a, B)], _bcast_dtkp(b, B), 1, B)
+        return self._run(a.registry, _IDPLANS.disj_plan(a.count), [_bcast_dtkp(a, B)], _bcast_dtkp(b, B), 1, B,
+                         a.ranked and b.ranked)
 
     def group_disj(self, tags: DtkpTags, groups) -> DtkpTags:
         kp = _group_plan(groups, tags.count)
         B = tags.batch
-        return self._run(tags.registry, kp, [_bcast_dtkp(tags, B)], None, 1, B)
+        return self._run(tags.registry, kp, [_bcast_dtkp(tags, B)], None, 1, B, tags.ranked)
 
     def concat_syms(self, parts) -> DtkpTags:
         registry = parts[0].registry
@@ -765,7 +774,7 @@ class DtkpAm:
         for p in parts:
             p.aligned()
         pms, pps = zip(*(_bcast_dtkp(p, B) for p in parts))
-        return DtkpTags(torch.cat(pms, dim=0), torch.cat(pps, dim=0), registry)
+        return DtkpTags(torch.cat(pms, dim=0), torch.cat(pps, dim=0), registry, ranked=all(p.ranked for p in parts))
 
     def probs(self, tags: DtkpTags) -> torch.Tensor:
         """Differentiable add-mult probability of every tag, (B, n) (provenance.py:398-413)."""
@@ -793,13 +802,14 @@ class DtkpAm:
         pp = torch.empty((n, *tags.pp.shape[1:]), device=tags.pp.device, dtype=torch.uint8)
         ops.rows_gather(tags.pm, idx, pm)
         ops.rows_gather(tags.pp, idx, pp)
-        return DtkpTags(pm, pp, tags.registry)
+        return DtkpTags(pm, pp, tags.registry, ranked=tags.ranked)
 
     def stack_parts(self, parts) -> DtkpTags:
         registry = parts[0].registry
         for p in parts:
             p.aligned()
-        return DtkpTags(torch.cat([p.pm for p in parts], dim=3), torch.cat([p.pp for p in parts], dim=2), registry)
+        return DtkpTags(torch.cat([p.pm for p in parts], dim=3), torch.cat([p.pp for p in parts], dim=2), registry,
+                        ranked=all(p.ranked for p in parts))
 
     def tags_from_proofs(self, registry, proofs, b: int = 1) -> DtkpTags:
         """Single-symbol tag from explicit proof index sets, normalised like the operators."""
@@ -816,7 +826,7 @@ class DtkpAm:
         pv = self._p(registry, b).t().double().contiguous()
         om, op = ops.dedup_topk(torch.as_tensor(member, device=dev), torch.as_tensor(present, device=dev), pv,
                                 self.k)
-        return DtkpTags(om.cpu().numpy()[:, None], op.cpu().numpy()[:, None], registry)
+        return DtkpTags(om.cpu().numpy()[:, None], op.cpu().numpy()[:, None], registry, ranked=True)
 
     # ---- fused entry points ---------------------------------------------------------
     # the fused conj -> group_disj launch is exact (tests/test_gpu_fused.py) but, as built,
@@ -841,7 +851,7 @@ class DtkpAm:
         if self.fuse_conj_group and len(tags_list) == 2:
             p = self._p(registry, batch)
             return DtkpTags(None, None, registry, pending=_PendingConj(self, registry, kp, ops_, batch, p))
-        return self._run(registry, kp, ops_, None, len(tags_list), batch)
+        return self._run(registry, kp, ops_, None, len(tags_list), batch, all(t.ranked for t in tags_list))
 
     def _run_fused(self, kp: KernelPlan, pend: "_PendingConj", B: int) -> DtkpTags:
         dseg, dmerge, dmerge2 = kp.device(pend.p.device).dtkp_fused(pend.kp)
@@ -851,7 +861,7 @@ class DtkpAm:
 
     def union_tags(self, a: DtkpTags, b: DtkpTags, uplan) -> DtkpTags:
         B = max(a.batch, b.batch)
-        return self._run(a.registry, uplan.kplan, [_bcast_dtkp(a, B)], _bcast_dtkp(b, B), 1, B)
+        return self._run(a.registry, uplan.kplan, [_bcast_dtkp(a, B)], _bcast_dtkp(b, B), 1, B, a.ranked and b.ranked)
 
 
 def wmc_exact(proofs, weights) -> float:

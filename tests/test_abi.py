@@ -56,7 +56,7 @@ def test_struct_layout_matches_c(tmp_path):
         " sizeof(sg_damp_plan), sizeof(sg_dtkp_operand), sizeof(sg_dtkp_apply_desc), offsetof(sg_damp_plan, fwd),"
         " offsetof(sg_dtkp_apply_desc, p), offsetof(sg_dtkp_apply_desc, seg), offsetof(sg_dtkp_apply_desc, merge),"
         " sizeof(sg_maxprod_plan), offsetof(sg_maxprod_plan, seg_off), offsetof(sg_maxprod_plan, in_recs),"
-        " offsetof(sg_dtkp_apply_desc, inner_ops), offsetof(sg_dtkp_apply_desc, inner_arity));"
+        " offsetof(sg_dtkp_apply_desc, inner_ops), offsetof(sg_dtkp_apply_desc, rows_ranked));"
         "return 0;}\n"
     )
     exe = tmp_path / "layout"
@@ -67,6 +67,6 @@ def test_struct_layout_matches_c(tmp_path):
         ctypes.sizeof(N.SgDtkpApplyDesc), N.SgDampPlan.fwd.offset, N.SgDtkpApplyDesc.p.offset,
         N.SgDtkpApplyDesc.seg.offset, N.SgDtkpApplyDesc.merge.offset, ctypes.sizeof(N.SgMaxprodPlan),
         N.SgMaxprodPlan.seg_off.offset, N.SgMaxprodPlan.in_recs.offset, N.SgDtkpApplyDesc.inner_ops.offset,
-        N.SgDtkpApplyDesc.inner_arity.offset,
+        N.SgDtkpApplyDesc.rows_ranked.offset,
     ]
     assert vals == expect

@@ -83,3 +83,24 @@ def _pending_case(cuda, sg):
     assert s.tags.pending is None and f.tags.pending is None
     p = sg.get_probs(sg.union(f, s))
     assert torch.isfinite(p).all()
+
+
+@pytest.mark.parametrize("name", ["dtkp_hwf7", "dtkp_clutrr_e5_r20_k5", "dtkp_path_k5", "dtkp_sum4_k5"])
+def test_ranked_early_exit_and_packing_are_exact(cuda, name):
+    """The streaming kernels' ranked-rows early exit (sg_dtkp_apply_desc.rows_ranked) and
+    the packed work items change no retained proof and no row order."""
+    from paper_2410_03348_b200 import ops, plan
+
+    gold = load_golden(name)
+    inputs = [gold[f"in{i}"] for i in range(int(gold["n_inputs"]))]
+    fast = run_gpu(name, inputs)
+    old = (ops.DTKP_RANKED, plan.DTKP_PACK)
+    try:
+        ops.DTKP_RANKED, plan.DTKP_PACK = False, False
+        plain = run_gpu(name, inputs)
+    finally:
+        ops.DTKP_RANKED, plan.DTKP_PACK = old
+    np.testing.assert_array_equal(fast["member"], plain["member"])
+    np.testing.assert_array_equal(fast["present"], plain["present"])
+    np.testing.assert_array_equal(fast["probs"], plain["probs"])
+    np.testing.assert_array_equal(fast["member"], gold["member"])
