@@ -491,7 +491,7 @@ __host__ __device__ constexpr int dtkp_min_blocks(int K, int WT, int AR) {
          : (WT <= 2 && K <= 3) ? (AR == 1 ? (SG_DTKP_STREAM_PREFETCH ? 5 : 6)
                                   : AR == 2 ? (K > SG_DTKP_CONJ_PREFETCH_MAXK ? 6 : 4)
                                   : AR == 3 ? SG_DTKP_FUSED_MINB : 1)
-         : (WT <= 2 && K <= 5 && AR == 1) ? 4
+         : (WT <= 2 && K <= 5 && AR == 1) ? 5
          : (WT <= 2 && K <= 5 && AR == 2 && K > SG_DTKP_CONJ_PREFETCH_MAXK) ? 4
          : 1;
 }
