@@ -121,6 +121,51 @@ def e2e_time(step_host, dev, iters):
     return (time.perf_counter() - t) * 1e3 / iters
 
 
+def graphed_e2e(step_fn, dev_inputs, host_inputs, dev, iters):
+    """ms per step through the public GraphedStep API with host buffers: each step copies
+    its inputs H2D from pinned memory into the capture (one arena copy), replays the graph
+    and reads the loss (output 0) back to the host."""
+    from paper_2410_03348_b200.graph import GraphedStep
+
+    g = GraphedStep(step_fn, dev_inputs)
+    views = g.pinned_inputs(0)
+    for v, h in zip(views, host_inputs):
+        v.copy_(h)
+
+    res = {}
+
+    def once():
+        out = g(*views)
+        r = out[0] if isinstance(out, (tuple, list)) else out
+        if r.numel() == 1:
+            return float(r)
+        if "host" not in res:  # the step's (B, n) result goes back to the host
+            res["host"] = torch.empty(r.shape, dtype=r.dtype).pin_memory()
+        res["host"].copy_(r.detach(), non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        return None
+
+    for _ in range(2):
+        once()
+    torch.cuda.synchronize(dev)
+    t = time.perf_counter()
+    for _ in range(iters):
+        once()
+    torch.cuda.synchronize(dev)
+    ms = (time.perf_counter() - t) * 1e3 / iters
+    del g
+    return ms
+
+
+def e2e_entry(graphed_ms, eager_ms, units, h2d, d2h, what):
+    return {"ms_per_step": graphed_ms, "value": units / (graphed_ms * 1e-3), "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h,
+            "api": f"GraphedStep (public API): {what}; inputs H2D from pinned host memory + graph replay + loss "
+                   "read back every step",
+            "eager": {"ms_per_step": eager_ms, "value": units / (eager_ms * 1e-3),
+                      "api": "the same step through the eager API calls, inputs H2D + loss.item() every step"}}
+
+
 def cpu_reference(workload, batch, steps=1, warmup=0, procs=0, **kw):
     env = dict(os.environ)
     env["OPENBLAS_NUM_THREADS"] = "1"
@@ -209,13 +254,14 @@ def sum2_train(dev, iters=20, cpu=True, B=64):
         return loss.item()
 
     e2e_ms = e2e_time(host_step, dev, iters)
+    g_ms = graphed_e2e(lambda x, t: step_on(x, t), [imgs, targets], [imgs_h.to(memory_format=torch.channels_last),
+                                                                     tgt_h], dev, iters)
     hbm, src = hbm_peak()
     res = {"config": "MNIST Sum-2 train: synthetic 28x28 digits, random-init LeNet, DAMP, B=64 (BASELINE configs[0])",
            "metric": "train samples/s", "batch": B,
            "device": {"ms_per_step": ms, "value": B / (ms * 1e-3), "mode": mode},
-           "e2e": {"ms_per_step": e2e_ms, "value": B / (e2e_ms * 1e-3), "h2d_bytes_per_step": pin_x.numel() * 4 + B * 8,
-                   "d2h_bytes_per_step": 8, "api": "eager: LeNet -> make_distribution -> sum_n -> get_probs -> "
-                                                   "loss_nll -> backward -> Adam, images H2D + loss.item() per step"},
+           "e2e": e2e_entry(g_ms, e2e_ms, B, pin_x.numel() * 4 + B * 8, 8,
+                            "LeNet -> make_distribution -> sum_n -> get_probs -> loss_nll -> backward -> Adam"),
            "roofline": roofline(alg, by, ms, hbm, src) | {"note": "symbolic kernels only; the step is launch-bound "
                                                                   "(LeNet + Adam dominate)"}}
     if cpu:
@@ -255,6 +301,8 @@ def hwf7(dev, iters=20, cpu=True, B=64):
         return loss.item()
 
     e2e_ms = e2e_time(host_step, dev, max(3, iters // 2))
+    g_ms = graphed_e2e(lambda *a: step_on(list(a[:7]), a[7]), xs + [targets], [xs_h[i] for i in range(7)] + [tgt_h],
+                       dev, iters)
     hbm, src = hbm_peak()
     combos = sum(int(np.prod(s)) for s in HWF7_SIZES)
     cand = by.get("dtkp_apply", {}).get("units", 0)
@@ -262,9 +310,8 @@ def hwf7(dev, iters=20, cpu=True, B=64):
            "fwd+loss+bwd)", "batch": B, "output_symbols": n_out,
            "device": {"ms_per_step": ms, "value": B / (ms * 1e-3), "symbol_combos_per_s": B * combos / (ms * 1e-3),
                       "candidate_rows_per_s": cand / (ms * 1e-3), "mode": mode},
-           "e2e": {"ms_per_step": e2e_ms, "value": B / (e2e_ms * 1e-3), "h2d_bytes_per_step": pin_x.numel() * 4 + B * 8,
-                   "d2h_bytes_per_step": 8, "api": "eager programs.hwf (memoised plans) + loss_nll + autograd.grad, "
-                                                   "inputs H2D + loss.item() per step"},
+           "e2e": e2e_entry(g_ms, e2e_ms, B, pin_x.numel() * 4 + B * 8, 8,
+                            "programs.hwf (memoised plans) + loss_nll + autograd.grad"),
            "first_call_s_incl_host_plans": first,
            "roofline": roofline(alg, by, ms, hbm, src), "issue_ceiling": issue_ceiling("hwf7_")}
     if cpu:
@@ -303,6 +350,7 @@ def clutrr(dev, iters=20, cpu=True, B=4096, n_entities=5, k=5):
         return loss.item()
 
     e2e_ms = e2e_time(host_step, dev, iters)
+    g_ms = graphed_e2e(lambda xv, t: step_on(xv, t), [x, targets], [x_h, tgt_h], dev, iters)
     hbm, src = hbm_peak()
     cand = by.get("dtkp_apply", {}).get("units", 0)
     res = {"config": f"CLUTRR-style kinship closure, {n_entities} entities x 20 relations, DTKP k={k}, B={B} "
@@ -310,9 +358,8 @@ def clutrr(dev, iters=20, cpu=True, B=4096, n_entities=5, k=5):
            "derived_facts": n_derived,
            "device": {"ms_per_step": ms, "value": B / (ms * 1e-3), "candidate_rows_per_s": cand / (ms * 1e-3),
                       "mode": mode},
-           "e2e": {"ms_per_step": e2e_ms, "value": B / (e2e_ms * 1e-3), "h2d_bytes_per_step": pin_x.numel() * 4 + B * 8,
-                   "d2h_bytes_per_step": 8, "api": "eager clutrr_closure (fixpoint.closure) + loss_nll + autograd.grad,"
-                                                   " inputs H2D + loss.item() per step"},
+           "e2e": e2e_entry(g_ms, e2e_ms, B, pin_x.numel() * 4 + B * 8, 8,
+                            "clutrr_closure (fixpoint.closure) + loss_nll + autograd.grad"),
            "roofline": roofline(alg, by, ms, hbm, src), "issue_ceiling": issue_ceiling("clutrr_")}
     if cpu:
         res["cpu"] = cpu_reference("clutrr", B, steps=1, warmup=0)
@@ -363,6 +410,8 @@ def sweep_point(dev, arity, size, B, iters=20, cpu=True, provenance="damp"):
         torch.cuda.current_stream(dev).synchronize()
 
     e2e_ms = e2e_time(host_step, dev, iters)
+    g_ms = graphed_e2e(lambda *a: step_on(list(a[:arity]), a[arity]), xs + [w], [xs_h[i] for i in range(arity)] + [w_h],
+                       dev, iters)
     C = size ** arity
     kp = sg.plan.build_plan(f, None, [tuple(syms)] * arity).kernel_plan()
     hbm, src = hbm_peak()
@@ -372,10 +421,8 @@ def sweep_point(dev, arity, size, B, iters=20, cpu=True, provenance="damp"):
            "device": {"ms_per_step": ms, "value": B * C / (ms * 1e-3), "fwd_ms": ms_f,
                       "fwd_combos_per_s": B * C / (ms_f * 1e-3), "mode": mode,
                       "fwd_hbm_frac": alg_f / (ms_f * 1e-3) / 1e9 / hbm},
-           "e2e": {"ms_per_step": e2e_ms, "value": B * C / (e2e_ms * 1e-3),
-                   "h2d_bytes_per_step": pin_x.numel() * 4 + pin_w.numel() * 4, "d2h_bytes_per_step": out_h.numel() * 4,
-                   "api": "eager make_distribution/apply/get_probs + autograd.grad(grad_outputs=w), inputs + w H2D, "
-                          "probs D2H per step"},
+           "e2e": e2e_entry(g_ms, e2e_ms, B * C, pin_x.numel() * 4 + pin_w.numel() * 4, out_h.numel() * 4,
+                            "make_distribution/apply/get_probs + autograd.grad(grad_outputs=w), probs D2H"),
            "roofline": roofline(alg, by, ms, hbm, src)}
     if cpu and provenance == "damp":
         cb = SWEEP_CPU_BATCH.get((arity, size))
@@ -415,13 +462,14 @@ def max_sum15(dev, iters=20, B=16384):
         return loss.item()
 
     e2e_ms = e2e_time(host_step, dev, iters)
+    g_ms = graphed_e2e(lambda *a: step_on(list(a[:15]), a[15]), xs + [targets], [xs_h[i] for i in range(15)] + [tgt_h],
+                       dev, iters)
     hbm, src = hbm_peak()
     return {"config": "max/DAMP variant: Sum-15 chain (14 max-product applies) + loss_nll, fwd+bwd, B=16384",
             "metric": "symbol-combos/s", "batch": B,
             "device": {"ms_per_step": ms, "value": B * 9590 / (ms * 1e-3), "mode": mode},
-            "e2e": {"ms_per_step": e2e_ms, "value": B * 9590 / (e2e_ms * 1e-3),
-                    "h2d_bytes_per_step": pin_x.numel() * 4 + B * 8, "d2h_bytes_per_step": 8,
-                    "api": "eager sum_n under DampMax + loss_nll + autograd.grad, inputs H2D + loss.item()"},
+            "e2e": e2e_entry(g_ms, e2e_ms, B * 9590, pin_x.numel() * 4 + B * 8, 8,
+                             "sum_n under DampMax + loss_nll + autograd.grad"),
             "roofline": roofline(alg, by, ms, hbm, src)}
 
 
