@@ -14,8 +14,10 @@
 // Mapping.  Lane = sample: a sample's whole chain lives in its own shared-memory column,
 // so no two lanes ever touch the same word and the kernels need no barrier at all.  The
 // forward updates the state in place (outputs descending, four at a time from one
-// 13-row window), streams the clamped intermediate states and the argmax tap j* (one
-// byte) per (step, output, sample) to HBM row-major over the batch (coalesced).  The
+// 13-row window), streams the clamped intermediate states to HBM row-major over the batch
+// and the argmax tap j* (one byte per step, output, sample) packed four outputs to a
+// 32-bit word in a warp-blocked layout ([warp][word][32 lanes]: one coalesced 128-byte
+// access per four outputs of the warp).  The
 // backward walks the steps down, loads v_{i-1} into its column, and scatters each
 // output's upstream gradient to its argmax record: G_{i-1}[s*] += g[o] * S[j*] (shared
 // column) and dS[j*] += g[o] * v_{i-1}[s*] (registers, select-updated), o ascending.
@@ -40,11 +42,12 @@ struct MaxChainArgs {
   int64_t dfilt_sr[kMcMaxSteps], dfilt_sb[kMcMaxSteps];
   int n[kMcMaxSteps + 1];
   int state_off[kMcMaxSteps + 1];  // row offset of v_i (i = 1..m-1) in `states`
-  int arg_off[kMcMaxSteps + 1];    // row offset of step i's argmax bytes (i = 1..m)
+  int arg_off[kMcMaxSteps + 1];    // word offset of step i's packed argmax (4 outputs per word)
+  int arg_words;                   // packed argmax words per warp
   int m, n_max;
   int64_t B;
   float* states;         // [state rows][B]
-  uint8_t* argmax;       // [arg rows][B]: j* of output o of step i
+  uint32_t* argmax;      // [warp][arg_words][32]: byte k of word w = j* of output 4w + k of the step
   float* out;            // [n_m][B]
   double* rowsum;        // optional [B]
   const float* g_out;    // [n_m][B]
@@ -92,9 +95,10 @@ __global__ void __launch_bounds__(32) k_maxchain_fwd(const MaxChainArgs a) {
     const int nin = a.n[i - 1], nout = a.n[i];
     const bool last = i == a.m;
     float* gst = last ? a.out : a.states + (size_t)a.state_off[i] * a.B;
-    uint8_t* gam = a.argmax + (size_t)a.arg_off[i] * a.B;
-    // outputs descending in groups of 4 (o3 = o0 - 3 .. o0): one window of KF + 3 rows
-    for (int o0 = nout - 1; o0 >= 0; o0 -= 4) {
+    uint32_t* gam = a.argmax + ((size_t)blockIdx.x * a.arg_words + a.arg_off[i]) * 32 + lane;
+    // outputs descending in aligned groups of 4 (4g+3 .. 4g): one window of KF + 3 rows,
+    // one packed argmax word per group
+    for (int o0 = ((nout - 1) | 3); o0 >= 0; o0 -= 4) {
       float w[KF + 3];
 #pragma unroll
       for (int u = 0; u < KF + 3; ++u) {
@@ -114,21 +118,21 @@ __global__ void __launch_bounds__(32) k_maxchain_fwd(const MaxChainArgs a) {
         for (int q = 0; q < 4; ++q) {
           const int o = o0 - q;
           const int s = o - j;
-          maxrec<KF>(best[q], arg[q], w[3 - q + PAD - j] * f[j], j, o >= 0 && s >= 0 && s < nin);
+          maxrec<KF>(best[q], arg[q], w[3 - q + PAD - j] * f[j], j, o < nout && s >= 0 && s < nin);
         }
       }
+      uint32_t word = 0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int o = o0 - q;
-        if (o < 0) break;
+        if (o >= nout) continue;  // the top group may reach past the step's last output
         const float v = clamp01(best[q]);  // every output of a Toeplitz step has a record
         V[(PAD + o) * 32] = v;
-        if (bval) {
-          gst[(size_t)o * a.B + b0] = v;
-          gam[(size_t)o * a.B + b0] = (uint8_t)arg[q];
-        }
+        if (bval) gst[(size_t)o * a.B + b0] = v;
+        word |= (uint32_t)arg[q] << (8 * (3 - q));  // byte (o & 3) = output o
         if (last) rs += (double)v;
       }
+      gam[(size_t)(o0 >> 2) * 32] = word;
     }
   }
   if (a.rowsum != nullptr && bval) a.rowsum[b0] = rs;
@@ -199,19 +203,19 @@ __global__ void __launch_bounds__(32) k_maxchain_bwd(const MaxChainArgs a) {
       }
     }
     for (int s = 0; s < nin; ++s) H[s * 32] = 0.f;
-    const uint8_t* am = a.argmax + (size_t)a.arg_off[i] * a.B + b;
-    // the argmax taps of 16 outputs are loaded together (independent loads in flight),
-    // then the outputs are scattered in ascending order
-    constexpr int kBatch = 16;
+    const uint32_t* am = a.argmax + ((size_t)blockIdx.x * a.arg_words + a.arg_off[i]) * 32 + lane;
+    // the packed argmax taps of 32 outputs (8 coalesced words) are loaded together, then
+    // the outputs are scattered in ascending order
+    constexpr int kBatch = 32;
     for (int o0 = 0; o0 < nout; o0 += kBatch) {
-      int jb[kBatch];
+      uint32_t jw[kBatch / 4];
 #pragma unroll
-      for (int q = 0; q < kBatch; ++q) jb[q] = o0 + q < nout ? (int)__ldg(am + (size_t)(o0 + q) * a.B) : 0;
+      for (int q = 0; q < kBatch / 4; ++q) jw[q] = o0 + 4 * q < nout ? __ldg(am + (size_t)((o0 >> 2) + q) * 32) : 0u;
 #pragma unroll
       for (int q = 0; q < kBatch; ++q) {
         const int o = o0 + q;
         if (o >= nout) break;
-        const int j = jb[q];
+        const int j = (int)((jw[q >> 2] >> (8 * (3 - (q & 3)))) & 0xffu);
         const int s = o - j;
         const float g = G[o * 32];
         float fj = f[0];
@@ -248,10 +252,11 @@ static int mc_fill(MaxChainArgs& a, const sg_chain* c) {
     a.state_off[i] = soff;
     if (i < c->m) soff += a.n[i];
     a.arg_off[i] = aoff;
-    aoff += a.n[i];
+    aoff += (a.n[i] + 3) / 4;
     if (a.n[i] > nmax) nmax = a.n[i];
   }
   a.state_off[0] = a.arg_off[0] = 0;
+  a.arg_words = aoff;
   a.n_max = nmax;
   a.states = c->states;
   return 0;
@@ -293,12 +298,12 @@ int64_t sg_maxchain_states_elems(int32_t n0, int32_t kf, int32_t m, int64_t B) {
 }
 
 int64_t sg_maxchain_argmax_bytes(int32_t n0, int32_t kf, int32_t m, int64_t B) {
-  int64_t rows = 0, n = n0;
+  int64_t words = 0, n = n0;
   for (int i = 1; i <= m; ++i) {
     n += kf - 1;
-    rows += n;
+    words += (n + 3) / 4;
   }
-  return rows * B;
+  return words * 4 * 32 * ((B + 31) / 32);  // [warp][words][32 lanes] u32
 }
 
 int32_t sg_maxchain_max_rows(int32_t kf) {
@@ -315,8 +320,9 @@ int sg_maxchain_fwd(const sg_chain* c, float* out, double* rowsum, uint8_t* argm
   SG_RETURN_IF(a.n_max > sg_maxchain_max_rows(c->kf), cudaErrorNotSupported);
   a.out = out;
   a.rowsum = rowsum;
-  a.argmax = argmax;
-  const size_t smem = (size_t)(c->kf - 1 + a.n_max) * 32 * sizeof(float);
+  a.argmax = reinterpret_cast<uint32_t*>(argmax);
+  SG_RETURN_IF(((uintptr_t)argmax & 3) != 0, cudaErrorInvalidValue);
+  const size_t smem = (size_t)(c->kf - 1 + a.n_max + 3) * 32 * sizeof(float);
   cudaStream_t st = (cudaStream_t)stream;
   switch (c->kf) {
 #define X(K) \
@@ -334,7 +340,8 @@ int sg_maxchain_bwd(const sg_chain* c, const uint8_t* argmax, const float* grad_
   if (rc) return rc;
   if (c->B <= 0) return 0;
   SG_RETURN_IF(a.n_max > sg_maxchain_max_rows(c->kf), cudaErrorNotSupported);
-  a.argmax = const_cast<uint8_t*>(argmax);
+  a.argmax = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(argmax));
+  SG_RETURN_IF(((uintptr_t)argmax & 3) != 0, cudaErrorInvalidValue);
   a.g_out = grad_out;
   a.dbase_p = grad_base.ptr;
   a.dbase_sr = grad_base.stride_row;
