@@ -112,13 +112,21 @@ __global__ void __launch_bounds__(32) k_maxchain_fwd(const MaxChainArgs a) {
         best[q] = 0.f;
         arg[q] = -1;
       }
+      // interior groups (warp-uniform): every tap of all four outputs is a record
+      if (o0 - 3 >= KF - 1 && o0 <= nin - 1) {
 #pragma unroll
-      for (int j = KF - 1; j >= 0; --j) {  // s = o - j ascending
+        for (int j = KF - 1; j >= 0; --j)  // s = o - j ascending
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int o = o0 - q;
-          const int s = o - j;
-          maxrec<KF>(best[q], arg[q], w[3 - q + PAD - j] * f[j], j, o < nout && s >= 0 && s < nin);
+          for (int q = 0; q < 4; ++q) maxrec<KF>(best[q], arg[q], w[3 - q + PAD - j] * f[j], j, true);
+      } else {
+#pragma unroll
+        for (int j = KF - 1; j >= 0; --j) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int o = o0 - q;
+            const int s = o - j;
+            maxrec<KF>(best[q], arg[q], w[3 - q + PAD - j] * f[j], j, o < nout && s >= 0 && s < nin);
+          }
         }
       }
       uint32_t word = 0;
@@ -215,7 +223,7 @@ __global__ void __launch_bounds__(32) k_maxchain_bwd(const MaxChainArgs a) {
       for (int q = 0; q < kBatch; ++q) {
         const int o = o0 + q;
         if (o >= nout) break;
-        const int j = (int)((jw[q >> 2] >> (8 * (3 - (q & 3)))) & 0xffu);
+        const int j = (int)((jw[q >> 2] >> (8 * (q & 3))) & 0xffu);  // byte (o & 3) of word o >> 2
         const int s = o - j;
         const float g = G[o * 32];
         float fj = f[0];
