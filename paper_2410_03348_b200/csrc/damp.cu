@@ -659,38 +659,45 @@ constexpr int kCsRows = 8;     // rows per warp tile
 constexpr int kCsPitch = 33;   // shared row pitch (floats): conflict-free transposed stores
 __device__ __forceinline__ int cs_div(int a, int b) { return (a + b - 1) / b; }
 
-// rows [0, n) of X for samples b0 .. b0 + 31 -> sm[r * kCsPitch + s] (0 past B)
+// rows [0, n) of X for samples b0 .. b0 + 31 -> sm[r * kCsPitch + s] (0 past B).  128
+// threads: a sample-major (user (B, n)) block is read as 4 threads per sample walking
+// its contiguous row (no index division, 4 loads in flight per thread); symbol-major rows
+// as 32 samples x 4 rows per pass.
 __device__ __forceinline__ void cs_stage(float* sm, const Rows& X, int n, int64_t B, int64_t b0) {
   const int tid = threadIdx.x;
-  const int nt = blockDim.x;
   const int ns = (int)(B - b0 < kWarp ? B - b0 : kWarp);
-  if (X.sr == 1 && X.sb != 0) {  // sample-major (user block): sample s's row is contiguous
-    for (int i = tid; i < kWarp * n; i += nt) {
-      const int sidx = i / n, r = i - sidx * n;
-      sm[r * kCsPitch + sidx] = sidx < ns ? __ldg(X.p + (b0 + sidx) * X.sb + r) : 0.f;
-    }
-  } else {  // symbol-major rows (or a batch broadcast): row r over the samples
-    for (int i = tid; i < kWarp * n; i += nt) {
-      const int r = i >> 5, sidx = i & 31;
-      sm[r * kCsPitch + sidx] = sidx < ns ? __ldg(X.p + (int64_t)r * X.sr + (b0 + sidx) * X.sb) : 0.f;
-    }
+  if (X.sr == 1 && X.sb != 0) {
+    const int sidx = tid >> 2, k0 = tid & 3;
+    const bool ok = sidx < ns;
+    const float* src = X.p + (b0 + (ok ? sidx : 0)) * X.sb;
+#pragma unroll 4
+    for (int r = k0; r < n; r += 4) sm[r * kCsPitch + sidx] = ok ? __ldg(src + r) : 0.f;
+  } else {
+    const int sidx = tid & 31;
+    const bool ok = sidx < ns;
+    const float* src = X.p + (b0 + (ok ? sidx : 0)) * X.sb;
+#pragma unroll 4
+    for (int r = tid >> 5; r < n; r += 4) sm[r * kCsPitch + sidx] = ok ? __ldg(src + (int64_t)r * X.sr) : 0.f;
   }
 }
 
 // sm[r * kCsPitch + s] -> rows [0, n) of Y for samples b0 .. b0 + 31 (coalesced either way)
 __device__ __forceinline__ void cs_unstage(const float* sm, const WRows& Y, int n, int64_t B, int64_t b0) {
   const int tid = threadIdx.x;
-  const int nt = blockDim.x;
   const int ns = (int)(B - b0 < kWarp ? B - b0 : kWarp);
   if (Y.sr == 1) {
-    for (int i = tid; i < kWarp * n; i += nt) {
-      const int sidx = i / n, r = i - sidx * n;
-      if (sidx < ns) Y.p[(b0 + sidx) * Y.sb + r] = sm[r * kCsPitch + sidx];
+    const int sidx = tid >> 2, k0 = tid & 3;
+    if (sidx < ns) {
+      float* dst = Y.p + (b0 + sidx) * Y.sb;
+#pragma unroll 4
+      for (int r = k0; r < n; r += 4) dst[r] = sm[r * kCsPitch + sidx];
     }
   } else {
-    for (int i = tid; i < kWarp * n; i += nt) {
-      const int r = i >> 5, sidx = i & 31;
-      if (sidx < ns) Y.p[(int64_t)r * Y.sr + (b0 + sidx) * Y.sb] = sm[r * kCsPitch + sidx];
+    const int sidx = tid & 31;
+    if (sidx < ns) {
+      float* dst = Y.p + (b0 + sidx) * Y.sb;
+#pragma unroll 4
+      for (int r = tid >> 5; r < n; r += 4) dst[(int64_t)r * Y.sr] = sm[r * kCsPitch + sidx];
     }
   }
 }

@@ -95,10 +95,10 @@ __global__ void __launch_bounds__(32) k_maxchain_fwd(const MaxChainArgs a) {
     const int nin = a.n[i - 1], nout = a.n[i];
     const bool last = i == a.m;
     float* gst = last ? a.out : a.states + (size_t)a.state_off[i] * a.B;
-    uint32_t* gam = a.argmax + ((size_t)blockIdx.x * a.arg_words + a.arg_off[i]) * 32 + lane;
-    // outputs descending in aligned groups of 4 (4g+3 .. 4g): one window of KF + 3 rows,
-    // one packed argmax word per group
-    for (int o0 = ((nout - 1) | 3); o0 >= 0; o0 -= 4) {
+    // byte (o & 3) of the lane's word o >> 2 of this step (packed layout, see the header)
+    uint8_t* gam = reinterpret_cast<uint8_t*>(a.argmax + ((size_t)blockIdx.x * a.arg_words + a.arg_off[i]) * 32 + lane);
+    // outputs descending in groups of 4 (o0 - 3 .. o0): one window of KF + 3 rows
+    for (int o0 = nout - 1; o0 >= 0; o0 -= 4) {
       float w[KF + 3];
 #pragma unroll
       for (int u = 0; u < KF + 3; ++u) {
@@ -112,35 +112,25 @@ __global__ void __launch_bounds__(32) k_maxchain_fwd(const MaxChainArgs a) {
         best[q] = 0.f;
         arg[q] = -1;
       }
-      // interior groups (warp-uniform): every tap of all four outputs is a record
-      if (o0 - 3 >= KF - 1 && o0 <= nin - 1) {
 #pragma unroll
-        for (int j = KF - 1; j >= 0; --j)  // s = o - j ascending
+      for (int j = KF - 1; j >= 0; --j) {  // s = o - j ascending
 #pragma unroll
-          for (int q = 0; q < 4; ++q) maxrec<KF>(best[q], arg[q], w[3 - q + PAD - j] * f[j], j, true);
-      } else {
-#pragma unroll
-        for (int j = KF - 1; j >= 0; --j) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int o = o0 - q;
-            const int s = o - j;
-            maxrec<KF>(best[q], arg[q], w[3 - q + PAD - j] * f[j], j, o < nout && s >= 0 && s < nin);
-          }
+        for (int q = 0; q < 4; ++q) {
+          const int o = o0 - q;
+          const int s = o - j;
+          maxrec<KF>(best[q], arg[q], w[3 - q + PAD - j] * f[j], j, o >= 0 && s >= 0 && s < nin);
         }
       }
-      uint32_t word = 0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int o = o0 - q;
-        if (o >= nout) continue;  // the top group may reach past the step's last output
+        if (o < 0) break;
         const float v = clamp01(best[q]);  // every output of a Toeplitz step has a record
         V[(PAD + o) * 32] = v;
         if (bval) gst[(size_t)o * a.B + b0] = v;
-        word |= (uint32_t)arg[q] << (8 * (3 - q));  // byte (o & 3) = output o
+        gam[(size_t)(o >> 2) * 128 + (o & 3)] = (uint8_t)arg[q];
         if (last) rs += (double)v;
       }
-      gam[(size_t)(o0 >> 2) * 32] = word;
     }
   }
   if (a.rowsum != nullptr && bval) a.rowsum[b0] = rs;
@@ -330,7 +320,7 @@ int sg_maxchain_fwd(const sg_chain* c, float* out, double* rowsum, uint8_t* argm
   a.rowsum = rowsum;
   a.argmax = reinterpret_cast<uint32_t*>(argmax);
   SG_RETURN_IF(((uintptr_t)argmax & 3) != 0, cudaErrorInvalidValue);
-  const size_t smem = (size_t)(c->kf - 1 + a.n_max + 3) * 32 * sizeof(float);
+  const size_t smem = (size_t)(c->kf - 1 + a.n_max) * 32 * sizeof(float);
   cudaStream_t st = (cudaStream_t)stream;
   switch (c->kf) {
 #define X(K) \
