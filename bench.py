@@ -198,12 +198,13 @@ def build_step(torch, sg, device):
 def chain_bytes(B, n0=10, kf=10, m=N_DIGITS - 1):
     """Algorithmic HBM bytes of one fused Sum-N chain launch (K1c/K2c):
     fwd reads v_0 and the m filters and writes the m-1 clamped states, v_m and its fp64
-    per-sample row sums; bwd reads
-    g_out, the filters, the states and v_0 and writes dS_1..m and dv_0."""
+    per-sample row sums; the step's bwd (sg_chain_bwd_nll: the loss gradient generated in
+    the kernel) reads the per-sample target, row sum and picked probability, the filters,
+    the states and v_0, and writes dS_1..m and dv_0."""
     states = sum(n0 + i * (kf - 1) for i in range(1, m))
     n_out = n0 + m * (kf - 1)
     fwd = 4 * B * (n0 + m * kf + states + n_out) + 8 * B  # + the fp64 row sums
-    bwd = 4 * B * (n_out + m * kf + states + n0 + m * kf + n0)
+    bwd = 4 * B * (m * kf + states + n0 + m * kf + n0) + 20 * B  # + target, row sum, p_t
     return fwd, bwd
 
 
@@ -236,7 +237,7 @@ def kernel_roofline(torch, device, B, hbm_gbs, reps=12):
     rows = sum(n0 + i * (kf - 1) for i in range(1, m))
     n_out = n0 + m * (kf - 1)
     fwd_bytes, bwd_bytes = chain_bytes(B, n0, kf, m)
-    per_set = 4 * B * (n0 + 2 * m * kf + rows + 2 * n_out + n0)
+    per_set = 4 * B * (n0 + 2 * m * kf + rows + 2 * n_out + n0) + 16 * B
     nsets = max(2, -(-2 * 126 * 2**20 // per_set) + 1)
     sets = []
     for _ in range(nsets):
@@ -246,23 +247,28 @@ def kernel_roofline(torch, device, B, hbm_gbs, reps=12):
         out = torch.empty((n_out, B), device=device)
         rowsum = torch.empty((B,), device=device, dtype=torch.float64)
         g = torch.rand((n_out, B), device=device)
+        tgt = torch.randint(0, n_out, (B,), device=device)
+        rowsum.fill_(1.0)
         gbase = torch.empty_like(base)
         gfilt = [torch.empty_like(f) for f in filt]
         c = ops._chain_struct(n0, kf, B, base, filt, states)
         garr = (N.SgRows * N.CHAIN_MAX_STEPS)()
         for i, t in enumerate(gfilt):
             garr[i] = N.rows(t)
-        sets.append((c, out, g, gbase, garr, (base, filt, states, gfilt, rowsum)))
+        sets.append((c, out, g, gbase, garr, (base, filt, states, gfilt, rowsum, tgt)))
 
     def run(kind, j):
         st = torch.cuda.current_stream(device).cuda_stream
         c, out, g, gbase, garr, _ = sets[j % nsets]
         if kind == "fwd":
             rc = lib.sg_chain_fwd(ctypes.byref(c), out.data_ptr(), sets[j % nsets][5][4].data_ptr(), st)
-        else:
-            rc = lib.sg_chain_bwd(ctypes.byref(c), g.data_ptr(), N.rows(gbase), garr, st)
+        else:  # the step's backward: the loss gradient is generated inside the kernel
+            keep = sets[j % nsets][5]
+            rc = lib.sg_chain_bwd_nll(ctypes.byref(c), N.rows(out), keep[5].data_ptr(), keep[4].data_ptr(),
+                                      one.data_ptr(), N.rows(gbase), garr, st)
         N.check(rc, kind)
 
+    one = torch.ones((), device=device, dtype=torch.float64)
     res = {}
     for kind, nbytes in (("fwd", fwd_bytes), ("bwd", bwd_bytes)):
         side = torch.cuda.Stream(device)
@@ -690,7 +696,8 @@ def run_gpu_arm(args):
             "gpu_launches_per_step": launches,
             "roofline": roof,
             "roofline_method": "algorithmic bytes of the fused chain launch (DESIGN.md 4: fwd 4B(n0+m*kf+"
-                               "states+n_out)+8B, bwd 4B(n_out+2*m*kf+states+2*n0)) / the launch's CUDA-event "
+                               "states+n_out)+8B, bwd (loss gradient generated in the kernel) "
+                               "4B(2*m*kf+states+2*n0)+20B) / the launch's CUDA-event "
                                "time inside the captured step; kernels[*].avg_us: the same launch alone, "
                                "graph-replayed back to back over rotating buffer sets > 2x L2 (cold)",
             "cpu_baseline": cpu,

@@ -171,6 +171,13 @@ int32_t sg_chain_max_rows(int32_t kf);
 int sg_chain_fwd(const sg_chain* chain, float* out, double* rowsum, sg_stream_t stream);
 int sg_chain_bwd(const sg_chain* chain, const float* grad_out, sg_rows grad_base,
                  const sg_rows* grad_filters, sg_stream_t stream);
+/* The same backward when the chain's output feeds loss_nll directly (learn.py:92-119): the
+ * upstream gradient rows are generated inside the kernel from the per-sample scalars
+ * (target, row sum, picked probability, d loss) exactly as sg_nll_bwd computes them, so
+ * the [n_m][B] gradient is never written or read.  probs = the chain's output v_m. */
+int sg_chain_bwd_nll(const sg_chain* chain, sg_rows probs, const int64_t* targets, const double* rowsum,
+                     const double* grad_loss, sg_rows grad_base, const sg_rows* grad_filters,
+                     sg_stream_t stream);
 
 /* 1 when sg_damp_apply_bwd of a short-filter Toeplitz plan (conv == 1) reads its upstream
  * gradient in any layout (the staged kernels); 0: it must be contiguous [n_out][B]. */

@@ -61,6 +61,13 @@ struct ChainArgs {
   float* out;          // [n[m]][B]
   double* rowsum;      // forward, optional: [B] sum over the output rows (fp64)
   const float* g_out;  // backward: [n[m]][B]
+  // backward with the fused loss (g_out == nullptr): the upstream gradient of
+  // loss_nll(v_m, targets) (learn.py:92-119) is generated in place from per-sample scalars
+  const float* nll_p;          // v_m values [n[m]][B] (sg_rows: stride_row, stride_b)
+  int64_t nll_sr, nll_sb;
+  const int64_t* nll_t;        // targets [B] (-1 = no mass)
+  const double* nll_rowsum;    // [B] sums of v_m rows (the forward's side output)
+  const double* nll_gloss;     // scalar upstream gradient of the loss
   float* dbase_p;      // backward: grad of v_0 (strided like base)
   int64_t dbase_sr, dbase_sb;
 };
@@ -507,6 +514,35 @@ __global__ void __launch_bounds__(32) k_chain_bwd(const ChainArgs a) {
     // g_out rows -> G through cp.async (all rows in flight at once), zero-filled past the
     // last row and for samples past B; joins the first ring group
     const int nm = a.n[a.m];
+    if (a.g_out == nullptr) {
+      // fused loss backward: d loss / d v_m[r][b] = coef_b * ([r == t_b] / den_b - p_t / den_b^2)
+      // with the fp64 scalars of k_nll_bwd (damp.cu), stored as fp32 exactly as it does
+      double cf[2], cm[2], inv[2];
+      int64_t tt[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t bb = h == 0 ? L.ba : L.bb;
+        const int64_t t = __ldg(a.nll_t + bb);
+        const bool bad = t < -1 || t >= (int64_t)nm;
+        const double sm = __ldg(a.nll_rowsum + bb);
+        const double pt = t >= 0 && !bad ? (double)__ldg(a.nll_p + t * a.nll_sr + bb * a.nll_sb) : 0.0;
+        const double den = sm + 1e-8;
+        const double c = fmax(t >= 0 ? fmax(pt / den, 1e-12) : 0.0, 1e-12);
+        cf[h] = bad ? __longlong_as_double(0x7ff8000000000000LL) : t >= 0 ? -(__ldg(a.nll_gloss) / (double)a.B) / c : 0.0;
+        cm[h] = -pt / (den * den);
+        inv[h] = 1.0 / den;
+        tt[h] = t;
+      }
+      for (int r = L.g; r < grows; r += kCG) {
+        float2 v = zero2();
+        if (r < nm) {
+          v.x = L.nv > 0 ? (float)(cf[0] * ((r == tt[0] ? inv[0] : 0.0) + cm[0])) : 0.f;
+          v.y = L.nv > 1 ? (float)(cf[1] * ((r == tt[1] ? inv[1] : 0.0) + cm[1])) : 0.f;
+        }
+        G[r * kCP + L.c] = v;
+      }
+      cp_commit();
+    } else {
     for (int r = L.g; r < grows; r += kCG) {
       const float* q = a.g_out + (size_t)(r < nm ? r : 0) * a.B;
       if (VEC) {
@@ -518,6 +554,7 @@ __global__ void __launch_bounds__(32) k_chain_bwd(const ChainArgs a) {
       }
     }
     cp_commit();
+    }
   }
   const float2* sblk =
       reinterpret_cast<const float2*>(a.states) + (size_t)L.wid * a.state_rows * (kCWS / 2) + L.c;
@@ -657,13 +694,40 @@ int sg_chain_fwd(const sg_chain* c, float* out, double* rowsum, sg_stream_t stre
   }
 }
 
+static int chain_bwd_impl(ChainArgs& a, const sg_chain* c, sg_rows grad_base, const sg_rows* grad_filters,
+                          sg_stream_t stream);
+
 int sg_chain_bwd(const sg_chain* c, const float* grad_out, sg_rows grad_base, const sg_rows* grad_filters,
                  sg_stream_t stream) {
   ChainArgs a{};
   int rc = fill_args(a, c);
   if (rc) return rc;
   if (c->B <= 0) return 0;
+  SG_RETURN_IF(grad_out == nullptr, cudaErrorInvalidValue);
   a.g_out = grad_out;
+  return chain_bwd_impl(a, c, grad_base, grad_filters, stream);
+}
+
+int sg_chain_bwd_nll(const sg_chain* c, sg_rows probs, const int64_t* targets, const double* rowsum,
+                     const double* grad_loss, sg_rows grad_base, const sg_rows* grad_filters, sg_stream_t stream) {
+  ChainArgs a{};
+  int rc = fill_args(a, c);
+  if (rc) return rc;
+  if (c->B <= 0) return 0;
+  SG_RETURN_IF(probs.ptr == nullptr || targets == nullptr || rowsum == nullptr || grad_loss == nullptr,
+               cudaErrorInvalidValue);
+  a.g_out = nullptr;
+  a.nll_p = probs.ptr;
+  a.nll_sr = probs.stride_row;
+  a.nll_sb = probs.stride_b;
+  a.nll_t = targets;
+  a.nll_rowsum = rowsum;
+  a.nll_gloss = grad_loss;
+  return chain_bwd_impl(a, c, grad_base, grad_filters, stream);
+}
+
+static int chain_bwd_impl(ChainArgs& a, const sg_chain* c, sg_rows grad_base, const sg_rows* grad_filters,
+                          sg_stream_t stream) {
   a.dbase_p = grad_base.ptr;
   a.dbase_sr = grad_base.stride_row;
   a.dbase_sb = grad_base.stride_b;
@@ -675,7 +739,7 @@ int sg_chain_bwd(const sg_chain* c, const float* grad_out, sg_rows grad_base, co
   const size_t smem = bwd_warp_bytes(c->kf, a.n_max);
   SG_RETURN_IF(smem > kChainSmemMax, cudaErrorNotSupported);
   cudaStream_t st = (cudaStream_t)stream;
-  const bool vec = (c->B % 2 == 0) && ((uintptr_t)grad_out % 8 == 0);
+  const bool vec = (c->B % 2 == 0) && ((uintptr_t)a.g_out % 8 == 0);
   switch (c->kf) {
 #define X(K)                                                                \
   case K:                                                                   \

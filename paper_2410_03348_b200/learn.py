@@ -42,7 +42,12 @@ def loss_nll(probs: torch.Tensor, targets) -> torch.Tensor:
     targets = targets.to(device=probs.device, dtype=torch.int64).contiguous()
     if probs.dtype != torch.float32:
         probs = probs.float()
-    return ops.NllLoss.apply(probs.t(), targets)
+    pnb = probs.t()
+    chain = ops.known_chain(pnb)
+    if chain is not None:  # the output of a fused Sum-N chain: one fused backward
+        n0, kf, B, base, filters, states, rowsum, _ = chain
+        return ops.ChainNllLoss.apply((n0, kf, B, states, rowsum), pnb.detach(), targets, base, *filters)
+    return ops.NllLoss.apply(pnb, targets)
 
 
 def _check_targets(targets, b: int, n: int) -> torch.Tensor:

@@ -277,6 +277,9 @@ class ConvChainFn(torch.autograd.Function):
         with launch_timer("chain_fwd"):
             rc = _lib().sg_chain_fwd(ctypes.byref(c), out.data_ptr(), rowsum.data_ptr(), N.stream_ptr(dev))
         N.check(rc, "sg_chain_fwd")
+        # what a directly following loss_nll needs to fuse its backward into the chain's
+        # (ChainNllLoss): the chain operands and the forward's per-sample row sums
+        out._sg_chain = (n0, kf, B, base, tuple(filters), states, rowsum, out._version)
         _ledger("chain_fwd", 4 * B * (n0 + m * kf + (elems // B if B else 0) + out.shape[0]) + 8 * B,
                 B * sum((n0 + i * (kf - 1)) * kf for i in range(m)))
         out._sg_rowsum = (rowsum, out._version)  # for loss_nll on exactly these values
@@ -356,6 +359,66 @@ class MaxChainFn(torch.autograd.Function):
         m = len(filters)
         _ledger("maxchain_bwd", 4 * B * (g.shape[0] + 2 * m * kf + states.numel() // max(B, 1) + 2 * n0)
                 + argmax.numel(), B * sum((n0 + i * (kf - 1)) * kf for i in range(m)))
+        return (None, None, None, gbase, *gfilt)
+
+
+FUSE_CHAIN_NLL = True  # loss_nll directly on a fused chain's output: one fused backward
+
+
+def known_chain(probs_nb: torch.Tensor):
+    """The chain operands behind ``probs_nb`` if it is exactly a fused chain's (unmodified)
+    output, else None."""
+    base = probs_nb._base if probs_nb._base is not None else probs_nb
+    tag = getattr(base, "_sg_chain", None)
+    if tag is None or not FUSE_CHAIN_NLL:
+        return None
+    if (base._version != tag[-1] or probs_nb.data_ptr() != base.data_ptr() or probs_nb.shape != base.shape
+            or probs_nb.stride() != base.stride()):
+        return None
+    return tag
+
+
+class ChainNllLoss(torch.autograd.Function):
+    """loss_nll (learn.py:92-119) of a fused Sum-N chain's output as ONE autograd node over
+    the chain's operands: the forward reuses the chain forward's output and row sums
+    (sg_nll_fwd_rowsum), the backward is a single sg_chain_bwd_nll launch whose upstream
+    gradient rows are generated inside the kernel (bit-identical to sg_nll_bwd's), so the
+    [n_out][B] loss gradient never exists.  The chain's own autograd node stays valid for
+    any other use of the probabilities."""
+
+    @staticmethod
+    def forward(ctx, meta, probs_nb, targets, base, *filters):
+        n0, kf, B, states, rowsum = meta
+        n = probs_nb.shape[0]
+        dev = probs_nb.device
+        loss = torch.empty((), device=dev, dtype=torch.float64)
+        scratch = _nll_scratch(dev, n, B)
+        rc = _lib().sg_nll_fwd_rowsum(N.rows(probs_nb), n, B, targets.data_ptr(), rowsum.data_ptr(), loss.data_ptr(),
+                                      scratch.data_ptr(), N.stream_ptr(dev))
+        N.check(rc, "sg_nll_fwd_rowsum")
+        _ledger("nll_fwd", 4 * B + 16 * B, B * n)
+        ctx.meta = (n0, kf, B)
+        ctx.save_for_backward(probs_nb, targets, rowsum, base, states, *filters)
+        return loss
+
+    @staticmethod
+    def backward(ctx, gloss):
+        probs_nb, targets, rowsum, base, states, *filters = ctx.saved_tensors
+        n0, kf, B = ctx.meta
+        g = gloss.detach().to(torch.float64).reshape(()).contiguous()
+        gbase = torch.empty_like(base)
+        gfilt = [torch.empty_like(f) for f in filters]
+        c = _chain_struct(n0, kf, B, base, filters, states)
+        arr = (N.SgRows * N.CHAIN_MAX_STEPS)()
+        for i, t in enumerate(gfilt):
+            arr[i] = N.rows(t)
+        with launch_timer("chain_bwd"):
+            rc = _lib().sg_chain_bwd_nll(ctypes.byref(c), N.rows(probs_nb), targets.data_ptr(), rowsum.data_ptr(),
+                                         g.data_ptr(), N.rows(gbase), arr, N.stream_ptr(g.device))
+        N.check(rc, "sg_chain_bwd_nll")
+        m = len(filters)
+        _ledger("chain_bwd", 4 * B * (2 * m * kf + states.numel() // max(B, 1) + 2 * n0) + 24 * B,
+                B * sum((n0 + i * (kf - 1)) * kf for i in range(m)))
         return (None, None, None, gbase, *gfilt)
 
 

@@ -666,3 +666,45 @@ def test_dtkp_long_group_disj_two_level_merge(cuda, k):
         ref = A.dtkp_group_disj(opair, groups, p, k)
         np.testing.assert_array_equal(got.member, ref[0])
         np.testing.assert_array_equal(got.present, ref[1])
+
+
+@pytest.mark.parametrize("n_digits,B", [(15, 4096), (6, 77), (3, 1)])
+def test_chain_nll_fused_backward_bit_identical(cuda, n_digits, B):
+    """loss_nll straight on a fused chain's output runs ONE fused backward
+    (sg_chain_bwd_nll, the loss gradient generated in the kernel); it must equal the
+    separate sg_nll_bwd + sg_chain_bwd launches bit for bit, loss and gradients, with
+    None targets and a second consumer of the same probabilities."""
+    S = sg()
+    from paper_2410_03348_b200 import ops
+    from paper_2410_03348_b200 import programs as P
+    from paper_2410_03348_b200.learn import loss_nll
+
+    rng = np.random.default_rng(n_digits * 31 + B)
+    xs = [G.rows(rng, B, 10) for _ in range(n_digits)]
+    t = rng.integers(-1, 9 * n_digits + 1, size=B)
+
+    def run(fuse, second):
+        old = ops.FUSE_CHAIN_NLL
+        ops.FUSE_CHAIN_NLL = fuse
+        try:
+            ctx = S.ProgramContext(S.Damp())
+            leaves = [torch.tensor(x, device=cuda, dtype=torch.float32, requires_grad=True) for x in xs]
+            probs = S.get_probs(P.sum_n(ctx, [S.make_distribution(ctx, lf, range(10)) for lf in leaves]))
+            loss = loss_nll(probs, torch.as_tensor(t, device=cuda))
+            total = loss * 3.0 + (probs[:, :3].double().sum() if second else 0.0)
+            total.backward()
+            return float(loss), [lf.grad.double().cpu().numpy() for lf in leaves]
+        finally:
+            ops.FUSE_CHAIN_NLL = old
+
+    l1, g1 = run(True, False)
+    l0, g0 = run(False, False)
+    assert l1 == l0
+    for a, b in zip(g1, g0):
+        np.testing.assert_array_equal(a, b)
+    # a second consumer of the probabilities: its gradient flows through the chain's own
+    # backward and is added by autograd (summed after, not before, the chain backward)
+    _, g1 = run(True, True)
+    _, g0 = run(False, True)
+    for a, b in zip(g1, g0):
+        assert_close_rel(a, b, 1e-5, 1e-6)
