@@ -505,6 +505,25 @@ __global__ void __launch_bounds__(32) k_chain_bwd(const ChainArgs a) {
   float2* G = F + kRing * KF * kCP;
   float2* scratch = G + (size_t)grows * kCP;  // [kCG * KF] rows
   pdl_wait_c();
+  // fused loss: the per-sample scalars are requested first, so their (dependent: target ->
+  // picked probability) loads overlap the filter staging below
+  const int nm_ = a.n[a.m];
+  int64_t tt[2] = {0, 0};
+  double rsm[2] = {0.0, 0.0}, ptv[2] = {0.0, 0.0};
+  if (a.g_out == nullptr) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t bb = h == 0 ? L.ba : L.bb;
+      tt[h] = __ldg(a.nll_t + bb);
+      rsm[h] = __ldg(a.nll_rowsum + bb);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t bb = h == 0 ? L.ba : L.bb;
+      const bool ok = tt[h] >= 0 && tt[h] < (int64_t)nm_;
+      ptv[h] = ok ? (double)__ldg(a.nll_p + tt[h] * a.nll_sr + bb * a.nll_sb) : 0.0;
+    }
+  }
   // backward step t handles apply i = m - t; its filter sits in ring slot t % kRing
   for (int t = 0; t < kRing - 1; ++t) {
     if (t < a.m) stage_filter<KF>(F, t % kRing, a.filt[a.m - 1 - t], L, a.B);
@@ -518,20 +537,16 @@ __global__ void __launch_bounds__(32) k_chain_bwd(const ChainArgs a) {
       // fused loss backward: d loss / d v_m[r][b] = coef_b * ([r == t_b] / den_b - p_t / den_b^2)
       // with the fp64 scalars of k_nll_bwd (damp.cu), stored as fp32 exactly as it does
       double cf[2], cm[2], inv[2];
-      int64_t tt[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int64_t bb = h == 0 ? L.ba : L.bb;
-        const int64_t t = __ldg(a.nll_t + bb);
+        const int64_t t = tt[h];
         const bool bad = t < -1 || t >= (int64_t)nm;
-        const double sm = __ldg(a.nll_rowsum + bb);
-        const double pt = t >= 0 && !bad ? (double)__ldg(a.nll_p + t * a.nll_sr + bb * a.nll_sb) : 0.0;
-        const double den = sm + 1e-8;
+        const double pt = ptv[h];
+        const double den = rsm[h] + 1e-8;
         const double c = fmax(t >= 0 ? fmax(pt / den, 1e-12) : 0.0, 1e-12);
         cf[h] = bad ? __longlong_as_double(0x7ff8000000000000LL) : t >= 0 ? -(__ldg(a.nll_gloss) / (double)a.B) / c : 0.0;
         cm[h] = -pt / (den * den);
         inv[h] = 1.0 / den;
-        tt[h] = t;
       }
       for (int r = L.g; r < grows; r += kCG) {
         float2 v = zero2();
