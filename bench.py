@@ -204,7 +204,7 @@ def chain_bytes(B, n0=10, kf=10, m=N_DIGITS - 1):
     states = sum(n0 + i * (kf - 1) for i in range(1, m))
     n_out = n0 + m * (kf - 1)
     fwd = 4 * B * (n0 + m * kf + states + n_out) + 8 * B  # + the fp64 row sums
-    bwd = 4 * B * (m * kf + states + n0 + m * kf + n0) + 20 * B  # + target, row sum, p_t
+    bwd = 4 * B * (m * kf + states + n0 + m * kf + n0) + 24 * B  # + target, row sum, p_t (fp64)
     return fwd, bwd
 
 
@@ -249,13 +249,14 @@ def kernel_roofline(torch, device, B, hbm_gbs, reps=12):
         g = torch.rand((n_out, B), device=device)
         tgt = torch.randint(0, n_out, (B,), device=device)
         rowsum.fill_(1.0)
+        picked = torch.rand((B,), device=device, dtype=torch.float64)
         gbase = torch.empty_like(base)
         gfilt = [torch.empty_like(f) for f in filt]
         c = ops._chain_struct(n0, kf, B, base, filt, states)
         garr = (N.SgRows * N.CHAIN_MAX_STEPS)()
         for i, t in enumerate(gfilt):
             garr[i] = N.rows(t)
-        sets.append((c, out, g, gbase, garr, (base, filt, states, gfilt, rowsum, tgt)))
+        sets.append((c, out, g, gbase, garr, (base, filt, states, gfilt, rowsum, tgt, picked)))
 
     def run(kind, j):
         st = torch.cuda.current_stream(device).cuda_stream
@@ -264,7 +265,7 @@ def kernel_roofline(torch, device, B, hbm_gbs, reps=12):
             rc = lib.sg_chain_fwd(ctypes.byref(c), out.data_ptr(), sets[j % nsets][5][4].data_ptr(), st)
         else:  # the step's backward: the loss gradient is generated inside the kernel
             keep = sets[j % nsets][5]
-            rc = lib.sg_chain_bwd_nll(ctypes.byref(c), N.rows(out), keep[5].data_ptr(), keep[4].data_ptr(),
+            rc = lib.sg_chain_bwd_nll(ctypes.byref(c), keep[5].data_ptr(), keep[4].data_ptr(), keep[6].data_ptr(),
                                       one.data_ptr(), N.rows(gbase), garr, st)
         N.check(rc, kind)
 
@@ -697,7 +698,7 @@ def run_gpu_arm(args):
             "roofline": roof,
             "roofline_method": "algorithmic bytes of the fused chain launch (DESIGN.md 4: fwd 4B(n0+m*kf+"
                                "states+n_out)+8B, bwd (loss gradient generated in the kernel) "
-                               "4B(2*m*kf+states+2*n0)+20B) / the launch's CUDA-event "
+                               "4B(2*m*kf+states+2*n0)+24B) / the launch's CUDA-event "
                                "time inside the captured step; kernels[*].avg_us: the same launch alone, "
                                "graph-replayed back to back over rotating buffer sets > 2x L2 (cold)",
             "cpu_baseline": cpu,

@@ -173,11 +173,11 @@ int sg_chain_bwd(const sg_chain* chain, const float* grad_out, sg_rows grad_base
                  const sg_rows* grad_filters, sg_stream_t stream);
 /* The same backward when the chain's output feeds loss_nll directly (learn.py:92-119): the
  * upstream gradient rows are generated inside the kernel from the per-sample scalars
- * (target, row sum, picked probability, d loss) exactly as sg_nll_bwd computes them, so
- * the [n_m][B] gradient is never written or read.  probs = the chain's output v_m. */
-int sg_chain_bwd_nll(const sg_chain* chain, sg_rows probs, const int64_t* targets, const double* rowsum,
-                     const double* grad_loss, sg_rows grad_base, const sg_rows* grad_filters,
-                     sg_stream_t stream);
+ * (target, row sum and picked probability from sg_nll_fwd_rowsum, d loss) exactly as
+ * sg_nll_bwd computes them, so the [n_m][B] gradient is never written or read. */
+int sg_chain_bwd_nll(const sg_chain* chain, const int64_t* targets, const double* rowsum,
+                     const double* picked, const double* grad_loss, sg_rows grad_base,
+                     const sg_rows* grad_filters, sg_stream_t stream);
 
 /* 1 when sg_damp_apply_bwd of a short-filter Toeplitz plan (conv == 1) reads its upstream
  * gradient in any layout (the staged kernels); 0: it must be contiguous [n_out][B]. */
@@ -208,7 +208,8 @@ int sg_nll_fwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, doub
 /* The same loss when the per-sample row sums are already known (rowsum: [B] fp64, e.g.
  * from sg_chain_fwd): one launch that only gathers p[t_b][b]. */
 int sg_nll_fwd_rowsum(sg_rows probs, int64_t n, int64_t B, const int64_t* targets,
-                      const double* rowsum, double* loss, void* scratch, sg_stream_t stream);
+                      const double* rowsum, double* loss, void* scratch, double* picked,
+                      sg_stream_t stream);  /* picked (optional): [B] p[t_b][b] as fp64 */
 /* grad[n][b] = -(g/B) / c_b * (delta(n, t_b) / (s_b + 1e-8) - p[t_b][b] / (s_b + 1e-8)^2) */
 int sg_nll_bwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets,
                const double* grad_loss, const double* rowsum, sg_rows grad, sg_stream_t stream);

@@ -147,8 +147,8 @@ EXPORTS = {
     "sg_chain_max_rows": (c_int32, [c_int32]),
     "sg_chain_fwd": (c_int32, [POINTER(SgChain), c_void_p, c_void_p, c_void_p]),
     "sg_chain_bwd": (c_int32, [POINTER(SgChain), c_void_p, SgRows, POINTER(SgRows), c_void_p]),
-    "sg_chain_bwd_nll": (c_int32, [POINTER(SgChain), SgRows, c_void_p, c_void_p, c_void_p, SgRows, POINTER(SgRows),
-                                   c_void_p]),
+    "sg_chain_bwd_nll": (c_int32, [POINTER(SgChain), c_void_p, c_void_p, c_void_p, c_void_p, SgRows,
+                                   POINTER(SgRows), c_void_p]),
     "sg_damp_conv_staged": (c_int32, [c_int32, c_int32, c_int32]),
     "sg_maxchain_states_elems": (c_int64, [c_int32, c_int32, c_int32, c_int64]),
     "sg_maxchain_argmax_bytes": (c_int64, [c_int32, c_int32, c_int32, c_int64]),
@@ -158,7 +158,8 @@ EXPORTS = {
     "sg_nll_scratch_bytes": (c_int64, [c_int64, c_int64]),
     "sg_nll_fwd": (c_int32, [SgRows, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "sg_nll_bwd": (c_int32, [SgRows, c_int64, c_int64, c_void_p, c_void_p, c_void_p, SgRows, c_void_p]),
-    "sg_nll_fwd_rowsum": (c_int32, [SgRows, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sg_nll_fwd_rowsum": (c_int32, [SgRows, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                    c_void_p]),
     "sg_maxprod_fwd": (c_int32, [POINTER(SgMaxprodPlan), POINTER(SgRows), c_int64, c_int32, c_void_p, c_void_p,
                                  c_void_p]),
     "sg_maxprod_bwd": (c_int32, [POINTER(SgMaxprodPlan), POINTER(SgRows), c_int64, c_void_p, SgRows, POINTER(SgRows),

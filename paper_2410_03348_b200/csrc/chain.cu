@@ -63,8 +63,7 @@ struct ChainArgs {
   const float* g_out;  // backward: [n[m]][B]
   // backward with the fused loss (g_out == nullptr): the upstream gradient of
   // loss_nll(v_m, targets) (learn.py:92-119) is generated in place from per-sample scalars
-  const float* nll_p;          // v_m values [n[m]][B] (sg_rows: stride_row, stride_b)
-  int64_t nll_sr, nll_sb;
+  const double* nll_pt;        // [B] picked probabilities p[t_b][b] (sg_nll_fwd_rowsum's side output)
   const int64_t* nll_t;        // targets [B] (-1 = no mass)
   const double* nll_rowsum;    // [B] sums of v_m rows (the forward's side output)
   const double* nll_gloss;     // scalar upstream gradient of the loss
@@ -505,9 +504,8 @@ __global__ void __launch_bounds__(32) k_chain_bwd(const ChainArgs a) {
   float2* G = F + kRing * KF * kCP;
   float2* scratch = G + (size_t)grows * kCP;  // [kCG * KF] rows
   pdl_wait_c();
-  // fused loss: the per-sample scalars are requested first, so their (dependent: target ->
-  // picked probability) loads overlap the filter staging below
-  const int nm_ = a.n[a.m];
+  // fused loss: the per-sample scalars (target, row sum, picked probability — independent
+  // loads) are requested first, so their latency overlaps the filter staging below
   int64_t tt[2] = {0, 0};
   double rsm[2] = {0.0, 0.0}, ptv[2] = {0.0, 0.0};
   if (a.g_out == nullptr) {
@@ -516,12 +514,7 @@ __global__ void __launch_bounds__(32) k_chain_bwd(const ChainArgs a) {
       const int64_t bb = h == 0 ? L.ba : L.bb;
       tt[h] = __ldg(a.nll_t + bb);
       rsm[h] = __ldg(a.nll_rowsum + bb);
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t bb = h == 0 ? L.ba : L.bb;
-      const bool ok = tt[h] >= 0 && tt[h] < (int64_t)nm_;
-      ptv[h] = ok ? (double)__ldg(a.nll_p + tt[h] * a.nll_sr + bb * a.nll_sb) : 0.0;
+      ptv[h] = __ldg(a.nll_pt + bb);
     }
   }
   // backward step t handles apply i = m - t; its filter sits in ring slot t % kRing
@@ -723,18 +716,16 @@ int sg_chain_bwd(const sg_chain* c, const float* grad_out, sg_rows grad_base, co
   return chain_bwd_impl(a, c, grad_base, grad_filters, stream);
 }
 
-int sg_chain_bwd_nll(const sg_chain* c, sg_rows probs, const int64_t* targets, const double* rowsum,
+int sg_chain_bwd_nll(const sg_chain* c, const int64_t* targets, const double* rowsum, const double* picked,
                      const double* grad_loss, sg_rows grad_base, const sg_rows* grad_filters, sg_stream_t stream) {
   ChainArgs a{};
   int rc = fill_args(a, c);
   if (rc) return rc;
   if (c->B <= 0) return 0;
-  SG_RETURN_IF(probs.ptr == nullptr || targets == nullptr || rowsum == nullptr || grad_loss == nullptr,
+  SG_RETURN_IF(picked == nullptr || targets == nullptr || rowsum == nullptr || grad_loss == nullptr,
                cudaErrorInvalidValue);
   a.g_out = nullptr;
-  a.nll_p = probs.ptr;
-  a.nll_sr = probs.stride_row;
-  a.nll_sb = probs.stride_b;
+  a.nll_pt = picked;
   a.nll_t = targets;
   a.nll_rowsum = rowsum;
   a.nll_gloss = grad_loss;

@@ -1081,7 +1081,8 @@ __global__ void __launch_bounds__(256) k_nll_fwd(const Rows p, int n, int64_t B,
 __global__ void __launch_bounds__(256) k_nll_fwd_given(const Rows p, int n, int64_t B,
                                                        const int64_t* __restrict__ targets,
                                                        const double* __restrict__ rowsum, double* __restrict__ loss,
-                                                       double* __restrict__ blocks, unsigned* __restrict__ counter) {
+                                                       double* __restrict__ blocks, unsigned* __restrict__ counter,
+                                                       double* __restrict__ picked) {
   const int64_t b0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   pdl_wait();
   double v = 0.0;
@@ -1090,6 +1091,7 @@ __global__ void __launch_bounds__(256) k_nll_fwd_given(const Rows p, int n, int6
     const bool bad = nll_bad_target(t, n);
     const double pt = t >= 0 && !bad ? (double)p.ld(t, b0) : 0.0;
     v = bad ? __longlong_as_double(0x7ff8000000000000LL) : log(nll_picked(__ldg(rowsum + b0), pt, t));
+    if (picked != nullptr) picked[b0] = pt;  // p[t_b][b] for a fused backward (sg_chain_bwd_nll)
   }
   nll_finish(v, loss, blocks, counter, B);
 }
@@ -1386,12 +1388,11 @@ int sg_nll_fwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, doub
 }
 
 int sg_nll_fwd_rowsum(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, const double* rowsum,
-                      double* loss, void* scratch, sg_stream_t stream) {
+                      double* loss, void* scratch, double* picked, sg_stream_t stream) {
   if (B <= 0) return 0;
   double* base = (double*)scratch;
   return (int)launch(k_nll_fwd_given, dim3(ceil_div(B, 256)), dim3(256), 0, (cudaStream_t)stream, rows_of(probs),
-                     (int)n, B,
-                     targets, rowsum, loss, base + 2, (unsigned*)base);
+                     (int)n, B, targets, rowsum, loss, base + 2, (unsigned*)base, picked);
 }
 
 int sg_nll_bwd(sg_rows probs, int64_t n, int64_t B, const int64_t* targets, const double* grad_loss,

@@ -393,17 +393,18 @@ class ChainNllLoss(torch.autograd.Function):
         dev = probs_nb.device
         loss = torch.empty((), device=dev, dtype=torch.float64)
         scratch = _nll_scratch(dev, n, B)
+        picked = torch.empty((B,), device=dev, dtype=torch.float64)
         rc = _lib().sg_nll_fwd_rowsum(N.rows(probs_nb), n, B, targets.data_ptr(), rowsum.data_ptr(), loss.data_ptr(),
-                                      scratch.data_ptr(), N.stream_ptr(dev))
+                                      scratch.data_ptr(), picked.data_ptr(), N.stream_ptr(dev))
         N.check(rc, "sg_nll_fwd_rowsum")
-        _ledger("nll_fwd", 4 * B + 16 * B, B * n)
+        _ledger("nll_fwd", 4 * B + 24 * B, B * n)
         ctx.meta = (n0, kf, B)
-        ctx.save_for_backward(probs_nb, targets, rowsum, base, states, *filters)
+        ctx.save_for_backward(targets, rowsum, picked, base, states, *filters)
         return loss
 
     @staticmethod
     def backward(ctx, gloss):
-        probs_nb, targets, rowsum, base, states, *filters = ctx.saved_tensors
+        targets, rowsum, picked, base, states, *filters = ctx.saved_tensors
         n0, kf, B = ctx.meta
         g = gloss.detach().to(torch.float64).reshape(()).contiguous()
         gbase = torch.empty_like(base)
@@ -413,7 +414,7 @@ class ChainNllLoss(torch.autograd.Function):
         for i, t in enumerate(gfilt):
             arr[i] = N.rows(t)
         with launch_timer("chain_bwd"):
-            rc = _lib().sg_chain_bwd_nll(ctypes.byref(c), N.rows(probs_nb), targets.data_ptr(), rowsum.data_ptr(),
+            rc = _lib().sg_chain_bwd_nll(ctypes.byref(c), targets.data_ptr(), rowsum.data_ptr(), picked.data_ptr(),
                                          g.data_ptr(), N.rows(gbase), arr, N.stream_ptr(g.device))
         N.check(rc, "sg_chain_bwd_nll")
         m = len(filters)
@@ -559,7 +560,7 @@ class NllLoss(torch.autograd.Function):
         rowsum = known_rowsum(probs_nb)
         if rowsum is not None:  # a fused chain forward already summed these rows
             rc = _lib().sg_nll_fwd_rowsum(N.rows(probs_nb), n, B, targets.data_ptr(), rowsum.data_ptr(),
-                                          loss.data_ptr(), scratch.data_ptr(), N.stream_ptr(dev))
+                                          loss.data_ptr(), scratch.data_ptr(), None, N.stream_ptr(dev))
             N.check(rc, "sg_nll_fwd_rowsum")
         else:
             rowsum = torch.empty((B,), device=dev, dtype=torch.float64)
