@@ -541,11 +541,20 @@ __global__ void __launch_bounds__(32) k_chain_bwd(const ChainArgs a) {
         cm[h] = -pt / (den * den);
         inv[h] = 1.0 / den;
       }
+      // every row but the target's is (float)(cf * (0.0 + cm)) = (float)(cf * cm); the
+      // target row is (float)(cf * (inv + cm)) — the same two values k_nll_bwd stores
+      float gb[2], gs[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const bool live = L.nv > h;
+        gb[h] = live ? (float)(cf[h] * cm[h]) : 0.f;
+        gs[h] = live ? (float)(cf[h] * (inv[h] + cm[h])) : 0.f;
+      }
       for (int r = L.g; r < grows; r += kCG) {
         float2 v = zero2();
         if (r < nm) {
-          v.x = L.nv > 0 ? (float)(cf[0] * ((r == tt[0] ? inv[0] : 0.0) + cm[0])) : 0.f;
-          v.y = L.nv > 1 ? (float)(cf[1] * ((r == tt[1] ? inv[1] : 0.0) + cm[1])) : 0.f;
+          v.x = r == tt[0] ? gs[0] : gb[0];
+          v.y = r == tt[1] ? gs[1] : gb[1];
         }
         G[r * kCP + L.c] = v;
       }
