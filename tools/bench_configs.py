@@ -138,7 +138,7 @@ def graphed_e2e(step_fn, dev_inputs, host_inputs, dev, iters):
         out = g(*views)
         r = out[0] if isinstance(out, (tuple, list)) else out
         if r.numel() == 1:
-            return float(r)
+            return float(r.detach())
         if "host" not in res:  # the step's (B, n) result goes back to the host
             res["host"] = torch.empty(r.shape, dtype=r.dtype).pin_memory()
         res["host"].copy_(r.detach(), non_blocking=True)
