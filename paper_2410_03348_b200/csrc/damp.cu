@@ -789,6 +789,167 @@ __global__ void __launch_bounds__(128) k_convs_bwd(const Rows g, int n_out, cons
   cs_unstage(sdS, dS, KF, B, b0);
 }
 
+// ------------------------------- sample-pair short Toeplitz -------------------------
+// Both lists short (the sweep's arity-2 |S| = 10, Sum-2): lane = one sample PAIR, the
+// whole rows of both samples in registers, every multiply-add a packed FFMA2 (two IEEE
+// FMAs, identical rounding), no shared memory and no index records.  A user (B, n)
+// block read in place is one contiguous 8n-byte span per pair, loaded as n 8-byte vectors
+// (half the instructions and 2x fewer L1 wavefronts per sample than per-row loads of
+// strided samples); symbol-major rows load as one float2 per pair (coalesced).  The
+// upstream gradient is read in either layout (no transposing copy before the backward)
+// and the gradients are stored in the operands' own layouts.  Forward FMA order is
+// k_conv_fwd's (bit-identical outputs).
+constexpr int kCpMax = 16;  // longest operand list on this path (n_out <= 2 kCpMax - 1)
+
+// v[r] = (X[r][b], X[r][b + 1]) for r < n, 0 past n and for a missing second sample
+template <int N>
+__device__ __forceinline__ void cp_load(float2 (&v)[N], const Rows& X, int n, int64_t b, bool two) {
+#pragma unroll
+  for (int r = 0; r < N; ++r) v[r] = make_float2(0.f, 0.f);
+  const float* q = X.p + b * X.sb;
+  if (X.sr == 1 && X.sb == n && two && (n & 1) == 0 && ((uintptr_t)q & 7) == 0) {
+    // each sample's row is n contiguous floats at an 8-byte boundary: n / 2 float2 each
+    const float2* q0 = reinterpret_cast<const float2*>(q);
+    const float2* q1 = reinterpret_cast<const float2*>(q + n);
+#pragma unroll
+    for (int u = 0; u < N / 2; ++u) {
+      if (2 * u < n) {
+        const float2 a0 = __ldg(q0 + u), a1 = __ldg(q1 + u);
+        v[2 * u] = make_float2(a0.x, a1.x);
+        v[2 * u + 1] = make_float2(a0.y, a1.y);
+      }
+    }
+    return;
+  }
+  if (X.sb == 1 && two && ((uintptr_t)q & 7) == 0) {  // symbol-major rows: one float2 per row
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+      if (r < n) v[r] = __ldg(reinterpret_cast<const float2*>(q + (int64_t)r * X.sr));
+    return;
+  }
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+    if (r < n) v[r] = make_float2(X.ld(r, b), two ? X.ld(r, b + 1) : 0.f);
+}
+
+// rows r < n of v -> Y[r][b], Y[r][b + 1] (the second only when `two`)
+template <int N>
+__device__ __forceinline__ void cp_store(const WRows& Y, int n, int64_t b, bool two, const float2 (&v)[N]) {
+  float* q = Y.p + b * Y.sb;
+  if (Y.sr == 1 && Y.sb == n && two && (n & 1) == 0 && ((uintptr_t)q & 7) == 0) {
+    float2* q0 = reinterpret_cast<float2*>(q);
+    float2* q1 = reinterpret_cast<float2*>(q + n);
+#pragma unroll
+    for (int u = 0; u < N / 2; ++u) {
+      if (2 * u < n) {
+        q0[u] = make_float2(v[2 * u].x, v[2 * u + 1].x);
+        q1[u] = make_float2(v[2 * u].y, v[2 * u + 1].y);
+      }
+    }
+    return;
+  }
+  if (Y.sb == 1 && two && ((uintptr_t)q & 7) == 0) {
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+      if (r < n) *reinterpret_cast<float2*>(q + (int64_t)r * Y.sr) = v[r];
+    return;
+  }
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    if (r < n) {
+      Y.st(r, b, v[r].x);
+      if (two) Y.st(r, b + 1, v[r].y);
+    }
+  }
+}
+
+template <int KF>
+__global__ void __launch_bounds__(128) k_convp_fwd(const Rows L, int nL, const Rows S, float* __restrict__ out,
+                                                   int n_out, int64_t B) {
+  const int64_t pr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t b = 2 * pr;
+  pdl_wait();
+  if (b >= B) return;
+  const bool two = b + 1 < B;
+  float2 l[kCpMax], f[KF];
+  cp_load<kCpMax>(l, L, nL, b, two);
+  {
+    float2 ft[KF];
+    cp_load<KF>(ft, S, KF, b, two);
+#pragma unroll
+    for (int j = 0; j < KF; ++j) f[j] = ft[j];
+  }
+  pdl_trigger();
+#pragma unroll
+  for (int o = 0; o < kCpMax + KF - 1; ++o) {
+    if (o < n_out) {
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < KF; ++j)  // k_conv_fwd's order: j ascending from 0
+        if (o - j >= 0 && o - j < kCpMax && o - j < nL) acc = __ffma2_rn(l[o - j < kCpMax ? o - j : 0], f[j], acc);
+      const float2 v = make_float2(clamp01(acc.x), clamp01(acc.y));
+      if (two && ((B & 1) == 0)) {
+        *reinterpret_cast<float2*>(out + (size_t)o * B + b) = v;
+      } else {
+        out[(size_t)o * B + b] = v.x;
+        if (two) out[(size_t)o * B + b + 1] = v.y;
+      }
+    }
+  }
+}
+
+// dL[s] = sum_j g[s + j] S[j] (j ascending);  dS[j] = sum_s g[s + j] L[s] (s ascending)
+template <int KF>
+__global__ void __launch_bounds__(128) k_convp_bwd(const Rows g, int n_out, const Rows L, int nL, const Rows S,
+                                                   WRows dL, WRows dS, int64_t B) {
+  const int64_t pr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t b = 2 * pr;
+  pdl_wait();
+  if (b >= B) return;
+  const bool two = b + 1 < B;
+  constexpr int NO = kCpMax + KF - 1;
+  float2 gv[NO], l[kCpMax], f[KF];
+  cp_load<NO>(gv, g, n_out, b, two);
+  cp_load<kCpMax>(l, L, nL, b, two);
+  cp_load<KF>(f, S, KF, b, two);
+  pdl_trigger();
+  float2 dl[kCpMax], ds[KF];
+#pragma unroll
+  for (int s0 = 0; s0 < kCpMax; ++s0) {
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < KF; ++j) acc = __ffma2_rn(gv[s0 + j], f[j], acc);
+    dl[s0] = acc;
+  }
+#pragma unroll
+  for (int j = 0; j < KF; ++j) {
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int s0 = 0; s0 < kCpMax; ++s0)
+      if (s0 < nL) acc = __ffma2_rn(gv[s0 + j], l[s0], acc);
+    ds[j] = acc;
+  }
+  cp_store<kCpMax>(dL, nL, b, two, dl);
+  cp_store<KF>(dS, KF, b, two, ds);
+}
+
+static bool convp_fits(int kf, int nL) { return kf <= kCpMax && nL <= kCpMax; }
+
+template <int KF>
+static int convp_fwd_t(const Rows& L, int nL, const Rows& S, float* out, int n_out, int64_t B, cudaStream_t st) {
+  const int64_t pairs = (B + 1) / 2;
+  return (int)launch(k_convp_fwd<KF>, dim3((unsigned)ceil_div(pairs, 128)), dim3(128), 0, st, L, nL, S, out, n_out,
+                     B);
+}
+
+template <int KF>
+static int convp_bwd_t(const Rows& g, int n_out, const Rows& L, int nL, const Rows& S, const WRows& dL,
+                       const WRows& dS, int64_t B, cudaStream_t st) {
+  const int64_t pairs = (B + 1) / 2;
+  return (int)launch(k_convp_bwd<KF>, dim3((unsigned)ceil_div(pairs, 128)), dim3(128), 0, st, g, n_out, L, nL, S, dL,
+                     dS, B);
+}
+
 static size_t convs_fwd_smem(int kf, int n_out) {
   return (size_t)(kf + kf - 1 + ceil_div(n_out, kCsRows) * kCsRows + kCsRows) * kCsPitch * sizeof(float);
 }
@@ -907,6 +1068,15 @@ static bool conv_staged(int kf, int nL, int n_out) {
 }
 
 static int conv_fwd(int kf, const Rows& L, int nL, const Rows& S, float* out, int n_out, int64_t B, cudaStream_t st) {
+  if (convp_fits(kf, nL)) {
+    switch (kf) {
+#define X(K) \
+  case K: return convp_fwd_t<K>(L, nL, S, out, n_out, B, st);
+      SG_CONV_CASES(X)
+#undef X
+      default: return (int)cudaErrorInvalidValue;
+    }
+  }
   const bool staged = conv_staged(kf, nL, n_out);
   switch (kf) {
 #define X(K) \
@@ -920,6 +1090,15 @@ static int conv_fwd(int kf, const Rows& L, int nL, const Rows& S, float* out, in
 // g: the staged kernel reads any layout; the unstaged one needs contiguous [n_out][B]
 static int conv_bwd(int kf, const Rows& g, int n_out, const Rows& L, int nL, const Rows& S, const WRows& dL,
                     const WRows& dS, int64_t B, cudaStream_t st) {
+  if (convp_fits(kf, nL)) {
+    switch (kf) {
+#define X(K) \
+  case K: return convp_bwd_t<K>(g, n_out, L, nL, S, dL, dS, B, st);
+      SG_CONV_CASES(X)
+#undef X
+      default: return (int)cudaErrorInvalidValue;
+    }
+  }
   if (conv_staged(kf, nL, n_out)) {
     switch (kf) {
 #define X(K) \
@@ -1354,7 +1533,7 @@ int sg_damp_rows_add(const sg_rows A, const int32_t* ia, const sg_rows Bm, const
 }
 
 int32_t sg_damp_conv_staged(int32_t kf, int32_t n_long, int32_t n_out) {
-  return conv_staged(kf, n_long, n_out) ? 1 : 0;
+  return (convp_fits(kf, n_long) || conv_staged(kf, n_long, n_out)) ? 1 : 0;
 }
 
 int64_t sg_nll_scratch_bytes(int64_t n, int64_t B) {
