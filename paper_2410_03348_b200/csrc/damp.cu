@@ -821,7 +821,7 @@ __device__ __forceinline__ void cp_load(float2 (&v)[N], const Rows& X, int n, in
     }
     return;
   }
-  if (X.sb == 1 && two && ((uintptr_t)q & 7) == 0) {  // symbol-major rows: one float2 per row
+  if (X.sb == 1 && two && (X.sr & 1) == 0 && ((uintptr_t)q & 7) == 0) {  // symbol-major rows: one float2 each
 #pragma unroll
     for (int r = 0; r < N; ++r)
       if (r < n) v[r] = __ldg(reinterpret_cast<const float2*>(q + (int64_t)r * X.sr));
@@ -848,7 +848,7 @@ __device__ __forceinline__ void cp_store(const WRows& Y, int n, int64_t b, bool 
     }
     return;
   }
-  if (Y.sb == 1 && two && ((uintptr_t)q & 7) == 0) {
+  if (Y.sb == 1 && two && (Y.sr & 1) == 0 && ((uintptr_t)q & 7) == 0) {
 #pragma unroll
     for (int r = 0; r < N; ++r)
       if (r < n) *reinterpret_cast<float2*>(q + (int64_t)r * Y.sr) = v[r];
