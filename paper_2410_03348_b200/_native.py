@@ -16,7 +16,8 @@ from pathlib import Path
 import torch
 
 MAX_ARITY = 8
-LIB_PATH = Path(__file__).resolve().parent / "libsgb200.so"
+# SGB200_LIB: an alternative build of the same library (A/B measurements, tools/ab_build.py)
+LIB_PATH = Path(os.environ.get("SGB200_LIB") or Path(__file__).resolve().parent / "libsgb200.so")
 
 
 class NativeError(RuntimeError):

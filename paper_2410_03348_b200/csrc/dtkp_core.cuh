@@ -20,6 +20,9 @@
 #ifndef SG_DTKP_FUSED_MINB  // resident CTAs/SM asked of the fused conj -> group_disj (K <= 3)
 #define SG_DTKP_FUSED_MINB 5
 #endif
+#ifndef SG_DTKP_CONJ3_MINB  // resident CTAs/SM asked of the binary conj at K = 3
+#define SG_DTKP_CONJ3_MINB 6
+#endif
 #ifndef SG_DTKP_UNROLL_K
 #define SG_DTKP_UNROLL_K 4
 #endif
@@ -140,9 +143,12 @@ __device__ __forceinline__ PCol stage_pcol(void* tile, const float* __restrict__
 // Set bits are consumed four at a time: the four shared-memory loads are issued together
 // and the products are taken in ascending order; missing slots multiply by 1.0, which is
 // exact in IEEE arithmetic, so the result is bit-identical to the one-bit-at-a-time loop.
+// `start` continues a product: proof_key(b, pc, proof_key(a, pc)) == proof_key(a | b, pc)
+// bit for bit when every member of a precedes every member of b (the fold is the same
+// sequence of multiplies).
 template <int WT>
-__device__ __forceinline__ double proof_key(const uint64_t (&mm)[WT], const PCol& pc) {
-  double prod = 1.0;
+__device__ __forceinline__ double proof_key(const uint64_t (&mm)[WT], const PCol& pc, double start = 1.0) {
+  double prod = start;
 #pragma unroll
   for (int w = 0; w < WT; ++w) {
     uint64_t x = mm[w];
@@ -266,6 +272,88 @@ __device__ __forceinline__ void conj_into(TopK<K, WT>& T, const TagRows<K, WT>& 
 #pragma unroll
       for (int w = 0; w < WT; ++w) mm[w] |= ma[w];
       T.insert(mm, proof_key<WT>(mm, pc), 0);
+    }
+  }
+}
+
+// Highest / lowest member column of a proof row (-1 / INT_MAX when it has none).
+template <int WT>
+__device__ __forceinline__ int hi_col(const uint64_t (&m)[WT]) {
+  int h = -1;
+#pragma unroll
+  for (int w = 0; w < WT; ++w)
+    if (m[w]) h = w * 64 + 63 - __clzll((long long)m[w]);
+  return h;
+}
+template <int WT>
+__device__ __forceinline__ int lo_col(const uint64_t (&m)[WT]) {
+  int l = 0x7fffffff;
+#pragma unroll
+  for (int w = WT - 1; w >= 0; --w)
+    if (m[w]) l = w * 64 + __ffsll((long long)m[w]) - 1;
+  return l;
+}
+template <int WT>
+__device__ __forceinline__ bool one_member(const uint64_t (&m)[WT]) {
+  int c = 0;
+#pragma unroll
+  for (int w = 0; w < WT; ++w) c += __popcll(m[w]);
+  return c == 1;
+}
+
+// Keys of the K rows of a left conj operand (0 for absent rows), computed once per loaded
+// tag and reused by every record of an item that conjoins the same left row.
+template <int K>
+struct RowKeys {
+  double k[K];
+  __device__ __forceinline__ double at(int q) const {
+    double v = k[0];
+#pragma unroll
+    for (int i = 1; i < K; ++i)
+      if (i == q) v = k[i];
+    return v;
+  }
+  template <int WT>
+  __device__ __forceinline__ void compute(const TagRows<K, WT>& A, const PCol& pc) {
+#pragma unroll
+    for (int q = 0; q < K; ++q) k[q] = ((A.pres >> q) & 1u) ? proof_key<WT>(A.m[q], pc) : 0.0;
+  }
+};
+
+#ifndef SG_DTKP_KEY_CONT  // 0: every conj candidate's key is a full product (A/B tests)
+#define SG_DTKP_KEY_CONT 1
+#endif
+
+// conj_into with the left rows' keys known (AK): a candidate whose right row's members all
+// follow the left row's (the usual case when a prefix is extended by a later input) takes
+// its key as the continuation of the left key — ONE multiply for a single-member right row —
+// bit-identical to the full ascending product (proof_key); any other candidate falls back
+// to the full product.  Same candidate order, same inserts as conj_into.
+template <int K, int WT>
+__device__ __forceinline__ void conj_keyed(TopK<K, WT>& T, const TagRows<K, WT>& A, const RowKeys<K>& AK,
+                                           const TagRows<K, WT>& Bt, const PCol& pc) {
+  constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
+#pragma unroll (kUnrollK)
+  for (int qa = 0; qa < K; ++qa) {
+    if (!((A.pres >> qa) & 1u)) continue;
+    uint64_t ma[WT];
+    A.row(qa, ma);
+    const double ka = AK.at(qa);
+    const int ha = hi_col<WT>(ma);
+#pragma unroll (kUnrollK)
+    for (int qb = 0; qb < K; ++qb) {
+      if (!((Bt.pres >> qb) & 1u)) continue;
+      uint64_t mb[WT], mm[WT];
+      Bt.row(qb, mb);
+#pragma unroll
+      for (int w = 0; w < WT; ++w) mm[w] = mb[w] | ma[w];
+      const int lb = lo_col<WT>(mb);
+      double kk;
+      if (ha < lb)
+        kk = one_member<WT>(mb) ? ka * pc(lb) : proof_key<WT>(mb, pc, ka);
+      else
+        kk = proof_key<WT>(mm, pc);
+      T.insert(mm, kk, 0);
     }
   }
 }
@@ -418,23 +506,43 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
     // next record's rows held in registers only while K is small (their registers cost
     // occupancy); otherwise loaded after the current record
     constexpr bool kPf = K <= SG_DTKP_CONJ_PREFETCH_MAXK;
+    // the left rows' keys, valid while consecutive records conjoin the same left row
+    // (records are grouped by output symbol, and e.g. a prefix extended by every symbol of
+    // the next input yields a run of records with one left row)
+    // (K <= 3 only: at K = 5 the key registers spill and CLUTRR-style closures, whose
+    // columns interleave, lose 9%)
+    constexpr bool kCont = SG_DTKP_KEY_CONT && K <= 3;
+    RowKeys<K> AK;
+    bool ak_ok = false;
     for (int c = item.y; c < item.z; ++c) {
       const bool more = c + 1 < item.z;
       const int rna = ran, rnb = rbn;
+      const bool same_a = kCont && (rna & kRowMask) == (wa & kRowMask);
       if (kPf && more) {
-        An.load(a.ops[0], a.B, b, rna & kRowMask);
+        if (!same_a) An.load(a.ops[0], a.B, b, rna & kRowMask);
         Bn.load(a.ops[1], a.B, b, rnb);
       }
       if (c + 2 < item.z) {
         ran = rec_row(a, c + 2, 0);
         rbn = rec_row(a, c + 2, 1);
       }
+      if (kCont && !ak_ok) {
+        AK.compute<WT>(A, pc);
+        ak_ok = true;
+      }
       if constexpr (AR == 2) {
-        conj_into<K, WT>(S, A, Bt, pc);  // exact: see conj_into
+        // exact: see conj_into / conj_keyed
+        if (kCont)
+          conj_keyed<K, WT>(S, A, AK, Bt, pc);
+        else
+          conj_into<K, WT>(S, A, Bt, pc);
       } else {
         TopK<K, WT> T;
         T.clear();
-        conj_into<K, WT>(T, A, Bt, pc);
+        if (kCont)
+          conj_keyed<K, WT>(T, A, AK, Bt, pc);
+        else
+          conj_into<K, WT>(T, A, Bt, pc);
 #pragma unroll 1
         for (int i = 2; i < a.arity; ++i) {
           TagRows<K, WT> Ci;
@@ -465,12 +573,13 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
       if (more) {
         wa = rna;
         if constexpr (kPf) {
-          A = An;
+          if (!same_a) A = An;
           Bt = Bn;
         } else {
-          A.load(a.ops[0], a.B, b, rna & kRowMask);
+          if (!same_a) A.load(a.ops[0], a.B, b, rna & kRowMask);
           Bt.load(a.ops[1], a.B, b, rnb);
         }
+        if (!same_a) ak_ok = false;
       }
     }
   }
@@ -489,7 +598,7 @@ __host__ __device__ constexpr int dtkp_min_blocks(int K, int WT, int AR) {
   // per-combo top-k set): 6 / 4 CTAs per SM at K <= 3 / K <= 5 without spills
   return SG_DTKP_MINB > 0 ? SG_DTKP_MINB
          : (WT <= 2 && K <= 3) ? (AR == 1 ? (SG_DTKP_STREAM_PREFETCH ? 5 : 6)
-                                  : AR == 2 ? (K > SG_DTKP_CONJ_PREFETCH_MAXK ? 6 : 4)
+                                  : AR == 2 ? (K > SG_DTKP_CONJ_PREFETCH_MAXK ? SG_DTKP_CONJ3_MINB : 4)
                                   : AR == 3 ? SG_DTKP_FUSED_MINB : 1)
          : (WT <= 2 && K <= 5 && AR == 1) ? 5
          : (WT <= 2 && K <= 5 && AR == 2 && K > SG_DTKP_CONJ_PREFETCH_MAXK) ? 4

@@ -65,25 +65,37 @@ __device__ __forceinline__ void maxrec(float& best, int& arg, float v, int j, bo
   }
 }
 
-// Forward: column V (stride 32 floats) holds KF-1 zero rows, then the state; in place.
-template <int KF>
+// Forward.  P lanes share one sample (SPW = 32 / P samples per warp): the state of sample
+// c ping-pongs between two shared columns (stride SPW floats, KF-1 zero rows in front), and
+// the lanes of a sample take the step's output groups of four round-robin, so a step's
+// dependent compare/select chains are split P ways (the kernel is bound by them: one warp
+// per scheduler at P = 1); one __syncwarp per step.  Each output is computed exactly as
+// before (same records, same order, same first-maximal rule), so P does not change a bit.
+template <int KF, int P>
 __global__ void __launch_bounds__(32) k_maxchain_fwd(const MaxChainArgs a) {
   extern __shared__ float mcs[];
+  constexpr int SPW = 32 / P;
+  constexpr int PAD = KF - 1;
   const int lane = threadIdx.x;
-  const int64_t b0 = (int64_t)blockIdx.x * 32 + lane;
+  const int c = lane % SPW, h = lane / SPW;
+  const int64_t b0 = (int64_t)blockIdx.x * SPW + c;
   const bool bval = b0 < a.B;
   const int64_t b = bval ? b0 : a.B - 1;
-  constexpr int PAD = KF - 1;
-  float* V = mcs + lane;  // row r at V[(PAD + r) * 32]
+  const int rows = PAD + a.n_max;
+  float* const VA = mcs + c;  // buffer 0 of sample c: row r at VA[r * SPW]; buffer 1 after it
+  float* const VB = VA + (size_t)rows * SPW;
   mc_pdl_wait();
-#pragma unroll
-  for (int r = 0; r < PAD; ++r) V[r * 32] = 0.f;
-#pragma unroll 8
-  for (int r = 0; r < a.n[0]; ++r) V[(PAD + r) * 32] = a.base.ld(r, b);
-  double rs = 0.0;
+  for (int r = h; r < PAD; r += P) {
+    VA[r * SPW] = 0.f;
+    VB[r * SPW] = 0.f;
+  }
+  for (int r = h; r < a.n[0]; r += P) VA[(PAD + r) * SPW] = a.base.ld(r, b);
   float fn[KF];  // the next step's filter, loaded one step ahead
 #pragma unroll
   for (int j = 0; j < KF; ++j) fn[j] = a.filt[0].ld(j, b);
+  // argmax bytes: [32-sample block][word][32 lanes], byte (o & 3) of word o >> 2
+  uint8_t* const am = reinterpret_cast<uint8_t*>(a.argmax + (size_t)(b0 >> 5) * a.arg_words * 32 + (b0 & 31));
+  __syncwarp();
   for (int i = 1; i <= a.m; ++i) {
     float f[KF];
 #pragma unroll
@@ -94,16 +106,17 @@ __global__ void __launch_bounds__(32) k_maxchain_fwd(const MaxChainArgs a) {
     }
     const int nin = a.n[i - 1], nout = a.n[i];
     const bool last = i == a.m;
+    const float* Vin = (i & 1) ? VA : VB;
+    float* Vout = (i & 1) ? VB : VA;
     float* gst = last ? a.out : a.states + (size_t)a.state_off[i] * a.B;
-    // byte (o & 3) of the lane's word o >> 2 of this step (packed layout, see the header)
-    uint8_t* gam = reinterpret_cast<uint8_t*>(a.argmax + ((size_t)blockIdx.x * a.arg_words + a.arg_off[i]) * 32 + lane);
-    // outputs descending in groups of 4 (o0 - 3 .. o0): one window of KF + 3 rows
-    for (int o0 = nout - 1; o0 >= 0; o0 -= 4) {
+    uint8_t* gam = am + (size_t)a.arg_off[i] * 128;
+    // output groups o0 - 3 .. o0 (o0 = nout - 1 - 4 gi), one window of KF + 3 rows each
+    for (int o0 = nout - 1 - 4 * h; o0 >= 0; o0 -= 4 * P) {
       float w[KF + 3];
 #pragma unroll
       for (int u = 0; u < KF + 3; ++u) {
         const int s = o0 - 3 - PAD + u;  // s >= -PAD - 3; rows < -PAD read as 0 (masked below)
-        w[u] = s >= -PAD ? V[(PAD + s) * 32] : 0.f;
+        w[u] = s >= -PAD ? Vin[(PAD + s) * SPW] : 0.f;
       }
       float best[4];
       int arg[4];
@@ -126,18 +139,37 @@ __global__ void __launch_bounds__(32) k_maxchain_fwd(const MaxChainArgs a) {
         const int o = o0 - q;
         if (o < 0) break;
         const float v = clamp01(best[q]);  // every output of a Toeplitz step has a record
-        V[(PAD + o) * 32] = v;
-        if (bval) gst[(size_t)o * a.B + b0] = v;
-        gam[(size_t)(o >> 2) * 128 + (o & 3)] = (uint8_t)arg[q];
-        if (last) rs += (double)v;
+        Vout[(PAD + o) * SPW] = v;
+        if (bval) {
+          gst[(size_t)o * a.B + b0] = v;
+          gam[(size_t)(o >> 2) * 128 + (o & 3) * 1] = (uint8_t)arg[q];
+        }
       }
     }
+    __syncwarp();
   }
-  if (a.rowsum != nullptr && bval) a.rowsum[b0] = rs;
+  if (a.rowsum != nullptr && bval && h == 0) {
+    // outputs descending, as the one-lane-per-sample forward summed them
+    const float* Vl = (a.m & 1) ? VB : VA;
+    double rs = 0.0;
+    for (int o = a.n[a.m] - 1; o >= 0; --o) rs += (double)Vl[(PAD + o) * SPW];
+    a.rowsum[b0] = rs;
+  }
 }
 
-// Backward.  Columns: G (current upstream gradient, n_max rows), H (the next one),
-// Vp (v_{i-1}).
+__device__ __forceinline__ void mc_cp4(float* dst, const float* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void mc_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void mc_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Backward.  Columns: G (the upstream gradient, updated IN PLACE into the next one) and
+// V[2] (v_{i-1} of the current step and, arriving through cp.async while this step runs,
+// v_{i-2} of the next).  In place: output o is read at iteration o and its slot restarts
+// as the accumulator of input row o (every contribution to input row s comes from an
+// output o >= s, o ascending), so the new gradient never overwrites an unread one.
 template <int KF>
 __global__ void __launch_bounds__(32) k_maxchain_bwd(const MaxChainArgs a) {
   extern __shared__ float mcs[];
@@ -146,22 +178,38 @@ __global__ void __launch_bounds__(32) k_maxchain_bwd(const MaxChainArgs a) {
   const bool bval = b0 < a.B;
   const int64_t b = bval ? b0 : a.B - 1;
   float* G = mcs + lane;
-  float* H = G + (size_t)a.n_max * 32;
-  float* Vp = H + (size_t)a.n_max * 32;
+  float* const V0 = G + (size_t)a.n_max * 32;  // buffer t at V0 + t * col
+  const size_t col = (size_t)a.n_max * 32;
+  // v_{i-1} rows -> column Vd (i >= 1): the stored state, or the base operand for i = 1
+  auto stage_prev = [&](float* Vd, int i) {
+    const int nin = a.n[i - 1];
+    if (i > 1) {
+      const float* st = a.states + (size_t)a.state_off[i - 1] * a.B + b;
+      for (int s = 0; s < nin; ++s) mc_cp4(Vd + s * 32, st + (size_t)s * a.B);
+    } else {
+      for (int s = 0; s < nin; ++s) mc_cp4(Vd + s * 32, a.base.p + s * a.base.sr + b * a.base.sb);
+    }
+  };
   mc_pdl_wait();
-  for (int o0 = 0; o0 < a.n[a.m]; o0 += 32) {
-    float v[32];
-#pragma unroll
-    for (int u = 0; u < 32; ++u) v[u] = o0 + u < a.n[a.m] ? __ldg(a.g_out + (size_t)(o0 + u) * a.B + b) : 0.f;
-#pragma unroll
-    for (int u = 0; u < 32; ++u)
-      if (o0 + u < a.n[a.m]) G[(o0 + u) * 32] = v[u];
-  }
+  for (int o = 0; o < a.n[a.m]; ++o) mc_cp4(G + o * 32, a.g_out + (size_t)o * a.B + b);
+  stage_prev(V0, a.m);
+  mc_commit();
   float fn[KF];  // the next (lower) step's filter, loaded one step ahead
 #pragma unroll
   for (int j = 0; j < KF; ++j) fn[j] = a.filt[a.m - 1].ld(j, b);
+  // packed argmax taps, 32 outputs (8 words) per batch, loaded one batch ahead (across
+  // step boundaries too)
+  constexpr int kBatch = 32;
+  auto load_words = [&](uint32_t (&jw)[kBatch / 4], int i, int o0) {
+    const uint32_t* am = a.argmax + ((size_t)blockIdx.x * a.arg_words + a.arg_off[i]) * 32 + lane;
+#pragma unroll
+    for (int q = 0; q < kBatch / 4; ++q) jw[q] = o0 + 4 * q < a.n[i] ? __ldg(am + (size_t)((o0 >> 2) + q) * 32) : 0u;
+  };
+  uint32_t jn[kBatch / 4];
+  load_words(jn, a.m, 0);
   for (int i = a.m; i >= 1; --i) {
-    const int nin = a.n[i - 1], nout = a.n[i];
+    const int nout = a.n[i];
+    float* Vp = V0 + ((a.m - i) & 1) * col;
     float f[KF], dS[KF];
 #pragma unroll
     for (int j = 0; j < KF; ++j) {
@@ -171,44 +219,18 @@ __global__ void __launch_bounds__(32) k_maxchain_bwd(const MaxChainArgs a) {
     if (i > 1) {
 #pragma unroll
       for (int j = 0; j < KF; ++j) fn[j] = a.filt[i - 2].ld(j, b);
+      stage_prev(V0 + ((a.m - i + 1) & 1) * col, i - 1);  // the next step's v_{i-2}, in flight during this step
     }
-    // v_{i-1} into the lane's column, 32 independent loads in flight per lane (one warp
-    // per scheduler here: memory-level parallelism has to come from inside the warp); the
-    // step after's rows are prefetched into L2 (one 128-byte line = one row of the warp)
-    if (i > 1) {
-      const float* st = a.states + (size_t)a.state_off[i - 1] * a.B;
-      for (int s0 = 0; s0 < nin; s0 += 32) {
-        float v[32];
-#pragma unroll
-        for (int u = 0; u < 32; ++u) v[u] = s0 + u < nin ? __ldg(st + (size_t)(s0 + u) * a.B + b) : 0.f;
-#pragma unroll
-        for (int u = 0; u < 32; ++u)
-          if (s0 + u < nin) Vp[(s0 + u) * 32] = v[u];
-      }
-      if (i > 2) {
-        const float* nx = a.states + (size_t)a.state_off[i - 2] * a.B + (b0 - lane);
-        for (int r = lane; r < a.n[i - 2]; r += 32)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + (size_t)r * a.B));
-      }
-    } else {
-      for (int s0 = 0; s0 < nin; s0 += 32) {
-        float v[32];
-#pragma unroll
-        for (int u = 0; u < 32; ++u) v[u] = s0 + u < nin ? a.base.ld(s0 + u, b) : 0.f;
-#pragma unroll
-        for (int u = 0; u < 32; ++u)
-          if (s0 + u < nin) Vp[(s0 + u) * 32] = v[u];
-      }
-    }
-    for (int s = 0; s < nin; ++s) H[s * 32] = 0.f;
-    const uint32_t* am = a.argmax + ((size_t)blockIdx.x * a.arg_words + a.arg_off[i]) * 32 + lane;
-    // the packed argmax taps of 32 outputs (8 coalesced words) are loaded together, then
-    // the outputs are scattered in ascending order
-    constexpr int kBatch = 32;
+    mc_commit();
+    mc_wait<1>();  // this step's rows (and, at the top, G) have landed; the newest group may fly
     for (int o0 = 0; o0 < nout; o0 += kBatch) {
       uint32_t jw[kBatch / 4];
 #pragma unroll
-      for (int q = 0; q < kBatch / 4; ++q) jw[q] = o0 + 4 * q < nout ? __ldg(am + (size_t)((o0 >> 2) + q) * 32) : 0u;
+      for (int q = 0; q < kBatch / 4; ++q) jw[q] = jn[q];
+      if (o0 + kBatch < nout)
+        load_words(jn, i, o0 + kBatch);
+      else if (i > 1)
+        load_words(jn, i - 1, 0);
 #pragma unroll
       for (int q = 0; q < kBatch; ++q) {
         const int o = o0 + q;
@@ -216,10 +238,11 @@ __global__ void __launch_bounds__(32) k_maxchain_bwd(const MaxChainArgs a) {
         const int j = (int)((jw[q >> 2] >> (8 * (q & 3))) & 0xffu);  // byte (o & 3) of word o >> 2
         const int s = o - j;
         const float g = G[o * 32];
+        G[o * 32] = 0.f;  // slot o now accumulates input row o
         float fj = f[0];
 #pragma unroll
         for (int jj = 1; jj < KF; ++jj) fj = jj == j ? f[jj] : fj;
-        H[s * 32] = fmaf(g, fj, H[s * 32]);
+        G[s * 32] = fmaf(g, fj, G[s * 32]);
         const float vs = Vp[s * 32];
 #pragma unroll
         for (int jj = 0; jj < KF; ++jj) dS[jj] = jj == j ? fmaf(g, vs, dS[jj]) : dS[jj];
@@ -229,9 +252,6 @@ __global__ void __launch_bounds__(32) k_maxchain_bwd(const MaxChainArgs a) {
 #pragma unroll
       for (int j = 0; j < KF; ++j) a.dfilt_p[i - 1][j * a.dfilt_sr[i - 1] + b0 * a.dfilt_sb[i - 1]] = dS[j];
     }
-    float* t = G;
-    G = H;
-    H = t;
   }
   if (bval)
     for (int s = 0; s < a.n[0]; ++s) a.dbase_p[s * a.dbase_sr + b0 * a.dbase_sb] = G[s * 32];
@@ -261,11 +281,12 @@ static int mc_fill(MaxChainArgs& a, const sg_chain* c) {
 }
 
 template <typename... KArgs>
-static cudaError_t mc_launch(void (*kernel)(KArgs...), const MaxChainArgs& a, size_t smem, cudaStream_t st) {
+static cudaError_t mc_launch(void (*kernel)(KArgs...), const MaxChainArgs& a, size_t smem, cudaStream_t st,
+                             int spw = 32) {
   cudaError_t e = ensure_smem((const void*)kernel, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)ceil_div(a.B, 32));
+  cfg.gridDim = dim3((unsigned)ceil_div(a.B, spw));
   cfg.blockDim = dim3(32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -306,7 +327,7 @@ int64_t sg_maxchain_argmax_bytes(int32_t n0, int32_t kf, int32_t m, int64_t B) {
 
 int32_t sg_maxchain_max_rows(int32_t kf) {
   if (kf < 1 || kf > 16) return 0;
-  // backward: three columns of n_max rows x 32 lanes x 4 B within 227 KB
+  // backward: three columns (G, two v_{i-1} buffers) of n_max rows x 32 lanes x 4 B
   return (int32_t)(227 * 1024 / (3 * 32 * 4));
 }
 
@@ -320,11 +341,22 @@ int sg_maxchain_fwd(const sg_chain* c, float* out, double* rowsum, uint8_t* argm
   a.rowsum = rowsum;
   a.argmax = reinterpret_cast<uint32_t*>(argmax);
   SG_RETURN_IF(((uintptr_t)argmax & 3) != 0, cudaErrorInvalidValue);
-  const size_t smem = (size_t)(c->kf - 1 + a.n_max) * 32 * sizeof(float);
+  // lanes per sample: enough warps to give every scheduler ~4 of them (the forward is
+  // bound by its per-lane compare/select chains), P = 4 up to B ~ 19k
+  int P = 4;
+  if (const char* e = getenv("SG_MC_LANES")) P = atoi(e);
+  else if (c->B > 37888) P = 1;
+  else if (c->B > 18944) P = 2;
+  SG_RETURN_IF(P != 1 && P != 2 && P != 4, cudaErrorInvalidValue);
+  // two state columns per sample, 32 columns-per-buffer-pair per warp whatever P is
+  const size_t smem = (size_t)2 * (c->kf - 1 + a.n_max) * 32 * sizeof(float);
   cudaStream_t st = (cudaStream_t)stream;
   switch (c->kf) {
-#define X(K) \
-  case K: return (int)mc_launch(k_maxchain_fwd<K>, a, smem, st);
+#define X(K)                                                                               \
+  case K:                                                                                  \
+    return (int)(P == 4   ? mc_launch(k_maxchain_fwd<K, 4>, a, smem / 4, st, 8)            \
+                 : P == 2 ? mc_launch(k_maxchain_fwd<K, 2>, a, smem / 2, st, 16)           \
+                          : mc_launch(k_maxchain_fwd<K, 1>, a, smem, st, 32));
     SG_MC_CASES(X)
 #undef X
     default: return (int)cudaErrorInvalidValue;
