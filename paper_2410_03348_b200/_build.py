@@ -47,8 +47,10 @@ def _units():
     return units
 
 
-def _deps():
-    return sorted(CSRC.glob("*.cu*")) + sorted(INCLUDE.glob("*.h"))
+def _deps(src: Path = None):
+    """A unit depends on its own source and every header (a .cu never includes another)."""
+    heads = sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.glob("*.h"))
+    return heads + [src] if src is not None else sorted(CSRC.glob("*.cu")) + heads
 
 
 def _stale(target: Path, deps) -> bool:
@@ -65,7 +67,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     jobs = []
     for obj, src, extra in _units():
         out = BUILD / obj
-        if force or _stale(out, deps):
+        if force or _stale(out, _deps(src)):
             cmd = [nvcc, *ARCH, *NVCC_FLAGS, *os.environ.get("SG_NVCC_EXTRA", "").split(), f"-I{INCLUDE}", *extra,
                    "-c", str(src), "-o", str(out)]
             jobs.append((obj, cmd))

@@ -203,7 +203,8 @@ __global__ void __launch_bounds__(32) k_maxchain_bwd(const MaxChainArgs a) {
   auto load_words = [&](uint32_t (&jw)[kBatch / 4], int i, int o0) {
     const uint32_t* am = a.argmax + ((size_t)blockIdx.x * a.arg_words + a.arg_off[i]) * 32 + lane;
 #pragma unroll
-    for (int q = 0; q < kBatch / 4; ++q) jw[q] = o0 + 4 * q < a.n[i] ? __ldg(am + (size_t)((o0 >> 2) + q) * 32) : 0u;
+    for (int q = 0; q < kBatch / 4; ++q)  // lanes past B read tap 0 (their bytes are never written)
+      jw[q] = bval && o0 + 4 * q < a.n[i] ? __ldg(am + (size_t)((o0 >> 2) + q) * 32) : 0u;
   };
   uint32_t jn[kBatch / 4];
   load_words(jn, a.m, 0);
