@@ -37,7 +37,10 @@ def _units():
     """(object name, source, extra flags) for every translation unit."""
     units = [
         ("damp.o", CSRC / "damp.cu", []),
-        ("chain.o", CSRC / "chain.cu", []),
+        ("chain_g4.o", CSRC / "chain.cu", ["-DSG_CHAIN_GROUPS=4"]),
+        ("chain_g8.o", CSRC / "chain.cu", ["-DSG_CHAIN_GROUPS=8"]),
+        ("chain_g16.o", CSRC / "chain.cu", ["-DSG_CHAIN_GROUPS=16"]),
+        ("chain_api.o", CSRC / "chain_api.cu", []),
         ("dtkp.o", CSRC / "dtkp.cu", []),
         ("maxprod.o", CSRC / "maxprod.cu", []),
         ("maxchain.o", CSRC / "maxchain.cu", []),

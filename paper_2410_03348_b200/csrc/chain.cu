@@ -23,14 +23,26 @@
 // (72 B), which puts the four groups' tiles (R = 8 rows apart) on alternating bank halves:
 // a warp-wide LDS.64 costs the minimum two wavefronts.  Intermediate states go to HBM in a
 // warp-blocked layout ([warp][row][16 samples]: one 64-byte segment per group-row).
+//
+// Row groups per warp (SG_CHAIN_GROUPS = 4 / 8 / 16, this file is compiled once per value,
+// chain_api.cu picks one per launch from B): a warp owns 2 * 32 / G samples and each lane
+// R = 32 / G rows of a 32-row round.  G = 4 gives the fewest window loads per FFMA2 and is
+// best when the batch fills the GPU (B >= ~12k: 1024+ warps); smaller batches take more
+// groups — fewer samples per warp, more warps, a shorter per-warp dependent chain (the
+// kernels are latency-bound: at B = 2048 and G = 4 there are only 128 warps).
 #include "common.cuh"
 
-namespace sg {
-
-constexpr int kChainMaxSteps = 32;
 #ifndef SG_CHAIN_GROUPS
 #define SG_CHAIN_GROUPS 4
 #endif
+#define SG_CH_CAT2(a, b) a##b
+#define SG_CH_CAT(a, b) SG_CH_CAT2(a, b)
+#define SG_CHAIN_NS SG_CH_CAT(chain_g, SG_CHAIN_GROUPS)
+
+namespace sg {
+namespace SG_CHAIN_NS {
+
+constexpr int kChainMaxSteps = 32;
 constexpr int kCG = SG_CHAIN_GROUPS;  // row groups per warp
 constexpr int kCR = 32 / kCG;         // rows per group tile
 constexpr int kPairs = 32 / kCG;      // sample pairs per group (lanes per group)
@@ -665,24 +677,19 @@ static int fill_args(ChainArgs& a, const sg_chain* c) {
 
 #define SG_CHAIN_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
 
-}  // namespace sg
-
-using namespace sg;
-
-extern "C" {
-
-int64_t sg_chain_states_elems(int32_t n0, int32_t kf, int32_t m, int64_t B) {
+// Entry points of this variant (declared in chain_api.cu, which exports the C ABI).
+int64_t states_elems(int32_t n0, int32_t kf, int32_t m, int64_t B) {
   return (int64_t)state_rows(n0, kf, m) * (int64_t)ceil_div(B, kCWS) * kCWS;
 }
 
-int32_t sg_chain_max_rows(int32_t kf) {
+int32_t max_rows(int32_t kf) {
   if (kf < 1 || kf > 16) return 0;
   int n = 0;
   while (fwd_warp_bytes(kf, n + 1, kRing) <= kChainSmemMax && bwd_warp_bytes(kf, n + 1) <= kChainSmemMax) ++n;
   return n;
 }
 
-int sg_chain_fwd(const sg_chain* c, float* out, double* rowsum, sg_stream_t stream) {
+int fwd(const sg_chain* c, float* out, double* rowsum, sg_stream_t stream) {
   ChainArgs a{};
   int rc = fill_args(a, c);
   if (rc) return rc;
@@ -714,8 +721,8 @@ int sg_chain_fwd(const sg_chain* c, float* out, double* rowsum, sg_stream_t stre
 static int chain_bwd_impl(ChainArgs& a, const sg_chain* c, sg_rows grad_base, const sg_rows* grad_filters,
                           sg_stream_t stream);
 
-int sg_chain_bwd(const sg_chain* c, const float* grad_out, sg_rows grad_base, const sg_rows* grad_filters,
-                 sg_stream_t stream) {
+int bwd(const sg_chain* c, const float* grad_out, sg_rows grad_base, const sg_rows* grad_filters,
+        sg_stream_t stream) {
   ChainArgs a{};
   int rc = fill_args(a, c);
   if (rc) return rc;
@@ -725,8 +732,8 @@ int sg_chain_bwd(const sg_chain* c, const float* grad_out, sg_rows grad_base, co
   return chain_bwd_impl(a, c, grad_base, grad_filters, stream);
 }
 
-int sg_chain_bwd_nll(const sg_chain* c, const int64_t* targets, const double* rowsum, const double* picked,
-                     const double* grad_loss, sg_rows grad_base, const sg_rows* grad_filters, sg_stream_t stream) {
+int bwd_nll(const sg_chain* c, const int64_t* targets, const double* rowsum, const double* picked,
+            const double* grad_loss, sg_rows grad_base, const sg_rows* grad_filters, sg_stream_t stream) {
   ChainArgs a{};
   int rc = fill_args(a, c);
   if (rc) return rc;
@@ -766,4 +773,5 @@ static int chain_bwd_impl(ChainArgs& a, const sg_chain* c, sg_rows grad_base, co
   }
 }
 
-}  // extern "C"
+}  // namespace SG_CHAIN_NS
+}  // namespace sg
