@@ -112,6 +112,10 @@ __host__ __device__ inline int ptile_mode(int I) {
   return 0;
 }
 
+__host__ __device__ inline size_t ptile_bytes(int I) {
+  return (size_t)I * kWarp * (ptile_mode(I) == 2 ? sizeof(double) : sizeof(float));
+}
+
 __device__ __forceinline__ PCol stage_pcol(void* tile, const float* __restrict__ p, int I, int64_t B, int64_t b,
                                            int lane, int warp, int nwarps) {
   const bool dbl = ptile_mode(I) == 2;
@@ -301,59 +305,65 @@ __device__ __forceinline__ bool one_member(const uint64_t (&m)[WT]) {
   return c == 1;
 }
 
-// Keys of the K rows of a left conj operand (0 for absent rows), computed once per loaded
-// tag and reused by every record of an item that conjoins the same left row.
-template <int K>
-struct RowKeys {
-  double k[K];
-  __device__ __forceinline__ double at(int q) const {
-    double v = k[0];
-#pragma unroll
-    for (int i = 1; i < K; ++i)
-      if (i == q) v = k[i];
-    return v;
-  }
-  template <int WT>
-  __device__ __forceinline__ void compute(const TagRows<K, WT>& A, const PCol& pc) {
-#pragma unroll
-    for (int q = 0; q < K; ++q) k[q] = ((A.pres >> q) & 1u) ? proof_key<WT>(A.m[q], pc) : 0.0;
-  }
-};
-
 #ifndef SG_DTKP_KEY_CONT  // 0: every conj candidate's key is a full product (A/B tests)
 #define SG_DTKP_KEY_CONT 1
 #endif
+#ifndef SG_DTKP_PRUNE  // 0: no upper-bound pruning of binary conj candidates (A/B tests)
+#define SG_DTKP_PRUNE 1
+#endif
+constexpr int kKeyStride = 128;  // per-thread key slots in shared memory: slot q at [q * 128 + tid]
 
-// conj_into with the left rows' keys known (AK): a candidate whose right row's members all
-// follow the left row's (the usual case when a prefix is extended by a later input) takes
-// its key as the continuation of the left key — ONE multiply for a single-member right row —
-// bit-identical to the full ascending product (proof_key); any other candidate falls back
-// to the full product.  Same candidate order, same inserts as conj_into.
+// Keys of a tag's present rows -> the thread's shared key slots ks[q * kKeyStride].
 template <int K, int WT>
-__device__ __forceinline__ void conj_keyed(TopK<K, WT>& T, const TagRows<K, WT>& A, const RowKeys<K>& AK,
-                                           const TagRows<K, WT>& Bt, const PCol& pc) {
+__device__ __forceinline__ void row_keys(double* ks, const TagRows<K, WT>& T, const PCol& pc) {
+  constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
+#pragma unroll (kUnrollK)
+  for (int q = 0; q < K; ++q) {
+    if (!((T.pres >> q) & 1u)) continue;
+    uint64_t m[WT];
+    T.row(q, m);
+    ks[q * kKeyStride] = proof_key<WT>(m, pc);
+  }
+}
+
+// Binary conj streamed into the segment's top-k S (AR = 2) with the operands' row keys
+// known (kA, kB: shared slots).  Same candidate order and the same inserts as conj_into;
+// two exact shortcuts:
+//  * bound: with every registry probability of the sample in [0, 1] (le1), the ascending
+//    fp64 product over a union never exceeds the product over either part (each extra
+//    factor is <= 1 and rounding is monotone), so once S is full a candidate whose left
+//    or right row key is not above S's k-th key cannot enter — insert() would reject it
+//    after computing its key; it is skipped before;
+//  * continuation: when every member of the right row follows the left row's, the
+//    union's product is the left key continued over the right row (one multiply for a
+//    single-member row), the same multiplies in the same order as proof_key.
+template <int K, int WT>
+__device__ __forceinline__ void conj_pruned(TopK<K, WT>& S, const TagRows<K, WT>& A, const TagRows<K, WT>& Bt,
+                                            const double* kA, const double* kB, bool le1, const PCol& pc) {
   constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
 #pragma unroll (kUnrollK)
   for (int qa = 0; qa < K; ++qa) {
     if (!((A.pres >> qa) & 1u)) continue;
+    const double ka = kA[qa * kKeyStride];
+    if (SG_DTKP_PRUNE && le1 && S.n == K && !(ka > S.key[K - 1])) continue;
     uint64_t ma[WT];
     A.row(qa, ma);
-    const double ka = AK.at(qa);
     const int ha = hi_col<WT>(ma);
 #pragma unroll (kUnrollK)
     for (int qb = 0; qb < K; ++qb) {
       if (!((Bt.pres >> qb) & 1u)) continue;
+      if (SG_DTKP_PRUNE && le1 && S.n == K && !(kB[qb * kKeyStride] > S.key[K - 1])) continue;
       uint64_t mb[WT], mm[WT];
       Bt.row(qb, mb);
 #pragma unroll
       for (int w = 0; w < WT; ++w) mm[w] = mb[w] | ma[w];
-      const int lb = lo_col<WT>(mb);
       double kk;
-      if (ha < lb)
+      const int lb = lo_col<WT>(mb);
+      if (SG_DTKP_KEY_CONT && ha < lb)
         kk = one_member<WT>(mb) ? ka * pc(lb) : proof_key<WT>(mb, pc, ka);
       else
         kk = proof_key<WT>(mm, pc);
-      T.insert(mm, kk, 0);
+      S.insert(mm, kk, 0);
     }
   }
 }
@@ -407,7 +417,8 @@ constexpr int kRowMask = 0x7fffffff;  // record word 0 bit 31: last record of a 
 // record of each intermediate flagged by bit 31 of its second word.  Each is its own kernel,
 // so the streaming kernel does not carry the conj fold's registers (occupancy) or code.
 template <int K, int WT, int AR>
-__device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, int64_t b0, bool bval, const PCol& pc) {
+__device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, int64_t b0, bool bval, const PCol& pc,
+                                           double* ks, bool le1) {
   constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
   const int4 item = __ldg(reinterpret_cast<const int4*>(a.items) + it);
   const bool multi = a.packed && item.w < 0;  // segments close at flagged records
@@ -506,18 +517,16 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
     // next record's rows held in registers only while K is small (their registers cost
     // occupancy); otherwise loaded after the current record
     constexpr bool kPf = K <= SG_DTKP_CONJ_PREFETCH_MAXK;
-    // the left rows' keys, valid while consecutive records conjoin the same left row
-    // (records are grouped by output symbol, and e.g. a prefix extended by every symbol of
-    // the next input yields a run of records with one left row)
-    // (K <= 3 only: at K = 5 the key registers spill and CLUTRR-style closures, whose
-    // columns interleave, lose 9%)
-    constexpr bool kCont = SG_DTKP_KEY_CONT && K <= 3;
-    RowKeys<K> AK;
+    // AR 2: the left rows' keys stay valid while consecutive records conjoin the same left
+    // row (records are grouped by output symbol, and e.g. a prefix extended by every symbol
+    // of the next input is a run of records with one left row); the right rows' keys are
+    // taken per record
+    constexpr bool kKeyed = AR == 2;
     bool ak_ok = false;
     for (int c = item.y; c < item.z; ++c) {
       const bool more = c + 1 < item.z;
       const int rna = ran, rnb = rbn;
-      const bool same_a = kCont && (rna & kRowMask) == (wa & kRowMask);
+      const bool same_a = kKeyed && (rna & kRowMask) == (wa & kRowMask);
       if (kPf && more) {
         if (!same_a) An.load(a.ops[0], a.B, b, rna & kRowMask);
         Bn.load(a.ops[1], a.B, b, rnb);
@@ -526,23 +535,18 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
         ran = rec_row(a, c + 2, 0);
         rbn = rec_row(a, c + 2, 1);
       }
-      if (kCont && !ak_ok) {
-        AK.compute<WT>(A, pc);
-        ak_ok = true;
-      }
       if constexpr (AR == 2) {
-        // exact: see conj_into / conj_keyed
-        if (kCont)
-          conj_keyed<K, WT>(S, A, AK, Bt, pc);
-        else
-          conj_into<K, WT>(S, A, Bt, pc);
+        // exact: see conj_into / conj_pruned
+        if (!ak_ok) {
+          row_keys<K, WT>(ks, A, pc);
+          ak_ok = true;
+        }
+        row_keys<K, WT>(ks + K * kKeyStride, Bt, pc);
+        conj_pruned<K, WT>(S, A, Bt, ks, ks + K * kKeyStride, le1, pc);
       } else {
         TopK<K, WT> T;
         T.clear();
-        if (kCont)
-          conj_keyed<K, WT>(T, A, AK, Bt, pc);
-        else
-          conj_into<K, WT>(T, A, Bt, pc);
+        conj_into<K, WT>(T, A, Bt, pc);
 #pragma unroll 1
         for (int i = 2; i < a.arity; ++i) {
           TagRows<K, WT> Ci;
@@ -616,6 +620,16 @@ __global__ void __launch_bounds__(128, dtkp_min_blocks(K, WT, AR)) k_dtkp_apply(
   const int64_t b = bval ? b0 : a.B - 1;
   const PCol pc = stage_pcol(ptile_raw, a.p, a.I, a.B, b, lane, warp, nwarps);
   __syncthreads();
+  // binary conj: per-thread key slots after the probability tile, and whether every
+  // registry probability of this sample lies in [0, 1] (the bound of conj_pruned)
+  double* ks = reinterpret_cast<double*>(ptile_raw + ptile_bytes(a.I)) + threadIdx.x;
+  bool le1 = true;
+  if (AR == 2) {
+    for (int j = 0; j < a.I; ++j) {
+      const double v = pc(j);
+      le1 = le1 && v >= 0.0 && v <= 1.0;
+    }
+  }
 
   if (a.sched != nullptr) {
     // dynamic: every warp takes the next item of its 32-sample column from a counter, so
@@ -626,7 +640,7 @@ __global__ void __launch_bounds__(128, dtkp_min_blocks(K, WT, AR)) k_dtkp_apply(
       if (lane == 0) it = atomicAdd(ctr, 1);
       it = __shfl_sync(0xffffffffu, it, 0);
       if (it >= a.n_items) break;
-      apply_item<K, WT, AR>(a, it, b, b0, bval, pc);
+      apply_item<K, WT, AR>(a, it, b, b0, bval, pc, ks, le1);
     }
     // the last CTA out re-zeroes the counters for the next launch that uses the buffer
     __syncthreads();
@@ -643,7 +657,7 @@ __global__ void __launch_bounds__(128, dtkp_min_blocks(K, WT, AR)) k_dtkp_apply(
   // static: CTAs stride over the work blocks; the probability tile is staged once per CTA
   for (int bk = blockIdx.y; bk < a.n_blk; bk += gridDim.y) {
     const int it0 = __ldg(a.blk + bk), it1 = __ldg(a.blk + bk + 1);
-    for (int it = it0 + warp; it < it1; it += nwarps) apply_item<K, WT, AR>(a, it, b, b0, bval, pc);
+    for (int it = it0 + warp; it < it1; it += nwarps) apply_item<K, WT, AR>(a, it, b, b0, bval, pc, ks, le1);
   }
 }
 
@@ -651,7 +665,7 @@ template <int K, int WT, int AR>
 static int launch_apply_kwa(const DtkpK& k, int n_blocks, cudaStream_t st) {
   const int mode = ptile_mode(k.I);
   if (mode == 0) return (int)cudaErrorNotSupported;
-  const size_t smem = (size_t)k.I * kWarp * (mode == 2 ? sizeof(double) : sizeof(float));
+  const size_t smem = ptile_bytes(k.I) + (AR == 2 ? (size_t)2 * K * kKeyStride * sizeof(double) : 0);
   {
     cudaError_t e = ensure_smem((const void*)k_dtkp_apply<K, WT, AR>, smem);
     if (e != cudaSuccess) return (int)e;
