@@ -282,12 +282,6 @@ typedef struct sg_dtkp_apply_desc {
 
 int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream);
 
-/* Input tags of n symbols registered at columns start .. start + n - 1 (DtkpAm.input_tags,
- * provenance.py:297-306): symbol i holds the single proof {start + i} in row 0, rows 1..K-1
- * absent.  member u64 [n][K][W][B], present u8 [n][K][B], both written in full (one launch). */
-int sg_dtkp_input_tags(int32_t start, int32_t n, int32_t K, int32_t W, int64_t B, uint64_t* member,
-                       uint8_t* present, sg_stream_t stream);
-
 /* P[n][b] = clamp01( sum_r present * prod_{j in row r} p[j][b] )  (fp64 inside, fp32 out) */
 int sg_dtkp_probs_fwd(const uint64_t* member, const uint8_t* present, int32_t N, int32_t K,
                       int32_t W, const float* p, int32_t I, int64_t B, float* out,

@@ -167,7 +167,6 @@ EXPORTS = {
                                  c_void_p]),
     "sg_rows_gather": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "sg_dtkp_apply": (c_int32, [POINTER(SgDtkpApplyDesc), c_void_p]),
-    "sg_dtkp_input_tags": (c_int32, [c_int32, c_int32, c_int32, c_int32, c_int64, c_void_p, c_void_p, c_void_p]),
     "sg_dtkp_probs_fwd": (
         c_int32,
         [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32, c_int64, c_void_p, c_void_p],

@@ -231,27 +231,6 @@ static int dedup_k(const uint8_t* member, const uint8_t* present, const double* 
 
 using namespace sg;
 
-namespace sg {
-// member [n][K][W][B] then present [n][K][B], one grid-stride pass over both
-__global__ void k_dtkp_input_tags(int32_t start, int32_t K, int32_t W, int64_t B, int64_t nm, int64_t np,
-                                  uint64_t* __restrict__ member, uint8_t* __restrict__ present) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nm + np; e += stride) {
-    if (e < nm) {
-      const int64_t row = e / B;  // (i * K + q) * W + w
-      const int w = (int)(row % W);
-      const int64_t iq = row / W;
-      const int q = (int)(iq % K);
-      const int col = start + (int)(iq / K);
-      member[e] = (q == 0 && w == col / 64) ? (1ull << (col % 64)) : 0ull;
-    } else {
-      const int64_t f = e - nm;
-      present[f] = ((f / B) % K) == 0 ? 1 : 0;
-    }
-  }
-}
-}  // namespace sg
-
 extern "C" {
 
 int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream) {
@@ -334,19 +313,6 @@ int sg_dtkp_apply(const sg_dtkp_apply_desc* d, sg_stream_t stream) {
   return 0;
 }
 
-int sg_dtkp_input_tags(int32_t start, int32_t n, int32_t K, int32_t W, int64_t B, uint64_t* member, uint8_t* present,
-                       sg_stream_t stream) {
-  if (n <= 0 || B <= 0) return 0;
-  SG_RETURN_IF(start < 0 || K < 1 || W < 1 || (int64_t)start + n > (int64_t)W * 64, cudaErrorInvalidValue);
-  const int64_t nm = (int64_t)n * K * W * B, np = (int64_t)n * K * B;
-  const int threads = 256;
-  const int64_t blocks = std::min<int64_t>(ceil_div(nm + np, threads), 148 * 16);
-  count_launch();
-  k_dtkp_input_tags<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(start, K, W, B, nm, np, member, present);
-  SG_LAUNCH_CHECK();
-  return 0;
-}
-
 int sg_dtkp_probs_fwd(const uint64_t* member, const uint8_t* present, int32_t N, int32_t K, int32_t W, const float* p,
                       int32_t I, int64_t B, float* out, sg_stream_t stream) {
   if (N <= 0 || B <= 0) return 0;
@@ -357,7 +323,7 @@ int sg_dtkp_probs_fwd(const uint64_t* member, const uint8_t* present, int32_t N,
   dim3 grid(ceil_div(B, kWarp), ceil_div(N, rows_per));
   const int mode = ptile_mode(I);
   SG_RETURN_IF(mode == 0, cudaErrorNotSupported);
-  const size_t smem = (size_t)I * kWarp * (mode == 2 ? sizeof(double) : sizeof(float));
+  const size_t smem = ptile_bytes(I);
 #define SG_PF(WT)                                                                                        \
   do {                                                                                                   \
     ensure_smem((const void*)k_dtkp_probs_fwd<WT>, smem);                                                \

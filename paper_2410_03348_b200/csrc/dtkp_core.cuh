@@ -98,6 +98,7 @@ struct PCol {
   const double* smd;
   const float* smf;
   bool dbl;
+  int one;  // index of a staged column holding exactly 1.0 (= I): the filler of proof_key
   __device__ __forceinline__ double operator()(int j) const {
     return dbl ? smd[(size_t)j * kWarp] : (double)smf[(size_t)j * kWarp];
   }
@@ -105,15 +106,16 @@ struct PCol {
 
 static constexpr size_t kMaxPTile = 192 * 1024;
 
-// Staging mode for a registry of I columns: 2 = fp64, 1 = fp32, 0 = does not fit.
+// Staging mode for a registry of I columns (+ the 1.0 column): 2 = fp64, 1 = fp32, 0 =
+// does not fit.
 __host__ __device__ inline int ptile_mode(int I) {
-  if ((size_t)I * kWarp * sizeof(double) <= kMaxPTile) return 2;
-  if ((size_t)I * kWarp * sizeof(float) <= kMaxPTile) return 1;
+  if ((size_t)(I + 1) * kWarp * sizeof(double) <= kMaxPTile) return 2;
+  if ((size_t)(I + 1) * kWarp * sizeof(float) <= kMaxPTile) return 1;
   return 0;
 }
 
 __host__ __device__ inline size_t ptile_bytes(int I) {
-  return (size_t)I * kWarp * (ptile_mode(I) == 2 ? sizeof(double) : sizeof(float));
+  return (size_t)(I + 1) * kWarp * (ptile_mode(I) == 2 ? sizeof(double) : sizeof(float));
 }
 
 __device__ __forceinline__ PCol stage_pcol(void* tile, const float* __restrict__ p, int I, int64_t B, int64_t b,
@@ -140,7 +142,13 @@ __device__ __forceinline__ PCol stage_pcol(void* tile, const float* __restrict__
       }
     }
   }
-  return PCol{reinterpret_cast<const double*>(tile) + lane, reinterpret_cast<const float*>(tile) + lane, dbl};
+  if (warp == 0) {  // column I = 1.0 exactly
+    if (dbl)
+      reinterpret_cast<double*>(tile)[(size_t)I * kWarp + lane] = 1.0;
+    else
+      reinterpret_cast<float*>(tile)[(size_t)I * kWarp + lane] = 1.f;
+  }
+  return PCol{reinterpret_cast<const double*>(tile) + lane, reinterpret_cast<const float*>(tile) + lane, dbl, I};
 }
 
 // fp64 product of member probabilities in ascending column order (_dtkpcore.pyx:53-57).
@@ -150,9 +158,34 @@ __device__ __forceinline__ PCol stage_pcol(void* tile, const float* __restrict__
 // `start` continues a product: proof_key(b, pc, proof_key(a, pc)) == proof_key(a | b, pc)
 // bit for bit when every member of a precedes every member of b (the fold is the same
 // sequence of multiplies).
+#ifndef SG_DTKP_KEY32  // 0: the 64-bit scan with selected fillers (A/B tests)
+#define SG_DTKP_KEY32 1
+#endif
 template <int WT>
 __device__ __forceinline__ double proof_key(const uint64_t (&mm)[WT], const PCol& pc, double start = 1.0) {
   double prod = start;
+#if SG_DTKP_KEY32
+  // 32-bit halves (one FLO per bit instead of a 64-bit find-first-set), and a missing slot
+  // of a group reads the staged 1.0 column instead of selecting 1.0 after the load
+#pragma unroll
+  for (int h = 0; h < 2 * WT; ++h) {
+    uint32_t x = (h & 1) ? (uint32_t)(mm[h >> 1] >> 32) : (uint32_t)mm[h >> 1];
+    while (x) {
+      int j[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        j[u] = x ? h * 32 + __ffs((int)x) - 1 : pc.one;
+        x &= x - 1;
+      }
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = pc(j[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) prod *= v[u];
+    }
+  }
+  return prod;
+#endif
 #pragma unroll
   for (int w = 0; w < WT; ++w) {
     uint64_t x = mm[w];
@@ -311,40 +344,45 @@ __device__ __forceinline__ bool one_member(const uint64_t (&m)[WT]) {
 #ifndef SG_DTKP_PRUNE  // 0: no upper-bound pruning of binary conj candidates (A/B tests)
 #define SG_DTKP_PRUNE 1
 #endif
-constexpr int kKeyStride = 128;  // per-thread key slots in shared memory: slot q at [q * 128 + tid]
 
-// Keys of a tag's present rows -> the thread's shared key slots ks[q * kKeyStride].
-template <int K, int WT>
-__device__ __forceinline__ void row_keys(double* ks, const TagRows<K, WT>& T, const PCol& pc) {
-  constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
-#pragma unroll (kUnrollK)
-  for (int q = 0; q < K; ++q) {
-    if (!((T.pres >> q) & 1u)) continue;
-    uint64_t m[WT];
-    T.row(q, m);
-    ks[q * kKeyStride] = proof_key<WT>(m, pc);
+// Keys of the K rows of a left conj operand (0 for absent rows), computed once per loaded
+// tag and reused by every record of an item that conjoins the same left row.
+template <int K>
+struct RowKeys {
+  double k[K];
+  __device__ __forceinline__ double at(int q) const {
+    double v = k[0];
+#pragma unroll
+    for (int i = 1; i < K; ++i)
+      if (i == q) v = k[i];
+    return v;
   }
-}
+  template <int WT>
+  __device__ __forceinline__ void compute(const TagRows<K, WT>& A, const PCol& pc) {
+#pragma unroll
+    for (int q = 0; q < K; ++q) k[q] = ((A.pres >> q) & 1u) ? proof_key<WT>(A.m[q], pc) : 0.0;
+  }
+};
 
-// Binary conj streamed into the segment's top-k S (AR = 2) with the operands' row keys
-// known (kA, kB: shared slots).  Same candidate order and the same inserts as conj_into;
-// two exact shortcuts:
+// Binary conj streamed into the segment's top-k S (AR = 2, K <= 3) with the left rows'
+// keys known (AK).  Same candidate order and the same inserts as conj_into; two exact
+// shortcuts:
 //  * bound: with every registry probability of the sample in [0, 1] (le1), the ascending
-//    fp64 product over a union never exceeds the product over either part (each extra
-//    factor is <= 1 and rounding is monotone), so once S is full a candidate whose left
-//    or right row key is not above S's k-th key cannot enter — insert() would reject it
-//    after computing its key; it is skipped before;
+//    fp64 product over a union never exceeds the product over its left part (each extra
+//    factor is <= 1 and rounding is monotone), so once S is full a left row whose key is
+//    not above S's k-th key contributes nothing — insert() would reject each of its
+//    candidates after computing their keys; the row is skipped before;
 //  * continuation: when every member of the right row follows the left row's, the
 //    union's product is the left key continued over the right row (one multiply for a
 //    single-member row), the same multiplies in the same order as proof_key.
 template <int K, int WT>
-__device__ __forceinline__ void conj_pruned(TopK<K, WT>& S, const TagRows<K, WT>& A, const TagRows<K, WT>& Bt,
-                                            const double* kA, const double* kB, bool le1, const PCol& pc) {
+__device__ __forceinline__ void conj_keyed(TopK<K, WT>& S, const TagRows<K, WT>& A, const RowKeys<K>& AK,
+                                           const TagRows<K, WT>& Bt, bool le1, const PCol& pc) {
   constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
 #pragma unroll (kUnrollK)
   for (int qa = 0; qa < K; ++qa) {
     if (!((A.pres >> qa) & 1u)) continue;
-    const double ka = kA[qa * kKeyStride];
+    const double ka = AK.at(qa);
     if (SG_DTKP_PRUNE && le1 && S.n == K && !(ka > S.key[K - 1])) continue;
     uint64_t ma[WT];
     A.row(qa, ma);
@@ -352,7 +390,6 @@ __device__ __forceinline__ void conj_pruned(TopK<K, WT>& S, const TagRows<K, WT>
 #pragma unroll (kUnrollK)
     for (int qb = 0; qb < K; ++qb) {
       if (!((Bt.pres >> qb) & 1u)) continue;
-      if (SG_DTKP_PRUNE && le1 && S.n == K && !(kB[qb * kKeyStride] > S.key[K - 1])) continue;
       uint64_t mb[WT], mm[WT];
       Bt.row(qb, mb);
 #pragma unroll
@@ -418,7 +455,7 @@ constexpr int kRowMask = 0x7fffffff;  // record word 0 bit 31: last record of a 
 // so the streaming kernel does not carry the conj fold's registers (occupancy) or code.
 template <int K, int WT, int AR>
 __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, int64_t b0, bool bval, const PCol& pc,
-                                           double* ks, bool le1) {
+                                           bool le1) {
   constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
   const int4 item = __ldg(reinterpret_cast<const int4*>(a.items) + it);
   const bool multi = a.packed && item.w < 0;  // segments close at flagged records
@@ -517,11 +554,12 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
     // next record's rows held in registers only while K is small (their registers cost
     // occupancy); otherwise loaded after the current record
     constexpr bool kPf = K <= SG_DTKP_CONJ_PREFETCH_MAXK;
-    // AR 2: the left rows' keys stay valid while consecutive records conjoin the same left
-    // row (records are grouped by output symbol, and e.g. a prefix extended by every symbol
-    // of the next input is a run of records with one left row); the right rows' keys are
-    // taken per record
-    constexpr bool kKeyed = AR == 2;
+    // AR 2, K <= 3: the left rows' keys stay valid while consecutive records conjoin the
+    // same left row (records are grouped by output symbol, and e.g. a prefix extended by
+    // every symbol of the next input is a run of records with one left row).  At K = 5 the
+    // key registers spill and CLUTRR-style closures lost 9-15%, so larger K stream plainly.
+    constexpr bool kKeyed = AR == 2 && K <= 3;
+    RowKeys<K> AK;
     bool ak_ok = false;
     for (int c = item.y; c < item.z; ++c) {
       const bool more = c + 1 < item.z;
@@ -536,13 +574,16 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
         rbn = rec_row(a, c + 2, 1);
       }
       if constexpr (AR == 2) {
-        // exact: see conj_into / conj_pruned
-        if (!ak_ok) {
-          row_keys<K, WT>(ks, A, pc);
-          ak_ok = true;
+        // exact: see conj_into / conj_keyed
+        if constexpr (kKeyed) {
+          if (!ak_ok) {
+            AK.compute<WT>(A, pc);
+            ak_ok = true;
+          }
+          conj_keyed<K, WT>(S, A, AK, Bt, le1, pc);
+        } else {
+          conj_into<K, WT>(S, A, Bt, pc);
         }
-        row_keys<K, WT>(ks + K * kKeyStride, Bt, pc);
-        conj_pruned<K, WT>(S, A, Bt, ks, ks + K * kKeyStride, le1, pc);
       } else {
         TopK<K, WT> T;
         T.clear();
@@ -620,11 +661,10 @@ __global__ void __launch_bounds__(128, dtkp_min_blocks(K, WT, AR)) k_dtkp_apply(
   const int64_t b = bval ? b0 : a.B - 1;
   const PCol pc = stage_pcol(ptile_raw, a.p, a.I, a.B, b, lane, warp, nwarps);
   __syncthreads();
-  // binary conj: per-thread key slots after the probability tile, and whether every
-  // registry probability of this sample lies in [0, 1] (the bound of conj_pruned)
-  double* ks = reinterpret_cast<double*>(ptile_raw + ptile_bytes(a.I)) + threadIdx.x;
+  // binary conj: whether every registry probability of this sample lies in [0, 1] (the
+  // bound of conj_keyed)
   bool le1 = true;
-  if (AR == 2) {
+  if (AR == 2 && K <= 3) {
     for (int j = 0; j < a.I; ++j) {
       const double v = pc(j);
       le1 = le1 && v >= 0.0 && v <= 1.0;
@@ -640,7 +680,7 @@ __global__ void __launch_bounds__(128, dtkp_min_blocks(K, WT, AR)) k_dtkp_apply(
       if (lane == 0) it = atomicAdd(ctr, 1);
       it = __shfl_sync(0xffffffffu, it, 0);
       if (it >= a.n_items) break;
-      apply_item<K, WT, AR>(a, it, b, b0, bval, pc, ks, le1);
+      apply_item<K, WT, AR>(a, it, b, b0, bval, pc, le1);
     }
     // the last CTA out re-zeroes the counters for the next launch that uses the buffer
     __syncthreads();
@@ -657,7 +697,7 @@ __global__ void __launch_bounds__(128, dtkp_min_blocks(K, WT, AR)) k_dtkp_apply(
   // static: CTAs stride over the work blocks; the probability tile is staged once per CTA
   for (int bk = blockIdx.y; bk < a.n_blk; bk += gridDim.y) {
     const int it0 = __ldg(a.blk + bk), it1 = __ldg(a.blk + bk + 1);
-    for (int it = it0 + warp; it < it1; it += nwarps) apply_item<K, WT, AR>(a, it, b, b0, bval, pc, ks, le1);
+    for (int it = it0 + warp; it < it1; it += nwarps) apply_item<K, WT, AR>(a, it, b, b0, bval, pc, le1);
   }
 }
 
@@ -665,7 +705,7 @@ template <int K, int WT, int AR>
 static int launch_apply_kwa(const DtkpK& k, int n_blocks, cudaStream_t st) {
   const int mode = ptile_mode(k.I);
   if (mode == 0) return (int)cudaErrorNotSupported;
-  const size_t smem = ptile_bytes(k.I) + (AR == 2 ? (size_t)2 * K * kKeyStride * sizeof(double) : 0);
+  const size_t smem = ptile_bytes(k.I);
   {
     cudaError_t e = ensure_smem((const void*)k_dtkp_apply<K, WT, AR>, smem);
     if (e != cudaSuccess) return (int)e;

@@ -584,17 +584,6 @@ class NllLoss(torch.autograd.Function):
         return grad, None
 
 
-def dtkp_input_tags(start: int, n: int, k: int, W: int, B: int, device) -> "tuple[torch.Tensor, torch.Tensor]":
-    """Input tags of n symbols at registry columns start.. (one launch, sg_dtkp_input_tags)."""
-    pm = torch.empty((n, k, W, B), device=device, dtype=torch.int64)
-    pp = torch.empty((n, k, B), device=device, dtype=torch.uint8)
-    if pm.numel():
-        rc = _lib().sg_dtkp_input_tags(start, n, k, W, B, pm.data_ptr(), pp.data_ptr(), N.stream_ptr(device))
-        N.check(rc, "sg_dtkp_input_tags")
-        _ledger("dtkp_input_tags", pm.numel() * 8 + pp.numel(), n)
-    return pm, pp
-
-
 def rows_gather(src: torch.Tensor, idx: torch.Tensor, out: torch.Tensor):
     """Copy whole contiguous symbol rows (DTKP tags): out[r] = src[idx[r]] or zeros for -1."""
     n = int(idx.numel())

@@ -630,6 +630,26 @@ def _bcast_dtkp(t: DtkpTags, B: int):
     return pm, pp
 
 
+_WORDS_CACHE: "dict[tuple, torch.Tensor]" = {}
+
+
+def _input_words(start: int, n: int, k: int, W: int, device) -> torch.Tensor:
+    """Device template [n][k][W] of single-proof input tags (cached: no H2D per call,
+    so programs stay CUDA-graph capturable)."""
+    key = (start, n, k, W, torch.device(device))
+    t = _WORDS_CACHE.get(key)
+    if t is None:
+        words = np.zeros((n, k, W), dtype=np.uint64)
+        for i in range(n):
+            j = start + i
+            words[i, 0, j // 64] = np.uint64(1) << np.uint64(j % 64)
+        t = torch.as_tensor(words.view(np.int64), device=device)
+        if len(_WORDS_CACHE) > 4096:
+            _WORDS_CACHE.clear()
+        _WORDS_CACHE[key] = t
+    return t
+
+
 class _IdentityPlans:
     """Cached KernelPlans of the column-wise DTKP operators (conj / disj) per width n."""
 
@@ -677,7 +697,10 @@ class DtkpAm:
         start = registry.add_block(ids, sm)
         n, b = sm.shape
         W = _words(registry.size)
-        pm, pp = ops.dtkp_input_tags(start, n, self.k, W, b, sm.device)
+        words = _input_words(start, n, self.k, W, sm.device)
+        pm = words[..., None].expand(n, self.k, W, b).contiguous()
+        pp = torch.zeros((n, self.k, b), device=sm.device, dtype=torch.uint8)
+        pp[:, 0] = 1
         return DtkpTags(pm, pp, registry)
 
     def zero(self, registry, b: int = 1, n: int = 1) -> DtkpTags:
