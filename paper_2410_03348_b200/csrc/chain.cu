@@ -397,27 +397,6 @@ __device__ __forceinline__ void load_prev(float2 (&pv)[R], const ChainArgs& a, c
   }
 }
 
-#ifndef SG_CHAIN_PF_ROUNDS  // backward: L1 prefetch of the v_{i-1} rows two rounds ahead
-#define SG_CHAIN_PF_ROUNDS 1
-#endif
-// rows r0 .. r0 + kRound - 1 of v_{ii-1} (the warp's contiguous block: kRound * kCWS * 4
-// bytes) -> L1, one 128-byte line per lane; the register loads of those rows are issued a
-// round later (load_prev), by which time the lines are close (ncu: the first FFMA2 using a
-// round's state rows was the kernel's hottest long-scoreboard stall)
-template <bool FIRST>
-__device__ __forceinline__ void prefetch_round(const ChainArgs& a, const float2* sblk, const Lane& L, int ii, int r0) {
-  if constexpr (!FIRST) {
-    if (!SG_CHAIN_PF_ROUNDS) return;
-    const int nin = a.n[ii - 1];
-    if (r0 >= nin) return;
-    const int rows = nin - r0 < kRound ? nin - r0 : kRound;
-    const char* base =
-        reinterpret_cast<const char*>(sblk - L.c + (size_t)(a.state_off[ii - 1] + r0) * (kCWS / 2));
-    const int o = (threadIdx.x & 31) * 128;
-    if (o < rows * kCWS * 4) asm volatile("prefetch.global.L1 [%0];" ::"l"(base + o));
-  }
-}
-
 // One backward step (apply i), in place on G.  Rounds ascend: G_{i-1}[s] reads G_i[s ..
 // s+KF-1], so a round only reads rows no earlier round has overwritten, and inside a round
 // every group loads its window before any group stores (__syncwarp).  Per tile: rows
@@ -480,17 +459,14 @@ __device__ __forceinline__ void bwd_step(float2* G, float2* scratch, const float
   float2 gA[R + KF - 1], gB[R + KF - 1];
   const int s0g = L.g * R;
   bwd_window<KF, R>(gA, G, s0g);
-  prefetch_round<FIRST>(a, sblk, L, i, STEP);
   for (int k = 0; k < kr; k += 2) {
     const int s0 = k * STEP + s0g;
-    prefetch_round<FIRST>(a, sblk, L, i, (k + 2) * STEP);
     if (k + 1 < kr) {
       load_prev<R, FIRST>(pvB, a, sblk, L, i, s0 + STEP);
       bwd_window<KF, R>(gB, G, s0 + STEP);
     }
     bwd_round<KF, R, FIRST>(G, f, gA, pvA, d2, s0, nin, (k + 1) * STEP <= nin, a, L);
     if (k + 1 >= kr) break;
-    prefetch_round<FIRST>(a, sblk, L, i, (k + 3) * STEP);
     if (k + 2 < kr) {
       load_prev<R, FIRST>(pvA, a, sblk, L, i, s0 + 2 * STEP);
       bwd_window<KF, R>(gA, G, s0 + 2 * STEP);

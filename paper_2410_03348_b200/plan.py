@@ -532,6 +532,21 @@ def dtkp_pack_size(n_rec: int, B: int) -> int:
     target = max(1, 4 * DTKP_RESIDENT_WARPS // gx)
     p = min(DTKP_MAX_ITEM, n_rec // target)
     return p if p > 1 else 0
+
+
+def dtkp_item_size(n_rec: int, B: int) -> int:
+    """Records per piece of a long segment.  48 while the problem fills the resident warps
+    several times over; a small problem with one long segment (HWF-7 step 4: 11,037
+    records, one 101-record segment, ~6 records per resident warp) is cut finer, because
+    its longest item is the launch's critical path — the two-level merge absorbs the
+    extra partial lists."""
+    gx = max(1, -(-B // 32))
+    per_warp = n_rec * gx / DTKP_RESIDENT_WARPS
+    if per_warp >= DTKP_MAX_ITEM / 2:
+        return DTKP_MAX_ITEM
+    return int(min(DTKP_MAX_ITEM, max(8, 2 * -(-int(per_warp * 2) // 2))))
+
+
 DTKP_FUSED_ITEM = int(os.environ.get("SG_DTKP_FUSED_ITEM", "48"))  # conj records per fused item
 DTKP_MERGE_ITEM = 8  # partial lists per first-level merge item (two-level merge)
 STAGE_BYTES = 200 * 1024
@@ -600,16 +615,17 @@ class KernelPlan:
             self._bwd_host[k] = h
         return h
 
-    def dtkp_host(self, pack: int = 0) -> HostSegsum:
+    def dtkp_host(self, pack: int = 0, item: int = DTKP_MAX_ITEM) -> HostSegsum:
         """DTKP work list; pack > 1 gathers runs of whole short segments of up to `pack`
-        records per item (sg_dtkp_apply_desc.seg_packed)."""
+        records per item (sg_dtkp_apply_desc.seg_packed); long segments are cut into
+        pieces of `item` records."""
         if self._dtkp_host is None:
             self._dtkp_host = {}
-        h = self._dtkp_host.get(pack)
+        h = self._dtkp_host.get((pack, item))
         if h is None:
             order, off = csr(self.out_idx, self.n_out)
-            h = HostSegsum(off, self.records[order], DTKP_MAX_ITEM, pack=pack)
-            self._dtkp_host[pack] = h
+            h = HostSegsum(off, self.records[order], item, pack=pack)
+            self._dtkp_host[(pack, item)] = h
         return h
 
     def dtkp_fused_host(self, inner: "KernelPlan") -> HostSegsum:
@@ -724,12 +740,13 @@ class DevicePlan:
     def dtkp(self, B: int = 0):
         """(items, merge, merge2) for batch B (the packing granularity depends on B)."""
         pack = dtkp_pack_size(self.kp.n_rec, B) if B else 0
+        item = dtkp_item_size(self.kp.n_rec, B) if B else DTKP_MAX_ITEM
         if self._dtkp is None:
             self._dtkp = {}
-        hit = self._dtkp.get(pack)
+        hit = self._dtkp.get((pack, item))
         if hit is None:
-            hit = self._dtkp_levels(self.kp.dtkp_host(pack))
-            self._dtkp[pack] = hit
+            hit = self._dtkp_levels(self.kp.dtkp_host(pack, item))
+            self._dtkp[(pack, item)] = hit
         return hit
 
     def dtkp_fused(self, inner: "KernelPlan"):
