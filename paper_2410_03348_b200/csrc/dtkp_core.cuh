@@ -161,56 +161,29 @@ __device__ __forceinline__ PCol stage_pcol(void* tile, const float* __restrict__
 #ifndef SG_DTKP_KEY32  // 0: the 64-bit scan with selected fillers (A/B tests)
 #define SG_DTKP_KEY32 1
 #endif
-#ifndef SG_DTKP_KEY32_MINBITS  // proofs with at least this many members scan 32-bit halves
-#define SG_DTKP_KEY32_MINBITS 8
-#endif
 template <int WT>
 __device__ __forceinline__ double proof_key(const uint64_t (&mm)[WT], const PCol& pc, double start = 1.0) {
   double prod = start;
 #if SG_DTKP_KEY32
-  // Dense proofs (>= 8 members: HWF's formulas): 32-bit halves, one FLO per bit instead of
-  // a 64-bit find-first-set.  Sparse ones (CLUTRR's 2-4-fact paths spread over the words):
-  // 64-bit words, fewer part-filled groups.  Either way a group's missing slots read the
-  // staged 1.0 column instead of selecting 1.0 after the load.  The branch is on the
-  // member count, near-uniform across a warp (one symbol's proofs have similar sizes).
-  int bits = 0;
+  // 32-bit halves (one FLO per bit instead of a 64-bit find-first-set), and a group's
+  // missing slots read the staged 1.0 column instead of selecting 1.0 after the load.
+  // (A member-count switch to 64-bit words for sparse proofs measured slower on both
+  // HWF-7 and CLUTRR: the branch and its registers cost more than the part-filled groups.)
 #pragma unroll
-  for (int w = 0; w < WT; ++w) bits += __popcll(mm[w]);
-  if (bits >= SG_DTKP_KEY32_MINBITS) {
+  for (int h = 0; h < 2 * WT; ++h) {
+    uint32_t x = (h & 1) ? (uint32_t)(mm[h >> 1] >> 32) : (uint32_t)mm[h >> 1];
+    while (x) {
+      int j[4];
 #pragma unroll
-    for (int h = 0; h < 2 * WT; ++h) {
-      uint32_t x = (h & 1) ? (uint32_t)(mm[h >> 1] >> 32) : (uint32_t)mm[h >> 1];
-      while (x) {
-        int j[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          j[u] = x ? h * 32 + __ffs((int)x) - 1 : pc.one;
-          x &= x - 1;
-        }
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = pc(j[u]);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) prod *= v[u];
+      for (int u = 0; u < 4; ++u) {
+        j[u] = x ? h * 32 + __ffs((int)x) - 1 : pc.one;
+        x &= x - 1;
       }
-    }
-  } else {
+      double v[4];
 #pragma unroll
-    for (int w = 0; w < WT; ++w) {
-      uint64_t x = mm[w];
-      while (x) {
-        int j[4];
+      for (int u = 0; u < 4; ++u) v[u] = pc(j[u]);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          j[u] = x ? w * 64 + __ffsll((long long)x) - 1 : pc.one;
-          x &= x - 1;
-        }
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = pc(j[u]);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) prod *= v[u];
-      }
+      for (int u = 0; u < 4; ++u) prod *= v[u];
     }
   }
   return prod;
