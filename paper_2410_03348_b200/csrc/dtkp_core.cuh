@@ -344,6 +344,15 @@ __device__ __forceinline__ bool one_member(const uint64_t (&m)[WT]) {
 #ifndef SG_DTKP_KEY_CONT  // 0: every conj candidate's key is a full product (A/B tests)
 #define SG_DTKP_KEY_CONT 1
 #endif
+#ifndef SG_DTKP_KEYED_MAXK  // largest K whose binary conj keeps left-row keys (registers)
+#define SG_DTKP_KEYED_MAXK 3
+#endif
+#ifndef SG_DTKP_CONJ5_MINB  // resident CTAs/SM asked of the binary conj at 3 < K <= 5
+#define SG_DTKP_CONJ5_MINB 4
+#endif
+#ifndef SG_DTKP_FIRST_FILL  // 0: the first record of a segment is inserted candidate by candidate
+#define SG_DTKP_FIRST_FILL 1
+#endif
 #ifndef SG_DTKP_PRUNE  // 0: no upper-bound pruning of binary conj candidates (A/B tests)
 #define SG_DTKP_PRUNE 1
 #endif
@@ -380,8 +389,37 @@ struct RowKeys {
 //    single-member row), the same multiplies in the same order as proof_key.
 template <int K, int WT>
 __device__ __forceinline__ void conj_keyed(TopK<K, WT>& S, const TagRows<K, WT>& A, const RowKeys<K>& AK,
-                                           const TagRows<K, WT>& Bt, bool le1, const PCol& pc) {
+                                           const TagRows<K, WT>& Bt, bool le1, bool ranked, const PCol& pc) {
   constexpr int kUnrollK = K <= SG_DTKP_UNROLL_K ? K : 1;
+  if (SG_DTKP_FIRST_FILL && ranked && S.n == 0 && Bt.pres == 1u && (A.pres & (A.pres + 1u)) == 0u) {
+    // First record of a segment, one single-member right row that follows every left row:
+    // the candidates a_q | b are distinct (the a_q are) and their keys key(a_q) * p_b are
+    // non-increasing in q (a ranked tag, one non-negative factor), so the inserts would
+    // append them in order — S takes them directly.
+    uint64_t mb[WT];
+    Bt.row(0, mb);
+    const int lb = lo_col<WT>(mb);
+    bool ok = one_member<WT>(mb);
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+      if ((A.pres >> q) & 1u) ok = ok && hi_col<WT>(A.m[q]) < lb;
+    if (ok) {
+      const double pb = pc(lb);
+      int n = 0;
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        if ((A.pres >> q) & 1u) {
+#pragma unroll
+          for (int w = 0; w < WT; ++w) S.m[q][w] = A.m[q][w] | mb[w];
+          S.key[q] = AK.k[q] * pb;
+          S.idx[q] = 0;
+          ++n;
+        }
+      }
+      S.n = n;
+      return;
+    }
+  }
 #pragma unroll (kUnrollK)
   for (int qa = 0; qa < K; ++qa) {
     if (!((A.pres >> qa) & 1u)) continue;
@@ -561,7 +599,7 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
     // same left row (records are grouped by output symbol, and e.g. a prefix extended by
     // every symbol of the next input is a run of records with one left row).  At K = 5 the
     // key registers spill and CLUTRR-style closures lost 9-15%, so larger K stream plainly.
-    constexpr bool kKeyed = AR == 2 && K <= 3;
+    constexpr bool kKeyed = AR == 2 && K <= SG_DTKP_KEYED_MAXK;
     RowKeys<K> AK;
     bool ak_ok = false;
     for (int c = item.y; c < item.z; ++c) {
@@ -583,7 +621,7 @@ __device__ __forceinline__ void apply_item(const DtkpK& a, int it, int64_t b, in
             AK.compute<WT>(A, pc);
             ak_ok = true;
           }
-          conj_keyed<K, WT>(S, A, AK, Bt, le1, pc);
+          conj_keyed<K, WT>(S, A, AK, Bt, le1, a.ranked != 0, pc);
         } else {
           conj_into<K, WT>(S, A, Bt, pc);
         }
@@ -649,7 +687,7 @@ __host__ __device__ constexpr int dtkp_min_blocks(int K, int WT, int AR) {
                                   : AR == 2 ? (K > SG_DTKP_CONJ_PREFETCH_MAXK ? SG_DTKP_CONJ3_MINB : 4)
                                   : AR == 3 ? SG_DTKP_FUSED_MINB : 1)
          : (WT <= 2 && K <= 5 && AR == 1) ? 5
-         : (WT <= 2 && K <= 5 && AR == 2 && K > SG_DTKP_CONJ_PREFETCH_MAXK) ? 4
+         : (WT <= 2 && K <= 5 && AR == 2 && K > SG_DTKP_CONJ_PREFETCH_MAXK) ? SG_DTKP_CONJ5_MINB
          : 1;
 }
 
@@ -667,7 +705,7 @@ __global__ void __launch_bounds__(128, dtkp_min_blocks(K, WT, AR)) k_dtkp_apply(
   // binary conj: whether every registry probability of this sample lies in [0, 1] (the
   // bound of conj_keyed)
   bool le1 = true;
-  if (AR == 2 && K <= 3) {
+  if (AR == 2 && K <= SG_DTKP_KEYED_MAXK) {
     for (int j = 0; j < a.I; ++j) {
       const double v = pc(j);
       le1 = le1 && v >= 0.0 && v <= 1.0;
