@@ -26,7 +26,9 @@ from paper_2410_03348_b200.learn import loss_nll  # noqa: E402
 def main():
     dev = torch.device("cuda", 0)
     # DTKP: HWF-5 (split segments + merges), CLUTRR closure (k=5, unions), dynamic and static
-    for name in ("dtkp_hwf5", "dtkp_clutrr_k5", "dtkp_stack_k3"):
+    # (round 2: HWF-7 for the keyed conj's continuation / pruning / first fill and the
+    # adaptive piece size; the benchmarked CLUTRR closure for k = 5)
+    for name in ("dtkp_hwf5", "dtkp_hwf7", "dtkp_clutrr_k5", "dtkp_clutrr_e5_r20_k5", "dtkp_stack_k3"):
         run_gpu(name)
     ops.DTKP_DYNAMIC = False
     run_gpu("dtkp_hwf3")
@@ -37,7 +39,10 @@ def main():
         x = torch.tensor(rng.uniform(0.01, 1, size=(B, n)).astype(np.float32), device=dev, requires_grad=True)
         loss_nll(x, torch.tensor(rng.integers(0, n, size=B), device=dev)).backward()
     # DAMP chain (fused fwd/bwd) + loss on the rowsum path, generic segmented apply
-    for name in ("damp_sum15", "damp_mod_cond_a2", "damp_mod_a3", "damp_union_filter", "max_sum4"):
+    # (damp_sum15 at B = 4 runs the 16-row-group chain variant; the sweep case the
+    # sample-pair Toeplitz kernels; max_sum4 the fused max chain with 4 lanes per sample)
+    for name in ("damp_sum15", "damp_sweep_a2_s10", "damp_mod_cond_a2", "damp_mod_a3", "damp_union_filter",
+                 "max_sum4"):
         run_gpu(name)
     torch.cuda.synchronize()
     print("sanitize cases done")
