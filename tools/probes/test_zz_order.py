@@ -1,0 +1,47 @@
+"""Probe (copied into tests/ on the GPU box): which module cache, cleared before the
+capture, makes the graphed CLUTRR closure match eager after the golden cases ran."""
+import os
+
+import numpy as np
+import pytest
+
+from runners import load_golden, run_gpu
+from test_fixpoint import _graphed
+
+
+@pytest.mark.gpu
+def test_zz_order(cuda):
+    import torch
+
+    from paper_2410_03348_b200 import distribution as D
+    from paper_2410_03348_b200 import ops
+    from paper_2410_03348_b200 import plan as PL
+    from paper_2410_03348_b200 import provenance as PV
+
+    what = os.environ.get("ZZ_CLEAR", "")
+    if "words" in what:
+        PV._WORDS_CACHE.clear()
+    if "union" in what:
+        D._UNION_CACHE.clear()
+    if "map" in what:
+        ops._MAP_CACHE.clear()
+        ops._GATHER_CACHE.clear()
+    if "sched" in what:
+        ops._SCHED.clear()
+    if "plan" in what:
+        PL.plan_cache_clear()
+    if "prov" in what:
+        for n in ("_GROUPS", "_COLWISE", "_PAIRMAX"):
+            getattr(PV, n).clear()
+    if "filter" in what:
+        D._FILTER_CACHE.clear()
+    name = "dtkp_clutrr_e5_r20_k5"
+    gold = load_golden(name)
+    x = gold["in0"]
+    eager = run_gpu(name, [x])
+    gc = _graphed(cuda, x, w=gold["w"])
+    loss, g = gc(torch.tensor(x, device=cuda, dtype=torch.float32))
+    torch.cuda.synchronize()
+    err = float(np.abs(g.double().cpu().numpy() - eager["grads"][0]).max())
+    print(f"ZZ {what!r} grad err {err}")
+    assert err == 0.0
