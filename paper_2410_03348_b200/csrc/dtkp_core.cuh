@@ -350,6 +350,9 @@ __device__ __forceinline__ bool one_member(const uint64_t (&m)[WT]) {
 #ifndef SG_DTKP_CONJ5_MINB  // resident CTAs/SM asked of the binary conj at 3 < K <= 5
 #define SG_DTKP_CONJ5_MINB 4
 #endif
+#ifndef SG_DTKP_STREAM5_MINB  // resident CTAs/SM asked of the streaming kernel at 3 < K <= 5
+#define SG_DTKP_STREAM5_MINB 5
+#endif
 #ifndef SG_DTKP_FIRST_FILL  // 0: the first record of a segment is inserted candidate by candidate
 #define SG_DTKP_FIRST_FILL 1
 #endif
@@ -686,7 +689,7 @@ __host__ __device__ constexpr int dtkp_min_blocks(int K, int WT, int AR) {
          : (WT <= 2 && K <= 3) ? (AR == 1 ? (SG_DTKP_STREAM_PREFETCH ? 5 : 6)
                                   : AR == 2 ? (K > SG_DTKP_CONJ_PREFETCH_MAXK ? SG_DTKP_CONJ3_MINB : 4)
                                   : AR == 3 ? SG_DTKP_FUSED_MINB : 1)
-         : (WT <= 2 && K <= 5 && AR == 1) ? 5
+         : (WT <= 2 && K <= 5 && AR == 1) ? SG_DTKP_STREAM5_MINB
          : (WT <= 2 && K <= 5 && AR == 2 && K > SG_DTKP_CONJ_PREFETCH_MAXK) ? SG_DTKP_CONJ5_MINB
          : 1;
 }
