@@ -45,5 +45,16 @@ def test_zz_order(cuda):
     loss, g = gc(torch.tensor(x, device=cuda, dtype=torch.float32))
     torch.cuda.synchronize()
     err = float(np.abs(g.double().cpu().numpy() - eager["grads"][0]).max())
-    print(f"ZZ {what!r} grad err {err}")
+    print(f"ZZ {what!r} grad err {err} loss {float(loss.detach())} eager loss {float((eager['probs'] * gold['w']).sum())}")
+    loss2, g2 = gc(torch.tensor(x, device=cuda, dtype=torch.float32))
+    torch.cuda.synchronize()
+    print("ZZ replay 2 grad err", float(np.abs(g2.double().cpu().numpy() - eager["grads"][0]).max()), float(loss2.detach()))
+    gp = _graphed(cuda, x)
+    pr = gp(torch.tensor(x, device=cuda, dtype=torch.float32))
+    torch.cuda.synchronize()
+    print("ZZ no-loss graph probs err", float(np.abs(pr.double().cpu().numpy() - eager["probs"]).max()))
+    gc3 = _graphed(cuda, x, w=gold["w"])
+    l3, g3 = gc3(torch.tensor(x, device=cuda, dtype=torch.float32))
+    torch.cuda.synchronize()
+    print("ZZ second loss graph grad err", float(np.abs(g3.double().cpu().numpy() - eager["grads"][0]).max()), float(l3.detach()))
     assert err == 0.0
