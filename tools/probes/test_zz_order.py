@@ -41,7 +41,17 @@ def test_zz_order(cuda):
     eager = run_gpu(name, [x])
     if os.environ.get("ZZ_AFTER"):  # clear after the eager run, right before the capture
         PV._WORDS_CACHE.clear()
-    gc = _graphed(cuda, x, w=gold["w"])
+    wu = int(os.environ.get("ZZ_WARMUP", "3"))
+    if wu != 3:
+        import paper_2410_03348_b200 as sg
+        from paper_2410_03348_b200.programs import _chain_link, kinship_compose
+        import golden_cases as G
+        wt = torch.as_tensor(gold["w"], device=cuda)
+        gc = sg.GraphedClosure(kinship_compose, _chain_link, G.clutrr_facts(5), lambda: sg.DtkpAm(5),
+                               torch.tensor(x, device=cuda, dtype=torch.float32),
+                               loss_fn=lambda p: (p.double() * wt).sum(), warmup=wu)
+    else:
+        gc = _graphed(cuda, x, w=gold["w"])
     loss, g = gc(torch.tensor(x, device=cuda, dtype=torch.float32))
     torch.cuda.synchronize()
     err = float(np.abs(g.double().cpu().numpy() - eager["grads"][0]).max())
